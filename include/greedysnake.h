@@ -1,0 +1,177 @@
+/* greedysnake.h — C-ABI of the B200-native GreedySnake hot path
+ * (libgreedysnake.so, built in-tree by paper_2512_17570_b200/csrc/Makefile).
+ *
+ * Plain C types only: no torch, no C++ in the signatures.  Every function
+ * returns an int status (GS_OK = 0) and never throws; the message of the last
+ * failure on the calling thread is available from gs_last_error().  Status
+ * codes mirror the reference CLI's exit codes (proj/tools/offsim_main.cpp:
+ * 400-409): ValidationError -> 2, InfeasibleError -> 3, PlanBugError -> 1.
+ *
+ * Three layers:
+ *  1. plan      — the reference's scheduler API (proj/include/offsim/
+ *                 schedule.hpp:73-86, traffic.hpp:42-50, simulator.hpp:34)
+ *                 over opaque handles: build_vertical / build_horizontal,
+ *                 closed-form and plan-summed ledgers, the event simulator.
+ *  2. engine    — the real B200 executor that replaces simulate(): runs a plan
+ *                 with sm_100a kernels, PCIe DMA, NVMe I/O (offsim/executor.hpp).
+ *  3. kernels   — device-pointer entry points of the hot kernels, asynchronous
+ *                 on a caller stream (cudaStream_t passed as void*).
+ * See INTEGRATION.md for the bindings a reference maintainer would add.
+ */
+#ifndef GREEDYSNAKE_H
+#define GREEDYSNAKE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_OK 0
+#define GS_ERR_PLAN_BUG 1   /* offsim::PlanBugError / internal inconsistency */
+#define GS_ERR_VALIDATION 2 /* offsim::ValidationError: bad argument or config */
+#define GS_ERR_INFEASIBLE 3 /* offsim::InfeasibleError: memory / residency caps */
+#define GS_ERR_CUDA 4       /* CUDA runtime or launch failure */
+#define GS_ERR_RUNTIME 5    /* I/O and other runtime failures */
+
+const char* gs_last_error(void);
+const char* gs_version(void);
+
+/* ------------------------------------------------------------------ plan */
+/* offsim::ModelSpec (proj/include/offsim/model.hpp:11-23) */
+typedef struct gs_model_spec {
+  int num_layers, hidden_dim, num_heads, seq_len, microbatch_size;
+  int low_precision_bytes, full_precision_bytes, optimizer_states_per_element, data_parallel_degree;
+} gs_model_spec;
+
+/* offsim::StorageSplit (schedule.hpp:22-29): CPU-resident fractions */
+typedef struct gs_split {
+  double x_ckpt, x_param, x_opt;
+} gs_split;
+
+/* offsim::MachineSpec (machine.hpp:12-33) */
+typedef struct gs_machine_spec {
+  uint64_t gpu_mem_bytes, cpu_usable_dram_bytes;
+  double pcie_h2d_bw, pcie_d2h_bw, ssd_read_bw, ssd_write_bw;
+  double fwd_compute_time_per_layer_per_mb, bwd_compute_time_per_layer_per_mb;
+  double cpu_step_throughput, fixed_overhead_time;
+  int num_gpus;
+  uint64_t gpu_working_set_bytes;
+  int ssd_duplex;
+} gs_machine_spec;
+
+/* offsim::Task (schedule.hpp:41-56); kind/data/link numbered as the enums */
+typedef struct gs_task {
+  int id, kind, layer, microbatch, stage, data, link;
+  uint64_t bytes, elements;
+  int cross_iter_dep, num_deps;
+} gs_task;
+
+typedef struct gs_plan gs_plan; /* opaque offsim::SchedulePlan */
+
+/* build_vertical(model, M, split, alpha)   schedule.hpp:79-80 */
+int gs_plan_build_vertical(const gs_model_spec* model, int num_microbatches, const gs_split* split, double alpha,
+                           gs_plan** out);
+/* build_horizontal(model, M, split)        schedule.hpp:73-74 */
+int gs_plan_build_horizontal(const gs_model_spec* model, int num_microbatches, const gs_split* split, gs_plan** out);
+/* plan_from_json(json)                     json_io.hpp:29 */
+int gs_plan_from_json(const char* json, gs_plan** out);
+void gs_plan_free(gs_plan* plan);
+int gs_plan_num_tasks(const gs_plan* plan);
+int gs_plan_task(const gs_plan* plan, int index, gs_task* out);
+/* deps of task `index` into out[0..cap) ; *n = number of deps */
+int gs_plan_task_deps(const gs_plan* plan, int index, int* out, int cap, int* n);
+/* plan_to_json(plan).dump() into buf (NUL-terminated); *len = bytes needed */
+int gs_plan_to_json(const gs_plan* plan, char* buf, size_t cap, size_t* len);
+/* ledger[link*5 + data], links H2D,D2H,SSD_read,SSD_write; data param,ckpt,
+   grad_accum,interlayer_grad,opt_state   (traffic.hpp:14-36) */
+int gs_plan_traffic(const gs_plan* plan, uint64_t ledger[20]);
+int gs_vertical_traffic(const gs_model_spec* model, int num_microbatches, const gs_split* split, double alpha,
+                        uint64_t ledger[20]);
+int gs_horizontal_traffic(const gs_model_spec* model, int num_microbatches, const gs_split* split,
+                          uint64_t ledger[20]);
+int64_t gs_plan_overlap_window(const gs_plan* plan);
+/* report_to_json(simulate(plan, machine)).dump()   simulator.hpp:34 */
+int gs_simulate_json(const gs_plan* plan, const gs_machine_spec* machine, char* buf, size_t cap, size_t* len);
+
+/* ---------------------------------------------------------------- engine */
+typedef struct gs_engine_config {
+  gs_model_spec model;     /* low_precision_bytes: 2 = bf16 training, 4 = fp32 parity mode */
+  int vocab_size;          /* tied embedding / LM head (FixedOps) */
+  float lr, beta1, beta2, eps, weight_decay;
+  uint64_t seed;
+  int device;
+  const char* nvme_dir;    /* directory for the NVMe tier file (NULL -> "/tmp") */
+  int odirect;             /* 1: O_DIRECT on the NVMe tier */
+  int opt_tier;            /* 0 auto, 1 HBM, 2 pinned host */
+  int record_trace;
+} gs_engine_config;
+
+typedef struct gs_run_report {
+  double total_ms;          /* CUDA-event time of the whole run */
+  int iterations;
+  int gpu_launches;         /* kernels launched during the run */
+  uint64_t ledger[20];      /* logical bytes of the last iteration (== gs_plan_traffic) */
+  uint64_t extension[20];   /* GPU-optimizer traffic outside the reference model */
+  uint64_t physical[20];    /* bytes physically moved (NVMe rounded to 4 KiB) */
+  uint64_t gpu_bytes, host_pinned_bytes;
+} gs_run_report;
+
+typedef struct gs_trace_record {
+  int iteration, task, resource;
+  double t_start_ms, t_end_ms;
+  uint64_t bytes, physical_bytes;
+} gs_trace_record;
+
+typedef struct gs_engine gs_engine; /* opaque offsim::Executor */
+
+/* Executor(plan, cfg): allocates HBM / pinned DRAM / NVMe state, initialises
+   weights from cfg->seed.  The plan may be freed afterwards. */
+int gs_engine_create(const gs_plan* plan, const gs_engine_config* cfg, gs_engine** out);
+void gs_engine_destroy(gs_engine* engine);
+/* Runs `iterations` chained iterations.  tokens: int32 [iterations][M][b][s+1]
+   in host memory (tokens_on_device = 0) or device memory (= 1).
+   losses (optional): per-iteration mean cross-entropy. */
+int gs_engine_run(gs_engine* engine, int iterations, const int32_t* tokens, int tokens_on_device, double* losses,
+                  gs_run_report* report);
+/* apply the pending alpha slice + embedding step */
+int gs_engine_flush(gs_engine* engine);
+/* fp32 master weights: layers [N][12 h^2], fixed [(V + s) h]; either may be NULL */
+int gs_engine_read_params(gs_engine* engine, float* layers, float* fixed);
+int gs_engine_read_moments(gs_engine* engine, float* layer_m, float* layer_v);
+/* trace of the last run (last <= 3 iterations when record_trace was set) */
+int gs_engine_trace(gs_engine* engine, gs_trace_record* out, int cap, int* n);
+
+/* --------------------------------------------------------------- kernels */
+/* dtype: 0 = fp32, 1 = bf16.  stream: cudaStream_t (NULL = legacy default). */
+/* C[M,N] = sum_k A(m,k) B(n,k);  a_kmajor: A is [M][K] else [K][M];
+   b_kmajor: B is [N][K] else [K][N].  epi: 0 store, 1 store + residual R,
+   2 fp32 accumulate (C fp32), 3 store + gelu to G, 4 fp32 store. */
+int gs_gemm(int dtype, int M, int N, int K, const void* A, int a_kmajor, const void* B, int b_kmajor, void* C,
+            const void* R, void* G, int epi, void* stream);
+/* same, forcing the CUDA-core path (reference for the tcgen05 path) */
+int gs_gemm_simt(int dtype, int M, int N, int K, const void* A, int a_kmajor, const void* B, int b_kmajor, void* C,
+                 const void* R, void* G, int epi, void* stream);
+int gs_attention_fwd(int dtype, const void* qkv, void* o, float* lse, int b, int s, int h, int heads, void* stream);
+size_t gs_attention_bwd_workspace(int b, int s, int h, int heads);
+int gs_attention_bwd(int dtype, const void* qkv, const void* o, const float* lse, const void* dout, void* dqkv,
+                     void* workspace, int b, int s, int h, int heads, void* stream);
+int gs_layernorm_fwd(int dtype, const void* x, void* y, float* mean, float* rstd, int rows, int h, void* stream);
+int gs_layernorm_bwd(int dtype, const void* x, const float* mean, const float* rstd, const void* dy, void* dx,
+                     int rows, int h, int accumulate, void* stream);
+/* fused Adam(W) on packed [master, m, v] fp32 state (12 B/elem); writes the
+   low-precision working copy to param_lp (dtype) when non-NULL */
+int gs_adam_step_packed(float lr, float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale,
+                        float* state, const float* grad, void* param_lp, int lp_dtype, int64_t n, void* stream);
+/* one layer forward / recompute+backward (the plan's FwdCompute / RecomputeAndBwd) */
+int gs_layer_forward(int dtype, int b, int s, int h, int heads, const void* W, const void* x, void* y, void* stream);
+int gs_layer_backward(int dtype, int b, int s, int h, int heads, const void* W, const void* x, const void* dy,
+                      void* dx, float* dW, int first, void* stream);
+/* number of device kernels launched through this library so far */
+int64_t gs_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,113 @@
+// The B200 executor: runs a SchedulePlan for real.
+//
+// This is the slot the reference fills with its discrete-event model
+// (`SimReport simulate(const SchedulePlan&, const MachineSpec&)`,
+// proj/include/offsim/simulator.hpp:34).  Every plan task is executed on the
+// resource simulate() would charge it to, in the same per-resource order
+// (proj/src/simulator.cpp:117-122):
+//
+//   GPU    FwdCompute / RecomputeAndBwd / FixedOps -> compute CUDA stream
+//   H2D    Xfer PCIe_H2D                           -> copy stream (pinned DRAM -> HBM)
+//   D2H    Xfer PCIe_D2H                           -> copy stream (HBM -> pinned DRAM)
+//   CPU    CpuStep                                 -> optimizer stream: fused Adam on
+//                                                     the GPU, state streamed through HBM
+//   SSD_R  Xfer SSD_Read                           -> NVMe file reads (O_DIRECT, thread pool)
+//   SSD_W  Xfer SSD_Write                          -> NVMe file writes
+//
+// Cross-resource dependencies become CUDA events / host completions; the
+// plan's cross_iter_dep edges chain consecutive iterations, so the alpha
+// slice of iteration i's optimizer step overlaps iteration i+1's forward.
+// The trace (task, resource, start, end, bytes) of every executed task sums
+// to plan_traffic(plan) exactly; transfers the GPU optimizer adds on top of
+// the reference model are reported in a separate extension ledger.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "offsim/offsim.hpp"
+
+namespace offsim {
+
+enum class OptTier {
+  Auto = 0,  // CPU-resident optimizer fraction in HBM when it fits, else pinned DRAM
+  Hbm = 1,   // CPU-resident fraction kept in HBM (B200: 180 GB)
+  Host = 2,  // CPU-resident fraction in pinned DRAM, streamed through HBM per step
+};
+
+struct AdamConfig {
+  float lr = 1e-3f, beta1 = 0.9f, beta2 = 0.95f, eps = 1e-8f, weight_decay = 0.0f;
+};
+
+struct ExecConfig {
+  ModelSpec model;          // geometry; low_precision_bytes 2 = bf16, 4 = fp32 parity mode
+  int vocab_size = 50304;   // embedding / tied LM head (FixedOps), off the ledger
+  AdamConfig adam;
+  uint64_t seed = 42;       // weight init (N(0,0.02), out-proj / sqrt(2N))
+  int device = 0;
+  std::string nvme_dir = "/tmp";  // directory of the NVMe tier file
+  bool odirect = true;
+  OptTier opt_tier = OptTier::Auto;
+  bool record_trace = false;   // per-task timestamps (adds event records)
+  int rank = 0, world = 1;     // data parallel (model.data_parallel_degree == world)
+};
+
+struct TraceRecord {
+  int iteration;
+  int task;
+  Resource resource;
+  double t_start_ms, t_end_ms;  // relative to the run start (GPU tasks: CUDA events)
+  u64 bytes;                    // logical bytes (the plan's)
+  u64 physical_bytes;           // bytes actually moved (NVMe rounds to 4 KiB)
+};
+
+struct ExecReport {
+  // measured, per iteration
+  std::vector<double> losses;
+  std::vector<double> iteration_ms;   // end-to-end time of each iteration (GPU clock)
+  double total_ms = 0.0;              // whole run, CUDA events
+  TrafficLedger ledger;               // logical bytes moved in the LAST iteration (== plan_traffic)
+  TrafficLedger extension;            // GPU-optimizer traffic outside the reference model
+  TrafficLedger physical;             // bytes physically moved in the last iteration
+  u64 gpu_bytes_allocated = 0;
+  u64 host_pinned_bytes = 0;
+  int gpu_launches = 0;               // kernels launched by the run (all iterations)
+  std::vector<TraceRecord> trace;     // when record_trace
+};
+
+class Executor {
+ public:
+  // Builds device / host / NVMe state for `plan` (weights initialised from
+  // cfg.seed; optimizer state zero).  Throws ValidationError / InfeasibleError.
+  Executor(const SchedulePlan& plan, const ExecConfig& cfg);
+  ~Executor();
+  Executor(const Executor&) = delete;
+  Executor& operator=(const Executor&) = delete;
+
+  // Runs `iterations` chained iterations of the plan.  tokens: host (or
+  // device, if tokens_on_device) int32 [iterations][M][b][s+1].
+  ExecReport run(int iterations, const int32_t* tokens, bool tokens_on_device = false);
+  // Applies the pending alpha slice of the last iteration's step and the
+  // pending embedding step ("flush"); idempotent.
+  void flush();
+  // fp32 master weights: layers [N][12h^2], fixed [(V+s)*h] (wte then wpe).
+  void read_params(float* layers, float* fixed);
+  // fp32 optimizer moments, same layout as read_params.
+  void read_moments(float* layer_m, float* layer_v);
+
+  const SchedulePlan& plan() const;
+  const ExecConfig& config() const;
+
+  struct Impl;
+
+ private:
+  std::unique_ptr<Impl> impl_;
+};
+
+// One-call form mirroring simulate(plan, machine).
+ExecReport execute(const SchedulePlan& plan, const ExecConfig& cfg, int iterations,
+                   const int32_t* tokens);
+
+}  // namespace offsim

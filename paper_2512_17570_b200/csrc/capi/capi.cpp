@@ -1,0 +1,337 @@
+// extern "C" boundary of libgreedysnake.so (declared in include/greedysnake.h).
+// Converts exceptions to status codes (the reference CLI's exit-code
+// convention, proj/tools/offsim_main.cpp:400-409) and keeps the last error
+// message per thread.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "greedysnake.h"
+#include "kernels.h"
+#include "layer_ops.hpp"
+#include "offsim/executor.hpp"
+#include "offsim/json_io.hpp"
+
+struct gs_plan {
+  offsim::SchedulePlan plan;
+};
+struct gs_engine {
+  std::unique_ptr<offsim::Executor> ex;
+  std::vector<offsim::TraceRecord> trace;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return GS_OK;
+  } catch (const offsim::ValidationError& e) {
+    g_error = e.what();
+    return GS_ERR_VALIDATION;
+  } catch (const offsim::InfeasibleError& e) {
+    g_error = e.what();
+    return GS_ERR_INFEASIBLE;
+  } catch (const offsim::PlanBugError& e) {
+    g_error = e.what();
+    return GS_ERR_PLAN_BUG;
+  } catch (const std::bad_alloc&) {
+    g_error = "out of host memory";
+    return GS_ERR_INFEASIBLE;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return std::strstr(e.what(), "CUDA") ? GS_ERR_CUDA : GS_ERR_RUNTIME;
+  }
+}
+
+int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return GS_OK;
+  g_error = std::string("CUDA: ") + cudaGetErrorString(e);
+  return GS_ERR_CUDA;
+}
+
+offsim::ModelSpec model_of(const gs_model_spec* m) {
+  if (!m) throw offsim::ValidationError("model spec is NULL");
+  offsim::ModelSpec s;
+  s.num_layers = m->num_layers;
+  s.hidden_dim = m->hidden_dim;
+  s.num_heads = m->num_heads;
+  s.seq_len = m->seq_len;
+  s.microbatch_size = m->microbatch_size;
+  s.low_precision_bytes = m->low_precision_bytes;
+  s.full_precision_bytes = m->full_precision_bytes;
+  s.optimizer_states_per_element = m->optimizer_states_per_element;
+  s.data_parallel_degree = m->data_parallel_degree;
+  return s;
+}
+offsim::StorageSplit split_of(const gs_split* x) {
+  if (!x) throw offsim::ValidationError("split is NULL");
+  offsim::StorageSplit s;
+  s.x_ckpt = x->x_ckpt;
+  s.x_param = x->x_param;
+  s.x_opt = x->x_opt;
+  return s;
+}
+void ledger_out(const offsim::TrafficLedger& t, uint64_t* out) {
+  for (int l = 0; l < 4; ++l)
+    for (int d = 0; d < 5; ++d) out[l * 5 + d] = t.bytes[static_cast<size_t>(l)][static_cast<size_t>(d)];
+}
+int copy_string(const std::string& s, char* buf, size_t cap, size_t* len) {
+  if (len) *len = s.size() + 1;
+  if (!buf || cap < s.size() + 1) {
+    g_error = "buffer too small";
+    return buf ? GS_ERR_VALIDATION : GS_OK;
+  }
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return GS_OK;
+}
+gs::DType dt_of(int dtype) { return dtype == 0 ? gs::DType::F32 : gs::DType::BF16; }
+
+}  // namespace
+
+namespace gs {
+long long& launch_counter_ref();
+}
+
+extern "C" {
+
+const char* gs_last_error(void) { return g_error.c_str(); }
+const char* gs_version(void) { return "greedysnake-b200 0.1 (sm_100a)"; }
+
+int gs_plan_build_vertical(const gs_model_spec* model, int mbs, const gs_split* split, double alpha, gs_plan** out) {
+  return guarded([&] {
+    auto p = std::make_unique<gs_plan>();
+    p->plan = offsim::build_vertical(model_of(model), mbs, split_of(split), alpha);
+    *out = p.release();
+  });
+}
+int gs_plan_build_horizontal(const gs_model_spec* model, int mbs, const gs_split* split, gs_plan** out) {
+  return guarded([&] {
+    auto p = std::make_unique<gs_plan>();
+    p->plan = offsim::build_horizontal(model_of(model), mbs, split_of(split));
+    *out = p.release();
+  });
+}
+int gs_plan_from_json(const char* json, gs_plan** out) {
+  return guarded([&] {
+    offsim::Json j;
+    try {
+      j = offsim::Json::parse(json ? json : "");
+    } catch (const std::exception& e) {
+      throw offsim::ValidationError(std::string("malformed plan JSON: ") + e.what());
+    }
+    auto p = std::make_unique<gs_plan>();
+    p->plan = offsim::plan_from_json(j);
+    *out = p.release();
+  });
+}
+void gs_plan_free(gs_plan* plan) { delete plan; }
+int gs_plan_num_tasks(const gs_plan* plan) { return plan ? static_cast<int>(plan->plan.tasks.size()) : -1; }
+int gs_plan_task(const gs_plan* plan, int index, gs_task* out) {
+  return guarded([&] {
+    if (!plan || index < 0 || index >= static_cast<int>(plan->plan.tasks.size()))
+      throw offsim::ValidationError("task index out of range");
+    const offsim::Task& t = plan->plan.tasks[static_cast<size_t>(index)];
+    out->id = t.id;
+    out->kind = static_cast<int>(t.kind);
+    out->layer = t.layer;
+    out->microbatch = t.microbatch;
+    out->stage = t.stage;
+    out->data = static_cast<int>(t.data);
+    out->link = static_cast<int>(t.link);
+    out->bytes = t.bytes;
+    out->elements = t.elements;
+    out->cross_iter_dep = t.cross_iter_dep;
+    out->num_deps = static_cast<int>(t.deps.size());
+  });
+}
+int gs_plan_task_deps(const gs_plan* plan, int index, int* out, int cap, int* n) {
+  return guarded([&] {
+    if (!plan || index < 0 || index >= static_cast<int>(plan->plan.tasks.size()))
+      throw offsim::ValidationError("task index out of range");
+    const auto& deps = plan->plan.tasks[static_cast<size_t>(index)].deps;
+    *n = static_cast<int>(deps.size());
+    for (int i = 0; i < cap && i < *n; ++i) out[i] = deps[static_cast<size_t>(i)];
+  });
+}
+int gs_plan_to_json(const gs_plan* plan, char* buf, size_t cap, size_t* len) {
+  int rc = GS_OK;
+  const int g = guarded([&] { rc = copy_string(offsim::plan_to_json(plan->plan).dump(), buf, cap, len); });
+  return g != GS_OK ? g : rc;
+}
+int gs_plan_traffic(const gs_plan* plan, uint64_t ledger[20]) {
+  return guarded([&] { ledger_out(offsim::plan_traffic(plan->plan), ledger); });
+}
+int gs_vertical_traffic(const gs_model_spec* model, int mbs, const gs_split* split, double alpha, uint64_t ledger[20]) {
+  return guarded([&] { ledger_out(offsim::vertical_traffic(model_of(model), mbs, split_of(split), alpha), ledger); });
+}
+int gs_horizontal_traffic(const gs_model_spec* model, int mbs, const gs_split* split, uint64_t ledger[20]) {
+  return guarded([&] { ledger_out(offsim::horizontal_traffic(model_of(model), mbs, split_of(split)), ledger); });
+}
+int64_t gs_plan_overlap_window(const gs_plan* plan) { return plan ? offsim::overlap_window(plan->plan) : -1; }
+int gs_simulate_json(const gs_plan* plan, const gs_machine_spec* m, char* buf, size_t cap, size_t* len) {
+  int rc = GS_OK;
+  const int g = guarded([&] {
+    offsim::MachineSpec mc;
+    mc.gpu_mem_bytes = m->gpu_mem_bytes;
+    mc.cpu_usable_dram_bytes = m->cpu_usable_dram_bytes;
+    mc.pcie_h2d_bw = m->pcie_h2d_bw;
+    mc.pcie_d2h_bw = m->pcie_d2h_bw;
+    mc.ssd_read_bw = m->ssd_read_bw;
+    mc.ssd_write_bw = m->ssd_write_bw;
+    mc.fwd_compute_time_per_layer_per_mb = m->fwd_compute_time_per_layer_per_mb;
+    mc.bwd_compute_time_per_layer_per_mb = m->bwd_compute_time_per_layer_per_mb;
+    mc.cpu_step_throughput = m->cpu_step_throughput;
+    mc.fixed_overhead_time = m->fixed_overhead_time;
+    mc.num_gpus = m->num_gpus;
+    mc.gpu_working_set_bytes = m->gpu_working_set_bytes;
+    mc.ssd_duplex = m->ssd_duplex != 0;
+    rc = copy_string(offsim::report_to_json(offsim::simulate(plan->plan, mc)).dump(), buf, cap, len);
+  });
+  return g != GS_OK ? g : rc;
+}
+
+// ------------------------------------------------------------------ engine
+int gs_engine_create(const gs_plan* plan, const gs_engine_config* c, gs_engine** out) {
+  return guarded([&] {
+    if (!plan || !c || !out) throw offsim::ValidationError("engine: NULL argument");
+    offsim::ExecConfig cfg;
+    cfg.model = model_of(&c->model);
+    cfg.vocab_size = c->vocab_size;
+    cfg.adam = {c->lr, c->beta1, c->beta2, c->eps, c->weight_decay};
+    cfg.seed = c->seed;
+    cfg.device = c->device;
+    cfg.nvme_dir = c->nvme_dir ? c->nvme_dir : "/tmp";
+    cfg.odirect = c->odirect != 0;
+    cfg.opt_tier = static_cast<offsim::OptTier>(c->opt_tier);
+    cfg.record_trace = c->record_trace != 0;
+    auto e = std::make_unique<gs_engine>();
+    e->ex = std::make_unique<offsim::Executor>(plan->plan, cfg);
+    *out = e.release();
+  });
+}
+void gs_engine_destroy(gs_engine* engine) { delete engine; }
+int gs_engine_run(gs_engine* engine, int iterations, const int32_t* tokens, int tokens_on_device, double* losses,
+                  gs_run_report* report) {
+  return guarded([&] {
+    if (!engine) throw offsim::ValidationError("engine is NULL");
+    const long long before = gs::launch_counter_ref();
+    offsim::ExecReport r = engine->ex->run(iterations, tokens, tokens_on_device != 0);
+    if (losses)
+      for (int i = 0; i < iterations; ++i) losses[i] = r.losses[static_cast<size_t>(i)];
+    engine->trace = r.trace;
+    if (report) {
+      report->total_ms = r.total_ms;
+      report->iterations = iterations;
+      report->gpu_launches = static_cast<int>(gs::launch_counter_ref() - before);
+      ledger_out(r.ledger, report->ledger);
+      ledger_out(r.extension, report->extension);
+      ledger_out(r.physical, report->physical);
+      report->gpu_bytes = r.gpu_bytes_allocated;
+      report->host_pinned_bytes = r.host_pinned_bytes;
+    }
+  });
+}
+int gs_engine_flush(gs_engine* engine) { return guarded([&] { engine->ex->flush(); }); }
+int gs_engine_read_params(gs_engine* engine, float* layers, float* fixed) {
+  return guarded([&] { engine->ex->read_params(layers, fixed); });
+}
+int gs_engine_read_moments(gs_engine* engine, float* m, float* v) {
+  return guarded([&] { engine->ex->read_moments(m, v); });
+}
+int gs_engine_trace(gs_engine* engine, gs_trace_record* out, int cap, int* n) {
+  return guarded([&] {
+    *n = static_cast<int>(engine->trace.size());
+    for (int i = 0; i < cap && i < *n; ++i) {
+      const offsim::TraceRecord& r = engine->trace[static_cast<size_t>(i)];
+      out[i] = {r.iteration, r.task, static_cast<int>(r.resource), r.t_start_ms, r.t_end_ms, r.bytes, r.physical_bytes};
+    }
+  });
+}
+
+// ----------------------------------------------------------------- kernels
+static int gemm_common(bool simt, int dtype, int M, int N, int K, const void* A, int a_k, const void* B, int b_k,
+                       void* C, const void* R, void* G, int epi, void* stream) {
+  gs::GemmArgs g;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.A = A;
+  g.B = B;
+  g.a_kmajor = a_k != 0;
+  g.b_kmajor = b_k != 0;
+  g.C = C;
+  g.R = R;
+  g.G = G;
+  g.epi = static_cast<gs::Epi>(epi);
+  g.dt = dt_of(dtype);
+  return cuda_status(simt ? gs::gemm_simt(g, static_cast<cudaStream_t>(stream))
+                          : gs::gemm(g, static_cast<cudaStream_t>(stream)));
+}
+int gs_gemm(int dtype, int M, int N, int K, const void* A, int a_k, const void* B, int b_k, void* C, const void* R,
+            void* G, int epi, void* stream) {
+  return gemm_common(false, dtype, M, N, K, A, a_k, B, b_k, C, R, G, epi, stream);
+}
+int gs_gemm_simt(int dtype, int M, int N, int K, const void* A, int a_k, const void* B, int b_k, void* C,
+                 const void* R, void* G, int epi, void* stream) {
+  return gemm_common(true, dtype, M, N, K, A, a_k, B, b_k, C, R, G, epi, stream);
+}
+int gs_attention_fwd(int dtype, const void* qkv, void* o, float* lse, int b, int s, int h, int heads, void* stream) {
+  return cuda_status(gs::attention_fwd(dt_of(dtype), qkv, o, lse, b, s, h, heads, static_cast<cudaStream_t>(stream)));
+}
+size_t gs_attention_bwd_workspace(int b, int s, int h, int heads) { return gs::attention_bwd_workspace(b, s, h, heads); }
+int gs_attention_bwd(int dtype, const void* qkv, const void* o, const float* lse, const void* dout, void* dqkv,
+                     void* work, int b, int s, int h, int heads, void* stream) {
+  return cuda_status(gs::attention_bwd(dt_of(dtype), qkv, o, lse, dout, dqkv, work, b, s, h, heads,
+                                       static_cast<cudaStream_t>(stream)));
+}
+int gs_layernorm_fwd(int dtype, const void* x, void* y, float* mean, float* rstd, int rows, int h, void* stream) {
+  return cuda_status(gs::layernorm_fwd(dt_of(dtype), x, y, mean, rstd, rows, h, static_cast<cudaStream_t>(stream)));
+}
+int gs_layernorm_bwd(int dtype, const void* x, const float* mean, const float* rstd, const void* dy, void* dx,
+                     int rows, int h, int accumulate, void* stream) {
+  return cuda_status(gs::layernorm_bwd(dt_of(dtype), x, mean, rstd, dy, dx, rows, h, accumulate != 0,
+                                       static_cast<cudaStream_t>(stream)));
+}
+int gs_adam_step_packed(float lr, float beta1, float beta2, float eps, float wd, int step, float grad_scale,
+                        float* state, const float* grad, void* param_lp, int lp_dtype, int64_t n, void* stream) {
+  gs::AdamHyper hp{lr, beta1, beta2, eps, wd};
+  return cuda_status(gs::adam_step_packed(hp, step, grad_scale, state, grad, param_lp, dt_of(lp_dtype), n,
+                                          static_cast<cudaStream_t>(stream)));
+}
+static int layer_call(int dtype, int b, int s, int h, int heads, bool fwd, const void* W, const void* x,
+                      const void* dy, void* out, float* dW, int first, void* stream) {
+  gs::engine::Dims d;
+  d.b = b;
+  d.s = s;
+  d.h = h;
+  d.H = heads;
+  d.V = 128;  // head unused here
+  d.dt = dt_of(dtype);
+  gs::engine::Workspace ws;
+  if (!gs::engine::alloc_workspace(d, ws)) return cuda_status(cudaErrorMemoryAllocation);
+  gs::engine::LaunchCounter lc;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = fwd ? gs::engine::layer_forward(d, W, x, out, ws, st, lc)
+                      : gs::engine::layer_backward(d, W, x, dy, out, dW, first != 0, nullptr, ws, st, lc);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  gs::engine::free_workspace(ws);
+  return cuda_status(e);
+}
+int gs_layer_forward(int dtype, int b, int s, int h, int heads, const void* W, const void* x, void* y, void* stream) {
+  return layer_call(dtype, b, s, h, heads, true, W, x, nullptr, y, nullptr, 0, stream);
+}
+int gs_layer_backward(int dtype, int b, int s, int h, int heads, const void* W, const void* x, const void* dy,
+                      void* dx, float* dW, int first, void* stream) {
+  return layer_call(dtype, b, s, h, heads, false, W, x, dy, dx, dW, first, stream);
+}
+int64_t gs_launch_count(void) { return gs::launch_counter_ref(); }
+
+}  // extern "C"

@@ -1,0 +1,1203 @@
+// The B200 executor (offsim/executor.hpp): runs a vertical (snake) or
+// horizontal plan with real kernels, real PCIe DMA and real NVMe I/O.
+//
+// Structure
+//  * One dispatcher thread per plan resource (GPU, CPU, H2D, D2H, SSD_R,
+//    SSD_W), each walking its tasks in plan order, iteration after iteration
+//    (the in-order discipline of proj/src/simulator.cpp:108-126).
+//  * Stream-backed resources record a CUDA event per task instance; a
+//    dependency on another stream task is a cudaStreamWaitEvent, on a host
+//    task a host wait.  cross_iter_dep edges bind to the previous iteration.
+//  * Buffer reuse hazards the plan leaves implicit (parity-indexed HBM
+//    staging slots, the gradient ring, NVMe read staging) are derived once by
+//    a WAR/WAW pass over two unrolled iterations and added as extra edges
+//    pointing backwards in (iteration, plan id) order, so no deadlock is
+//    possible.
+//  * Each data kind lives in a "blob" cut into segments by the split's byte
+//    boundaries (types.hpp:35-53 rounding) and by the immediate/delayed
+//    element boundary; SSD segments have a pinned image (authoritative copy /
+//    CPU double buffer), a pinned read-staging buffer and a 4 KiB-aligned
+//    region of the NVMe file.  Reads that the plan routes through the SSD
+//    are served from the read staging, so every SSD byte really round-trips.
+#include "offsim/executor.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
+#include <sstream>
+#include <thread>
+
+#include "host_tiers.hpp"
+#include "kernels.h"
+#include "layer_ops.hpp"
+
+namespace offsim {
+
+using gs::DType;
+using namespace gs::engine;
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------ weight init
+// Bit-identical to oracle/gs_oracle.c (gso_splitmix64 / gso_normal /
+// gso_init_layer / gso_init_fixed).
+uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+double normal_at(uint64_t key, uint64_t i) {
+  const uint64_t a = splitmix64(key + 2 * i), b = splitmix64(key + 2 * i + 1);
+  const double u1 = static_cast<double>((a >> 11) + 1) * 0x1.0p-53;
+  const double u2 = static_cast<double>(b >> 11) * 0x1.0p-53;
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+}
+uint64_t stream_key(uint64_t seed, uint64_t stream) {
+  return splitmix64(seed ^ splitmix64(stream + 0x632BE59BD9B4E019ull));
+}
+template <typename F>
+void parallel_for(long long n, F&& f) {
+  const int nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  if (n < (1 << 16) || nt == 1) {
+    f(0LL, n);
+    return;
+  }
+  std::vector<std::thread> ts;
+  const long long per = (n + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    const long long lo = t * per, hi = std::min(n, lo + per);
+    if (lo < hi) ts.emplace_back([&f, lo, hi] { f(lo, hi); });
+  }
+  for (auto& t : ts) t.join();
+}
+
+uint16_t f32_to_bf16(float f) {  // round to nearest even (finite inputs)
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7FFF + ((u >> 16) & 1);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+// ------------------------------------------------------------ tiers
+enum class Tier { Dram, Ssd, Hbm };
+struct Segment {
+  u64 lo = 0, hi = 0;  // logical byte range within the blob
+  Tier tier = Tier::Dram;
+  uint8_t* img = nullptr;  // pinned image (Dram / Ssd)
+  uint8_t* rd = nullptr;   // pinned NVMe read staging (Ssd)
+  uint8_t* dev = nullptr;  // HBM (Hbm)
+  u64 file_off = 0;        // NVMe region (Ssd)
+  u64 size() const { return hi - lo; }
+};
+struct Blob {
+  u64 size = 0;
+  std::vector<Segment> segs;
+};
+
+// Source selection for an upload of a blob range.
+enum class Src { Image, ReadStaging, Auto };
+
+// ------------------------------------------------------------ hazards
+struct ExtraDep {
+  int task;
+  int offset;  // 0 = same iteration, -1 = previous
+};
+
+}  // namespace
+
+// =========================================================================
+struct Executor::Impl {
+  SchedulePlan plan;
+  ExecConfig cfg;
+  Dims d;
+  int N = 0, M = 0;
+  u64 P = 0, pb = 0, cb = 0;
+  u64 el_now = 0, el_late = 0;
+  bool horizontal = false;
+  int grad_ring = 3;
+
+  // streams
+  cudaStream_t s_gpu = nullptr, s_h2d = nullptr, s_d2h = nullptr, s_opt = nullptr;
+
+  // device state
+  std::vector<void*> dev_allocs;
+  u64 dev_bytes = 0;
+  void* dev_param[2] = {nullptr, nullptr};
+  std::vector<float*> grad_slot;
+  std::vector<float*> retain;  // [N] el_late floats
+  float *fx_master = nullptr, *fx_m = nullptr, *fx_v = nullptr, *fx_grad = nullptr;
+  void* fx_lp = nullptr;
+  long long n_fixed = 0;
+  Workspace ws;
+  std::vector<void*> in_x, out_y, in_g, out_g;  // [2*M] each, index p*M+m
+  int32_t* dev_tok[2] = {nullptr, nullptr};
+  double* dev_loss = nullptr;  // [loss_cap] per run iteration
+  int loss_cap = 0;
+  float* opt_stage = nullptr;  // 12 * chunk floats
+  void* lp_stage = nullptr;    // chunk lp elements
+  long long chunk = 0;
+
+  // host state
+  PinnedArena arena;
+  std::unique_ptr<NvmeFile> nvme;
+  std::vector<Blob> param_blob, opt_blob;  // [N]
+  std::vector<Blob> ckpt_blob;             // [N*M]
+  std::vector<uint8_t*> host_grad;         // [N]
+  std::vector<uint8_t*> host_ilg;          // [2*M]
+  int32_t* tok_pinned = nullptr;
+  long long tok_capacity = 0;
+
+  // task bookkeeping
+  std::vector<Resource> res_of;
+  std::vector<std::vector<int>> queue;  // per resource, task ids in plan order
+  std::vector<std::vector<ExtraDep>> extra;
+  std::vector<char> is_stream;          // task completes via CUDA event
+  std::vector<char> fwd_phase;          // emitted before the first RecomputeAndBwd
+  std::vector<u64> chunk_lo;            // param H2D: byte offset of the chunk
+  std::vector<std::array<cudaEvent_t, 3>> ev_done;
+  std::vector<std::array<cudaEvent_t, 3>> ev_start;  // trace mode
+  std::vector<std::atomic<int>> done_iter;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::array<std::atomic<int>, kNumResources> finished{};
+  std::atomic<bool> failed{false};
+  std::string error;
+
+  // run state
+  long long global_iter = 0;  // iterations completed before this run
+  long long fixed_done = 0;   // embedding grads of iterations < fixed_done are applied
+  // per layer: global iteration whose alpha-slice grads are retained / applied
+  std::unique_ptr<std::atomic<long long>[]> late_ready, late_applied;
+  const int32_t* run_tokens = nullptr;
+  bool run_tokens_dev = false;
+  std::atomic<int> launches{0};
+  // ledgers (last iteration)
+  TrafficLedger led_logical, led_ext, led_phys;
+  std::mutex led_mu;
+  int last_iter = -1;
+  std::vector<TraceRecord> trace;
+  std::mutex trace_mu;
+  std::chrono::steady_clock::time_point host_base;
+  cudaEvent_t ev_base = nullptr;
+
+  // ------------------------------------------------------------ setup
+  Impl(const SchedulePlan& p, const ExecConfig& c);
+  ~Impl();
+  void* dmalloc(u64 bytes);
+  Blob make_blob(u64 size, std::vector<u64> cuts, u64 cpu_bytes, bool hbm_for_cpu);
+  void init_weights();
+  void build_tasks();
+  void hazards();
+
+  // ------------------------------------------------------------ data movement
+  u64 upload(const Blob& b, u64 lo, u64 hi, void* dst, Src src, cudaStream_t st, u64 delayed_lo);
+  u64 download(Blob& b, u64 lo, u64 hi, const void* src, cudaStream_t st);
+  u64 ssd_io(Blob& b, u64 lo, u64 hi, bool write);
+
+  // ------------------------------------------------------------ execution
+  void dispatch(Resource r, int iterations);
+  void wait_dep(int dep, int iter, bool on_stream, cudaStream_t st);
+  void run_task(int t, int it);
+  void compute_task(const Task& t, int it);
+  void step_task(const Task& t, int it);
+  void xfer_task(const Task& t, int it, u64& phys);
+  cudaStream_t stream_of(Resource r) const;
+  int first_mb(int st) const { return st % 2 == 0 ? 0 : M - 1; }
+  int last_mb(int st) const { return st % 2 == 0 ? M - 1 : 0; }
+  // forward-phase optimizer work (CpuStep, OptState I/O, Param SSD write) is
+  // the delayed alpha slice of the previous iteration's step
+  bool delayed(const Task& t) const { return fwd_phase[static_cast<size_t>(t.id)] != 0; }
+  void apply_adam(int layer, u64 e0, u64 e1, const float* grad, int step, cudaStream_t st, int it);
+  void note_ledger(int it, const Task& t, u64 phys);
+  void note_ext(int it, LinkKind l, DataKind dk, u64 bytes);
+};
+
+// =========================================================================
+Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(c) {
+  check_plan(plan);
+  const ModelSpec& ms = cfg.model;
+  ms.validate();
+  if (plan.kind.variant == ScheduleVariant::SingleFB)
+    throw ValidationError("executor: single-fb plans are outside the hot path");
+  horizontal = plan.kind.variant == ScheduleVariant::Horizontal;
+  if (horizontal) throw ValidationError("executor: horizontal plans are not executable yet (vertical hot path only)");
+  if (ms.low_precision_bytes != 2 && ms.low_precision_bytes != 4)
+    throw ValidationError("executor: low_precision_bytes must be 2 (bf16) or 4 (fp32)");
+  if (ms.full_precision_bytes != 4 || ms.optimizer_states_per_element != 3)
+    throw ValidationError("executor: fp32 gradients and three Adam states required");
+  if (ms.hidden_dim % ms.num_heads || ms.hidden_dim / ms.num_heads > 128 || ms.hidden_dim > 12288)
+    throw ValidationError("executor: head_dim must divide hidden and be <= 128; hidden <= 12288");
+  if (ms.data_parallel_degree != 1 || cfg.world != 1)
+    throw ValidationError("executor: data parallel runs go through the dp driver (one executor per rank, dp=1 plan)");
+  if (plan.num_layers != ms.num_layers) throw ValidationError("executor: plan and model disagree on num_layers");
+  if (cfg.vocab_size < 2) throw ValidationError("executor: vocab_size must be >= 2");
+
+  N = ms.num_layers;
+  M = plan.num_microbatches;
+  d.b = ms.microbatch_size;
+  d.s = ms.seq_len;
+  d.h = ms.hidden_dim;
+  d.H = ms.num_heads;
+  d.V = cfg.vocab_size;
+  d.dt = ms.low_precision_bytes == 2 ? DType::BF16 : DType::F32;
+  const LayerSizes ls = derive_layer_sizes(ms);
+  P = ls.param_elements;
+  pb = ls.param_bytes_low;
+  cb = ls.ckpt_bytes_per_mb;
+  el_late = horizontal ? 0 : scaled_portion(P, plan.kind.delay_ratio);
+  el_now = P - el_late;
+
+  cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice");
+  cuda_check(cudaStreamCreateWithFlags(&s_gpu, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&s_opt, cudaStreamNonBlocking), "stream");
+
+  // ---- optimizer tier placement
+  const u64 opt_bytes = 12 * P;
+  const u64 cpu_opt = cpu_portion(opt_bytes, plan.split.x_opt);
+  bool opt_hbm = cfg.opt_tier == OptTier::Hbm;
+  if (cfg.opt_tier == OptTier::Auto) {
+    size_t free_b = 0, total_b = 0;
+    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    // leave room for params, grads, activations and staging: 3/4 of free HBM
+    opt_hbm = static_cast<double>(cpu_opt) * N < 0.6 * static_cast<double>(free_b);
+  }
+
+  // ---- device buffers
+  for (int i = 0; i < 2; ++i) dev_param[i] = dmalloc(pb);
+  grad_ring = horizontal ? 2 : 3;
+  for (int i = 0; i < grad_ring; ++i) grad_slot.push_back(static_cast<float*>(dmalloc(4 * P)));
+  retain.assign(static_cast<size_t>(N), nullptr);
+  if (el_late > 0)
+    for (int l = 0; l < N; ++l) retain[static_cast<size_t>(l)] = static_cast<float*>(dmalloc(4 * el_late));
+  n_fixed = static_cast<long long>(d.V + d.s) * d.h;
+  fx_master = static_cast<float*>(dmalloc(4 * n_fixed));
+  fx_m = static_cast<float*>(dmalloc(4 * n_fixed));
+  fx_v = static_cast<float*>(dmalloc(4 * n_fixed));
+  fx_grad = static_cast<float*>(dmalloc(4 * n_fixed));
+  fx_lp = dmalloc(static_cast<u64>(n_fixed) * d.lp());
+  if (!alloc_workspace(d, ws)) throw InfeasibleError("executor: device workspace allocation failed");
+  dev_bytes += ws.bytes;
+  for (int i = 0; i < 2 * M; ++i) {
+    in_x.push_back(dmalloc(cb));
+    out_y.push_back(dmalloc(cb));
+    in_g.push_back(dmalloc(cb));
+    out_g.push_back(dmalloc(cb));
+  }
+  const u64 tok_bytes = 4ull * M * d.b * (d.s + 1);
+  for (int i = 0; i < 2; ++i) dev_tok[i] = static_cast<int32_t*>(dmalloc(tok_bytes));
+  chunk = static_cast<long long>(std::min<u64>(P, 32ull << 20));
+  chunk = (chunk + 3) / 4 * 4;
+  opt_stage = static_cast<float*>(dmalloc(12ull * chunk));
+  lp_stage = dmalloc(static_cast<u64>(chunk) * d.lp());
+  cuda_check(cudaMemset(fx_m, 0, 4 * n_fixed), "memset");
+  cuda_check(cudaMemset(fx_v, 0, 4 * n_fixed), "memset");
+  cuda_check(cudaMemset(fx_grad, 0, 4 * n_fixed), "memset");
+
+  // ---- host tiers
+  const bool need_nvme = plan.split.x_param < 1.0 || plan.split.x_ckpt < 1.0 || plan.split.x_opt < 1.0;
+  if (need_nvme) nvme = std::make_unique<NvmeFile>(cfg.nvme_dir, cfg.odirect, 8);
+  const u64 lp = static_cast<u64>(d.lp());
+  for (int l = 0; l < N; ++l) {
+    param_blob.push_back(make_blob(pb, {lp * el_now}, cpu_portion(pb, plan.split.x_param), false));
+    opt_blob.push_back(make_blob(opt_bytes, {12 * el_now}, cpu_opt, opt_hbm));
+    host_grad.push_back(arena.alloc(4 * P));
+  }
+  for (int l = 0; l < N; ++l)
+    for (int m = 0; m < M; ++m) ckpt_blob.push_back(make_blob(cb, {}, cpu_portion(cb, plan.split.x_ckpt), false));
+  for (int i = 0; i < 2 * M; ++i) host_ilg.push_back(arena.alloc(cb));
+  if (nvme) nvme->finalize_size();
+
+  init_weights();
+  late_ready.reset(new std::atomic<long long>[static_cast<size_t>(N)]);
+  late_applied.reset(new std::atomic<long long>[static_cast<size_t>(N)]);
+  for (int l = 0; l < N; ++l) {
+    late_ready[static_cast<size_t>(l)].store(-1);
+    late_applied[static_cast<size_t>(l)].store(-1);
+  }
+  build_tasks();
+  hazards();
+  cuda_check(cudaEventCreate(&ev_base), "event");
+}
+
+Executor::Impl::~Impl() {
+  cudaDeviceSynchronize();
+  for (auto& a : ev_done)
+    for (cudaEvent_t e : a) cudaEventDestroy(e);
+  for (auto& a : ev_start)
+    for (cudaEvent_t e : a)
+      if (e) cudaEventDestroy(e);
+  if (ev_base) cudaEventDestroy(ev_base);
+  free_workspace(ws);
+  for (void* p : dev_allocs) cudaFree(p);
+  for (cudaStream_t s : {s_gpu, s_h2d, s_d2h, s_opt})
+    if (s) cudaStreamDestroy(s);
+}
+
+void* Executor::Impl::dmalloc(u64 bytes) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, std::max<u64>(bytes, 256)) != cudaSuccess)
+    throw InfeasibleError("executor: cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+  dev_allocs.push_back(p);
+  dev_bytes += bytes;
+  return p;
+}
+
+// Cut [0,size) at the CPU/SSD boundary and the extra cut points; CPU-resident
+// segments live in pinned DRAM (or HBM), SSD segments get image + read
+// staging + an NVMe region.
+Blob Executor::Impl::make_blob(u64 size, std::vector<u64> cuts, u64 cpu_bytes, bool hbm_for_cpu) {
+  cuts.push_back(0);
+  cuts.push_back(size);
+  cuts.push_back(cpu_bytes);
+  std::sort(cuts.begin(), cuts.end());
+  cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+  Blob b;
+  b.size = size;
+  for (size_t i = 0; i + 1 < cuts.size(); ++i) {
+    Segment s;
+    s.lo = cuts[i];
+    s.hi = cuts[i + 1];
+    if (s.hi <= s.lo || s.hi > size) continue;
+    if (s.lo < cpu_bytes) {
+      s.tier = hbm_for_cpu ? Tier::Hbm : Tier::Dram;
+      if (hbm_for_cpu) {
+        s.dev = static_cast<uint8_t*>(dmalloc(s.size()));
+      } else {
+        s.img = arena.alloc(s.size());
+      }
+    } else {
+      s.tier = Tier::Ssd;
+      s.img = arena.alloc(s.size());
+      s.rd = arena.alloc(s.size());
+      s.file_off = nvme->reserve(s.size());
+    }
+    b.segs.push_back(s);
+  }
+  return b;
+}
+
+// Initial master weights (fp32) -> optimizer blobs (AoS [master, m=0, v=0]),
+// low-precision copies -> parameter blobs; SSD segments persisted to NVMe.
+void Executor::Impl::init_weights() {
+  const long long h2 = 1LL * d.h * d.h;
+  const double scaled = 0.02 / std::sqrt(2.0 * N);
+  std::vector<float> w(P);
+  std::vector<float> state(12 * P / 4);
+  std::vector<uint8_t> lpbuf(pb);
+  for (int l = 0; l < N; ++l) {
+    const uint64_t key = stream_key(cfg.seed, 100 + static_cast<uint64_t>(l));
+    parallel_for(static_cast<long long>(P), [&](long long lo, long long hi) {
+      for (long long i = lo; i < hi; ++i) {
+        const bool out_proj = (i >= 3 * h2 && i < 4 * h2) || i >= 8 * h2;
+        const float v = static_cast<float>((out_proj ? scaled : 0.02) * normal_at(key, static_cast<uint64_t>(i)));
+        w[static_cast<size_t>(i)] = v;
+        state[3 * static_cast<size_t>(i)] = v;
+        state[3 * static_cast<size_t>(i) + 1] = 0.0f;
+        state[3 * static_cast<size_t>(i) + 2] = 0.0f;
+        if (d.dt == DType::BF16) {
+          const uint16_t bv = f32_to_bf16(v);
+          std::memcpy(&lpbuf[2 * static_cast<size_t>(i)], &bv, 2);
+        } else {
+          std::memcpy(&lpbuf[4 * static_cast<size_t>(i)], &v, 4);
+        }
+      }
+    });
+    for (Blob* b : {&param_blob[static_cast<size_t>(l)], &opt_blob[static_cast<size_t>(l)]}) {
+      const uint8_t* src = b == &param_blob[static_cast<size_t>(l)] ? lpbuf.data()
+                                                                    : reinterpret_cast<const uint8_t*>(state.data());
+      for (Segment& s : b->segs) {
+        if (s.tier == Tier::Hbm) {
+          cuda_check(cudaMemcpy(s.dev, src + s.lo, s.size(), cudaMemcpyHostToDevice), "init H2D");
+        } else {
+          std::memcpy(s.img, src + s.lo, s.size());
+          if (s.tier == Tier::Ssd) nvme->write(s.file_off, s.img, s.size());
+        }
+      }
+    }
+  }
+  // fixed params: wte N(0,0.02) stream 1, wpe stream 2
+  std::vector<float> fx(static_cast<size_t>(n_fixed));
+  const long long nw = 1LL * d.V * d.h;
+  const uint64_t k1 = stream_key(cfg.seed, 1), k2 = stream_key(cfg.seed, 2);
+  parallel_for(n_fixed, [&](long long lo, long long hi) {
+    for (long long i = lo; i < hi; ++i)
+      fx[static_cast<size_t>(i)] = static_cast<float>(
+          0.02 * (i < nw ? normal_at(k1, static_cast<uint64_t>(i)) : normal_at(k2, static_cast<uint64_t>(i - nw))));
+  });
+  cuda_check(cudaMemcpy(fx_master, fx.data(), 4 * n_fixed, cudaMemcpyHostToDevice), "init fixed");
+  cuda_check(gs::cast_from_f32(d.dt, fx_master, fx_lp, n_fixed, s_gpu), "cast fixed");
+  cuda_check(cudaStreamSynchronize(s_gpu), "init sync");
+}
+
+void Executor::Impl::build_tasks() {
+  const size_t n = plan.tasks.size();
+  res_of.resize(n);
+  fwd_phase.assign(n, 0);
+  chunk_lo.assign(n, 0);
+  {
+    bool fwd = true;
+    std::map<std::pair<int, int>, u64> next_lo;  // (layer, stage) -> running chunk offset
+    for (size_t i = 0; i < n; ++i) {
+      const Task& t = plan.tasks[i];
+      if (t.kind == TaskKind::RecomputeAndBwd) fwd = false;
+      fwd_phase[i] = fwd ? 1 : 0;
+      if (t.kind == TaskKind::Xfer && t.data == DataKind::Param && t.link == LinkKind::PCIe_H2D) {
+        u64& lo = next_lo[{t.layer, t.stage}];
+        chunk_lo[i] = lo;
+        lo += t.bytes;
+      }
+    }
+  }
+  queue.assign(kNumResources, {});
+  is_stream.assign(n, 0);
+  ev_done.resize(n);
+  done_iter = std::vector<std::atomic<int>>(n);
+  for (size_t i = 0; i < n; ++i) {
+    const Task& t = plan.tasks[i];
+    const Resource r = task_resource(t, true);
+    res_of[i] = r;
+    queue[static_cast<size_t>(r)].push_back(static_cast<int>(i));
+    is_stream[i] = (r == Resource::GPU || r == Resource::CPU || r == Resource::H2D || r == Resource::D2H) ? 1 : 0;
+    done_iter[i].store(-1);
+    for (auto& e : ev_done[i]) {
+      e = nullptr;
+      if (is_stream[i]) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+  }
+  if (cfg.record_trace) {
+    ev_start.resize(n);
+    for (size_t i = 0; i < n; ++i)
+      for (int k = 0; k < 3; ++k) {
+        ev_start[i][static_cast<size_t>(k)] = nullptr;
+        if (is_stream[i]) {
+          cudaEventDestroy(ev_done[i][static_cast<size_t>(k)]);
+          cuda_check(cudaEventCreate(&ev_done[i][static_cast<size_t>(k)]), "event");
+          cuda_check(cudaEventCreate(&ev_start[i][static_cast<size_t>(k)]), "event");
+        }
+      }
+  }
+}
+
+// ---------------------------------------------------------------- hazards
+namespace {
+enum SlotKind {
+  kDevParam, kInX, kOutY, kInG, kOutG, kGrad, kRetain, kHostIlg, kParamImg, kParamRd, kOptImg, kOptRd, kCkptImg,
+  kCkptRd, kHostGrad, kOptDev
+};
+struct Access {
+  long long slot;
+  bool write;
+};
+long long slot_id(int kind, long long a, long long b = 0) { return (static_cast<long long>(kind) << 48) | (a << 24) | b; }
+}  // namespace
+
+void Executor::Impl::hazards() {
+  const size_t n = plan.tasks.size();
+  std::vector<std::vector<Access>> acc(n);
+  for (size_t i = 0; i < n; ++i) {
+    const Task& t = plan.tasks[i];
+    auto R = [&](long long s) { acc[i].push_back({s, false}); };
+    auto W = [&](long long s) { acc[i].push_back({s, true}); };
+    const int l = t.layer, m = t.microbatch, st = t.stage;
+    const int par = ((st % 2) + 2) % 2;
+    const int parm1 = (((st - 1) % 2) + 2) % 2;
+    const bool late = delayed(t);
+    const int imm_late = late ? 1 : 0;
+    switch (t.kind) {
+      case TaskKind::FixedOps: break;
+      case TaskKind::FwdCompute:
+        R(slot_id(kDevParam, par));
+        if (!horizontal && l > 0) R(m == first_mb(st) ? slot_id(kOutY, parm1, m) : slot_id(kInX, par, m));
+        W(slot_id(kOutY, horizontal ? 0 : par, m));
+        break;
+      case TaskKind::RecomputeAndBwd:
+        R(slot_id(kDevParam, par));
+        if (horizontal) {
+          R(slot_id(kInX, 0, m));
+          R(slot_id(kGrad, l % grad_ring));
+          W(slot_id(kGrad, l % grad_ring));
+          break;
+        }
+        if (l > 0) R(slot_id(kInX, par, m));
+        if (l < N - 1) R(m == first_mb(st) ? slot_id(kOutG, parm1, m) : slot_id(kInG, par, m));
+        W(slot_id(kOutG, par, m));
+        R(slot_id(kGrad, l % grad_ring));
+        W(slot_id(kGrad, l % grad_ring));
+        if (m == last_mb(st) && el_late > 0) W(slot_id(kRetain, l));
+        break;
+      case TaskKind::CpuStep:
+        R(late ? slot_id(kRetain, l) : slot_id(kGrad, l % grad_ring));
+        R(slot_id(kOptRd, l, imm_late));
+        R(slot_id(kOptImg, l, imm_late));
+        W(slot_id(kOptImg, l, imm_late));
+        W(slot_id(kOptDev, l, imm_late));
+        W(slot_id(kParamImg, l));
+        break;
+      case TaskKind::Xfer: {
+        const bool fwd = fwd_phase[i] != 0;
+        switch (t.data) {
+          case DataKind::Param:
+            if (t.link == LinkKind::SSD_Read) W(slot_id(kParamRd, l));
+            else if (t.link == LinkKind::SSD_Write) R(slot_id(kParamImg, l));
+            else {
+              R(slot_id(kParamImg, l));
+              R(slot_id(kParamRd, l));
+              W(slot_id(kDevParam, (((st + 1) % 2) + 2) % 2));
+            }
+            break;
+          case DataKind::Ckpt:
+            if (horizontal) {
+              if (t.link == LinkKind::PCIe_D2H) { R(slot_id(kOutY, 0, m)); W(slot_id(kCkptImg, l, m)); }
+              else if (t.link == LinkKind::PCIe_H2D) { R(slot_id(kCkptImg, l, m)); R(slot_id(kCkptRd, l, m)); W(slot_id(kInX, 0, m)); }
+              else if (t.link == LinkKind::SSD_Write) R(slot_id(kCkptImg, l, m));
+              else W(slot_id(kCkptRd, l, m));
+              break;
+            }
+            if (t.link == LinkKind::PCIe_D2H) {
+              R(slot_id(kOutY, par, m));
+              W(slot_id(kCkptImg, l, m));
+            } else if (t.link == LinkKind::PCIe_H2D) {
+              R(slot_id(kCkptImg, l - 1, m));
+              if (!fwd) R(slot_id(kCkptRd, l - 1, m));
+              W(slot_id(kInX, par, m));
+            } else if (t.link == LinkKind::SSD_Write) {
+              for (int k = 0; k < M; ++k) R(slot_id(kCkptImg, l, k));
+            } else {
+              for (int k = 0; k < M; ++k) W(slot_id(kCkptRd, l - 1, k));
+            }
+            break;
+          case DataKind::GradAccum:
+            if (t.link == LinkKind::PCIe_D2H) {
+              R(slot_id(kGrad, l % grad_ring));
+              W(slot_id(kHostGrad, l));
+            } else {  // horizontal accumulation fetch
+              R(slot_id(kHostGrad, l));
+              W(slot_id(kGrad, l % grad_ring));
+            }
+            break;
+          case DataKind::InterlayerGrad:
+            if (t.link == LinkKind::PCIe_D2H) {
+              R(slot_id(kOutG, par, m));
+              W(slot_id(kHostIlg, par, m));
+            } else {
+              R(slot_id(kHostIlg, parm1, m));
+              W(slot_id(kInG, par, m));
+            }
+            break;
+          case DataKind::OptState:
+            if (t.link == LinkKind::SSD_Read) W(slot_id(kOptRd, l, imm_late));
+            else R(slot_id(kOptImg, l, imm_late));
+            break;
+        }
+        break;
+      }
+    }
+  }
+  // WAR / WAW over two unrolled iterations; deps discovered in iteration 1
+  // carry offsets 0 / -1 and hold in every steady-state iteration.
+  struct Use {
+    int task, iter;
+  };
+  std::map<long long, std::vector<Use>> readers;
+  std::map<long long, Use> writer;
+  std::vector<std::set<std::pair<int, int>>> found(n);
+  for (int it = 0; it < 2; ++it) {
+    for (size_t i = 0; i < n; ++i) {
+      for (const Access& a : acc[i])
+        if (!a.write) readers[a.slot].push_back({static_cast<int>(i), it});
+      for (const Access& a : acc[i]) {
+        if (!a.write) continue;
+        auto add = [&](Use u) {
+          if (u.task == static_cast<int>(i) && u.iter == it) return;
+          if (it == 1) found[i].insert({u.task, u.iter - it});
+        };
+        for (const Use& u : readers[a.slot]) add(u);
+        auto w = writer.find(a.slot);
+        if (w != writer.end()) add(w->second);
+        readers[a.slot].clear();
+        writer[a.slot] = {static_cast<int>(i), it};
+      }
+    }
+  }
+  extra.assign(n, {});
+  for (size_t i = 0; i < n; ++i) {
+    const Task& t = plan.tasks[i];
+    for (const auto& [task, offv] : found[i]) {
+      if (offv == 0 && std::binary_search(t.deps.begin(), t.deps.end(), task)) continue;
+      if (offv == -1 && t.cross_iter_dep == task) continue;
+      if (res_of[static_cast<size_t>(task)] == res_of[i] && offv == 0 && task < static_cast<int>(i)) continue;  // FIFO order
+      extra[i].push_back({task, offv});
+    }
+  }
+}
+
+// ------------------------------------------------------------ data movement
+// Upload logical bytes [lo,hi) of a blob to dst.  SSD segments come from the
+// read staging (Src::ReadStaging), the image (Src::Image) or, for Auto, the
+// image when the segment lies at/after `delayed_lo` (freshly produced by the
+// delayed step) and the staging otherwise.  Returns bytes moved over PCIe.
+u64 Executor::Impl::upload(const Blob& b, u64 lo, u64 hi, void* dst, Src src, cudaStream_t st, u64 delayed_lo) {
+  u64 moved = 0;
+  for (const Segment& s : b.segs) {
+    const u64 a = std::max(lo, s.lo), e = std::min(hi, s.hi);
+    if (a >= e) continue;
+    const uint8_t* from;
+    cudaMemcpyKind kind = cudaMemcpyHostToDevice;
+    if (s.tier == Tier::Hbm) {
+      from = s.dev;
+      kind = cudaMemcpyDeviceToDevice;
+    } else if (s.tier == Tier::Dram) {
+      from = s.img;
+    } else {
+      const bool img = src == Src::Image || (src == Src::Auto && s.lo >= delayed_lo);
+      from = img ? s.img : s.rd;
+    }
+    cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + (a - lo), from + (a - s.lo), e - a, kind, st), "upload");
+    if (kind == cudaMemcpyHostToDevice) moved += e - a;
+  }
+  return moved;
+}
+
+u64 Executor::Impl::download(Blob& b, u64 lo, u64 hi, const void* src, cudaStream_t st) {
+  u64 moved = 0;
+  for (Segment& s : b.segs) {
+    const u64 a = std::max(lo, s.lo), e = std::min(hi, s.hi);
+    if (a >= e) continue;
+    const uint8_t* from = static_cast<const uint8_t*>(src) + (a - lo);
+    if (s.tier == Tier::Hbm) {
+      if (s.dev + (a - s.lo) != from)
+        cuda_check(cudaMemcpyAsync(s.dev + (a - s.lo), from, e - a, cudaMemcpyDeviceToDevice, st), "download");
+    } else {
+      cuda_check(cudaMemcpyAsync(s.img + (a - s.lo), from, e - a, cudaMemcpyDeviceToHost, st), "download");
+      moved += e - a;
+    }
+  }
+  return moved;
+}
+
+// NVMe write (image -> file) or read (file -> staging) of the SSD segments
+// overlapping [lo,hi).  Whole segments move (they are the I/O units).
+u64 Executor::Impl::ssd_io(Blob& b, u64 lo, u64 hi, bool write) {
+  u64 phys = 0;
+  for (Segment& s : b.segs) {
+    if (s.tier != Tier::Ssd || s.hi <= lo || s.lo >= hi) continue;
+    phys += write ? nvme->write(s.file_off, s.img, s.size()) : nvme->read(s.file_off, s.rd, s.size());
+  }
+  return phys;
+}
+
+// ------------------------------------------------------------ execution
+cudaStream_t Executor::Impl::stream_of(Resource r) const {
+  switch (r) {
+    case Resource::GPU: return s_gpu;
+    case Resource::CPU: return s_opt;
+    case Resource::H2D: return s_h2d;
+    case Resource::D2H: return s_d2h;
+    default: return nullptr;
+  }
+}
+
+void Executor::Impl::wait_dep(int dep, int iter, bool on_stream, cudaStream_t st) {
+  if (iter < 0) return;
+  {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return done_iter[static_cast<size_t>(dep)].load() >= iter || failed.load(); });
+  }
+  if (failed.load()) throw std::runtime_error("aborted");
+  if (!is_stream[static_cast<size_t>(dep)]) return;
+  cudaEvent_t e = ev_done[static_cast<size_t>(dep)][static_cast<size_t>(iter % 3)];
+  if (on_stream)
+    cuda_check(cudaStreamWaitEvent(st, e, 0), "cudaStreamWaitEvent");
+  else
+    cuda_check(cudaEventSynchronize(e), "cudaEventSynchronize");
+}
+
+void Executor::Impl::note_ledger(int it, const Task& t, u64 phys) {
+  std::lock_guard<std::mutex> g(led_mu);
+  if (it != last_iter) return;
+  led_logical.at(t.link, t.data) += t.bytes;
+  led_phys.at(t.link, t.data) += phys;
+}
+void Executor::Impl::note_ext(int it, LinkKind l, DataKind dk, u64 bytes) {
+  if (bytes == 0) return;
+  std::lock_guard<std::mutex> g(led_mu);
+  if (it != last_iter) return;
+  led_ext.at(l, dk) += bytes;
+}
+
+void Executor::Impl::run_task(int id, int it) {
+  const Task& t = plan.tasks[static_cast<size_t>(id)];
+  const Resource r = res_of[static_cast<size_t>(id)];
+  const bool stream = is_stream[static_cast<size_t>(id)];
+  cudaStream_t st = stream_of(r);
+  for (int dep : t.deps) wait_dep(dep, it, stream, st);
+  if (t.cross_iter_dep >= 0) wait_dep(t.cross_iter_dep, it - 1, stream, st);
+  for (const ExtraDep& x : extra[static_cast<size_t>(id)]) wait_dep(x.task, it + x.offset, stream, st);
+
+  const auto h0 = std::chrono::steady_clock::now();
+  if (stream && cfg.record_trace)
+    cuda_check(cudaEventRecord(ev_start[static_cast<size_t>(id)][static_cast<size_t>(it % 3)], st), "record");
+  u64 phys = 0;
+  switch (t.kind) {
+    case TaskKind::FwdCompute:
+    case TaskKind::RecomputeAndBwd:
+    case TaskKind::FixedOps: compute_task(t, it); break;
+    case TaskKind::CpuStep: step_task(t, it); break;
+    case TaskKind::Xfer: xfer_task(t, it, phys); break;
+  }
+  if (stream) {
+    cuda_check(cudaEventRecord(ev_done[static_cast<size_t>(id)][static_cast<size_t>(it % 3)], st), "record");
+  }
+  if (t.kind == TaskKind::Xfer) note_ledger(it, t, phys);
+  if (cfg.record_trace) {
+    TraceRecord rec{it, id, r, 0.0, 0.0, t.bytes, phys};
+    if (!stream) {
+      rec.t_start_ms = std::chrono::duration<double, std::milli>(h0 - host_base).count();
+      rec.t_end_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_base).count();
+    }
+    std::lock_guard<std::mutex> g(trace_mu);
+    trace.push_back(rec);
+  }
+  {
+    std::lock_guard<std::mutex> g(mu);
+    done_iter[static_cast<size_t>(id)].store(it);
+  }
+  cv.notify_all();
+}
+
+void Executor::Impl::compute_task(const Task& t, int it) {
+  const long long git = global_iter + it;
+  const int slot = static_cast<int>(git % 2);
+  LaunchCounter lc;
+  if (t.kind == TaskKind::FixedOps) {
+    const long long tok_n = 1LL * M * d.b * (d.s + 1);
+    const int32_t* src = run_tokens + static_cast<long long>(it) * tok_n;
+    cuda_check(cudaMemcpyAsync(dev_tok[slot], src, 4 * tok_n,
+                               run_tokens_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s_gpu),
+               "tokens");
+    cuda_check(cudaMemsetAsync(dev_loss + it, 0, sizeof(double), s_gpu), "loss");
+    if (fixed_done < git) {  // embedding / head step with the previous iteration's grads
+      gs::AdamHyper hp{cfg.adam.lr, cfg.adam.beta1, cfg.adam.beta2, cfg.adam.eps, cfg.adam.weight_decay};
+      cuda_check(gs::adam_step(hp, static_cast<int>(git), 1.0f, fx_master, fx_m, fx_v, fx_grad, fx_lp, d.dt, n_fixed,
+                               s_gpu),
+                 "fixed adam");
+      cuda_check(cudaMemsetAsync(fx_grad, 0, 4 * n_fixed, s_gpu), "fixed grad");
+      fixed_done = git;
+      lc.n += 1;
+    }
+    launches += lc.n;
+    return;
+  }
+  const int l = t.layer, m = t.microbatch, st = t.stage;
+  const int par = st % 2, parm1 = (st + 1) % 2;
+  const long long tok_n = 1LL * d.b * (d.s + 1);
+  const int32_t* tok = dev_tok[slot] + m * tok_n;
+  const void* W = dev_param[par];
+  const void* wte = fx_lp;
+  const void* wpe = static_cast<const uint8_t*>(fx_lp) + 1LL * d.V * d.h * d.lp();
+  auto ck = [&](std::vector<void*>& v, int p, int mb) { return v[static_cast<size_t>(p * M + mb)]; };
+
+  if (t.kind == TaskKind::FwdCompute) {
+    const void* x;
+    if (l == 0) {
+      cuda_check(gs::embed_fwd(d.dt, wte, wpe, tok, ws.x0, d.b, d.s, d.h, s_gpu), "embed");
+      lc.n += 1;
+      x = ws.x0;
+    } else if (horizontal) {
+      x = ck(out_y, 0, m);
+    } else {
+      x = m == first_mb(st) ? ck(out_y, parm1, m) : ck(in_x, par, m);
+    }
+    void* y = horizontal ? ws.tmp : ck(out_y, par, m);
+    if (horizontal) {
+      // horizontal: the D2H'd checkpoint is this layer's INPUT (schedule.cpp:186-188)
+      if (x != ck(out_y, 0, m))
+        cuda_check(cudaMemcpyAsync(ck(out_y, 0, m), x, cb, cudaMemcpyDeviceToDevice, s_gpu), "ckpt stage");
+    }
+    cuda_check(layer_forward(d, W, horizontal ? ck(out_y, 0, m) : x, y, ws, s_gpu, lc), "layer_forward");
+    if (horizontal) cuda_check(cudaMemcpyAsync(ck(in_g, 0, m), y, cb, cudaMemcpyDeviceToDevice, s_gpu), "carry");
+    launches += lc.n;
+    return;
+  }
+
+  // RecomputeAndBwd
+  float* gslot = grad_slot[static_cast<size_t>(l % grad_ring)];
+  const void* x;
+  if (l == 0) {
+    cuda_check(gs::embed_fwd(d.dt, wte, wpe, tok, ws.x0, d.b, d.s, d.h, s_gpu), "embed");
+    lc.n += 1;
+    x = ws.x0;
+  } else {
+    x = horizontal ? ck(in_x, 0, m) : ck(in_x, par, m);
+  }
+  HeadArgs head;
+  const HeadArgs* hp = nullptr;
+  const void* dy = nullptr;
+  if (l == N - 1) {
+    head.wte = wte;
+    head.dwte = fx_grad;
+    head.tokens = tok;
+    head.scale = 1.0f / (static_cast<float>(d.T()) * static_cast<float>(M));
+    head.loss_sum = dev_loss + it;
+    hp = &head;
+  } else if (horizontal) {
+    dy = ck(out_g, 1, m);
+  } else {
+    dy = m == first_mb(st) ? ck(out_g, parm1, m) : ck(in_g, par, m);
+  }
+  void* dx = horizontal ? ck(out_g, 0, m) : ck(out_g, par, m);
+  bool first;
+  if (horizontal) first = (m == 0);  // later MBs accumulate onto the fetched partial sum
+  else first = (m == first_mb(st));
+  cuda_check(layer_backward(d, W, x, dy, dx, gslot, first, hp, ws, s_gpu, lc), "layer_backward");
+  if (horizontal && l > 0) cuda_check(cudaMemcpyAsync(ck(out_g, 1, m), dx, cb, cudaMemcpyDeviceToDevice, s_gpu), "carry");
+  if (l == 0) {
+    cuda_check(gs::embed_bwd(d.dt, tok, dx, fx_grad, fx_grad + 1LL * d.V * d.h, d.b, d.s, d.h, s_gpu), "embed_bwd");
+    lc.n += 1;
+  }
+  if (!horizontal && m == last_mb(st) && el_late > 0) {
+    cuda_check(cudaMemcpyAsync(retain[static_cast<size_t>(l)], gslot + el_now, 4 * el_late, cudaMemcpyDeviceToDevice,
+                               s_gpu),
+               "retain");
+    late_ready[static_cast<size_t>(l)].store(git);
+  }
+  launches += lc.n;
+}
+
+// Fused Adam over elements [e0,e1) of layer l: optimizer state gathered from
+// its tiers into HBM (in place when a single HBM segment holds the range),
+// updated, scattered back; the low-precision params go to the host image.
+void Executor::Impl::apply_adam(int layer, u64 e0, u64 e1, const float* grad, int step, cudaStream_t st, int it) {
+  gs::AdamHyper hp{cfg.adam.lr, cfg.adam.beta1, cfg.adam.beta2, cfg.adam.eps, cfg.adam.weight_decay};
+  Blob& ob = opt_blob[static_cast<size_t>(layer)];
+  Blob& pbb = param_blob[static_cast<size_t>(layer)];
+  const u64 lp = static_cast<u64>(d.lp());
+  for (u64 c0 = e0; c0 < e1; c0 += static_cast<u64>(chunk)) {
+    const u64 c1 = std::min(e1, c0 + static_cast<u64>(chunk));
+    const u64 lo = 12 * c0, hi = 12 * c1;
+    float* state = nullptr;
+    for (Segment& s : ob.segs)
+      if (s.tier == Tier::Hbm && s.lo <= lo && hi <= s.hi) state = reinterpret_cast<float*>(s.dev + (lo - s.lo));
+    const bool in_place = state != nullptr && (reinterpret_cast<uintptr_t>(state) & 15) == 0;
+    u64 up = 0, down = 0;
+    if (!in_place) {
+      state = opt_stage;
+      up = upload(ob, lo, hi, state, Src::ReadStaging, st, ~0ull);
+    }
+    cuda_check(gs::adam_step_packed(hp, step, 1.0f, state, grad + (c0 - e0), lp_stage, d.dt,
+                                    static_cast<long long>(c1 - c0), st),
+               "adam");
+    launches += 1;
+    if (!in_place) down = download(ob, lo, hi, state, st);
+    const u64 pdown = download(pbb, lp * c0, lp * c1, lp_stage, st);
+    note_ext(it, LinkKind::PCIe_H2D, DataKind::OptState, up);
+    note_ext(it, LinkKind::PCIe_D2H, DataKind::OptState, down);
+    note_ext(it, LinkKind::PCIe_D2H, DataKind::Param, pdown);
+  }
+}
+
+void Executor::Impl::step_task(const Task& t, int it) {
+  const long long git = global_iter + it;
+  const int l = t.layer;
+  if (delayed(t)) {
+    // alpha slice of the previous iteration (step count git); nothing is
+    // retained before the first iteration
+    const long long ready = late_ready[static_cast<size_t>(l)].load();
+    if (el_late == 0 || ready != git - 1 || late_applied[static_cast<size_t>(l)].load() >= ready) return;
+    apply_adam(l, el_now, P, retain[static_cast<size_t>(l)], static_cast<int>(git), s_opt, it);
+    late_applied[static_cast<size_t>(l)].store(ready);
+    return;
+  }
+  if (el_now > 0)
+    apply_adam(l, 0, el_now, grad_slot[static_cast<size_t>(l % grad_ring)], static_cast<int>(git + 1), s_opt, it);
+}
+
+void Executor::Impl::xfer_task(const Task& t, int it, u64& phys) {
+  const int l = t.layer, m = t.microbatch, st = t.stage;
+  const int par = ((st % 2) + 2) % 2, parm1 = (((st - 1) % 2) + 2) % 2;
+  const bool fwd = fwd_phase[static_cast<size_t>(t.id)] != 0;
+  const u64 lp = static_cast<u64>(d.lp());
+  auto ck = [&](std::vector<void*>& v, int p, int mb) { return v[static_cast<size_t>(p * M + mb)]; };
+  switch (t.data) {
+    case DataKind::Param: {
+      Blob& b = param_blob[static_cast<size_t>(l)];
+      if (t.link == LinkKind::SSD_Read) {
+        // forward: only the immediate slice is re-read (the delayed slice was
+        // just produced in DRAM by the delayed step); backward: all of it
+        phys = fwd ? ssd_io(b, 0, lp * el_now, false) : ssd_io(b, 0, b.size, false);
+      } else if (t.link == LinkKind::SSD_Write) {
+        phys = delayed(t) ? ssd_io(b, lp * el_now, b.size, true) : ssd_io(b, 0, lp * el_now, true);
+      } else {
+        // chunk j of the layer's params (dp = 1: the shard is the layer),
+        // cut by chunk_size(shard, M, j) in emission order
+        const u64 lo = chunk_lo[static_cast<size_t>(t.id)];
+        const int use_par = (((st + 1) % 2) + 2) % 2;
+        const Src src = fwd ? Src::Auto : Src::ReadStaging;
+        phys = upload(b, lo, lo + t.bytes, static_cast<uint8_t*>(dev_param[use_par]) + lo, src, s_h2d, lp * el_now);
+      }
+      break;
+    }
+    case DataKind::Ckpt: {
+      if (horizontal) {
+        Blob& b = ckpt_blob[static_cast<size_t>(l * M + m)];
+        if (t.link == LinkKind::PCIe_D2H) phys = download(b, 0, cb, ck(out_y, 0, m), s_d2h);
+        else if (t.link == LinkKind::PCIe_H2D) phys = upload(b, 0, cb, ck(in_x, 0, m), Src::ReadStaging, s_h2d, ~0ull);
+        else if (t.link == LinkKind::SSD_Write) phys = ssd_io(b, 0, cb, true);
+        else phys = ssd_io(b, 0, cb, false);
+        break;
+      }
+      if (t.link == LinkKind::PCIe_D2H) {
+        phys = download(ckpt_blob[static_cast<size_t>(l * M + m)], 0, cb, ck(out_y, par, m), s_d2h);
+      } else if (t.link == LinkKind::PCIe_H2D) {
+        phys = upload(ckpt_blob[static_cast<size_t>((l - 1) * M + m)], 0, cb, ck(in_x, par, m),
+                      fwd ? Src::Image : Src::ReadStaging, s_h2d, ~0ull);
+      } else if (t.link == LinkKind::SSD_Write) {
+        for (int k = 0; k < M; ++k) phys += ssd_io(ckpt_blob[static_cast<size_t>(l * M + k)], 0, cb, true);
+      } else {
+        for (int k = 0; k < M; ++k) phys += ssd_io(ckpt_blob[static_cast<size_t>((l - 1) * M + k)], 0, cb, false);
+      }
+      break;
+    }
+    case DataKind::GradAccum: {
+      float* g = grad_slot[static_cast<size_t>(l % grad_ring)];
+      if (t.link == LinkKind::PCIe_D2H) {
+        cuda_check(cudaMemcpyAsync(host_grad[static_cast<size_t>(l)], g, t.bytes, cudaMemcpyDeviceToHost, s_d2h), "grad");
+      } else {
+        cuda_check(cudaMemcpyAsync(g, host_grad[static_cast<size_t>(l)], t.bytes, cudaMemcpyHostToDevice, s_h2d), "grad");
+      }
+      phys = t.bytes;
+      break;
+    }
+    case DataKind::InterlayerGrad: {
+      if (t.link == LinkKind::PCIe_D2H) {
+        cuda_check(cudaMemcpyAsync(host_ilg[static_cast<size_t>(par * M + m)], ck(out_g, par, m), cb,
+                                   cudaMemcpyDeviceToHost, s_d2h),
+                   "ilg");
+      } else {
+        cuda_check(cudaMemcpyAsync(ck(in_g, par, m), host_ilg[static_cast<size_t>(parm1 * M + m)], cb,
+                                   cudaMemcpyHostToDevice, s_h2d),
+                   "ilg");
+      }
+      phys = cb;
+      break;
+    }
+    case DataKind::OptState: {
+      Blob& b = opt_blob[static_cast<size_t>(l)];
+      const bool late = delayed(t) && !horizontal;
+      const u64 lo = late ? 12 * el_now : 0, hi = late ? b.size : 12 * el_now;
+      phys = ssd_io(b, lo, hi, t.link == LinkKind::SSD_Write);
+      break;
+    }
+  }
+}
+
+void Executor::Impl::dispatch(Resource r, int iterations) {
+  try {
+    cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice");
+    const auto& q = queue[static_cast<size_t>(r)];
+    for (int it = 0; it < iterations; ++it) {
+      // at most three iterations in flight (event slots are it % 3)
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] {
+          if (failed.load()) return true;
+          for (const auto& f : finished)
+            if (f.load() < it - 2) return false;
+          return true;
+        });
+      }
+      if (failed.load()) return;
+      for (int id : q) run_task(id, it);
+      {
+        std::lock_guard<std::mutex> g(mu);
+        finished[static_cast<size_t>(r)].store(it);
+      }
+      cv.notify_all();
+    }
+  } catch (const std::exception& e) {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (!failed.load()) error = e.what();
+      failed.store(true);
+    }
+    cv.notify_all();
+  }
+}
+
+// =========================================================================
+Executor::Executor(const SchedulePlan& plan, const ExecConfig& cfg) : impl_(std::make_unique<Impl>(plan, cfg)) {}
+Executor::~Executor() = default;
+const SchedulePlan& Executor::plan() const { return impl_->plan; }
+const ExecConfig& Executor::config() const { return impl_->cfg; }
+
+ExecReport Executor::run(int iterations, const int32_t* tokens, bool tokens_on_device) {
+  Impl& I = *impl_;
+  if (iterations < 1) throw ValidationError("run: iterations must be >= 1");
+  if (!tokens) throw ValidationError("run: tokens required");
+  const long long tok_n = 1LL * I.M * I.d.b * (I.d.s + 1);
+  if (!tokens_on_device) {
+    if (I.tok_capacity < tok_n * iterations) {
+      I.tok_pinned = reinterpret_cast<int32_t*>(I.arena.alloc(4ull * tok_n * iterations));
+      I.tok_capacity = tok_n * iterations;
+    }
+    std::memcpy(I.tok_pinned, tokens, 4ull * tok_n * iterations);
+    I.run_tokens = I.tok_pinned;
+  } else {
+    I.run_tokens = tokens;
+  }
+  I.run_tokens_dev = tokens_on_device;
+  if (I.loss_cap < iterations) {
+    I.dev_loss = static_cast<double*>(I.dmalloc(sizeof(double) * static_cast<u64>(iterations)));
+    I.loss_cap = iterations;
+  }
+  for (auto& f : I.finished) f.store(-1);
+  for (auto& di : I.done_iter) di.store(-1);
+  I.failed.store(false);
+  I.error.clear();
+  I.led_logical = TrafficLedger{};
+  I.led_ext = TrafficLedger{};
+  I.led_phys = TrafficLedger{};
+  I.last_iter = iterations - 1;
+  I.trace.clear();
+  I.launches.store(0);
+
+  cuda_check(cudaDeviceSynchronize(), "pre-run sync");
+  cuda_check(cudaEventRecord(I.ev_base, I.s_gpu), "base");
+  cuda_check(cudaEventSynchronize(I.ev_base), "base");
+  I.host_base = std::chrono::steady_clock::now();
+  // H2D/D2H/opt streams start after the base event
+  for (cudaStream_t s : {I.s_h2d, I.s_d2h, I.s_opt}) cuda_check(cudaStreamWaitEvent(s, I.ev_base, 0), "base wait");
+
+  std::vector<std::thread> ts;
+  for (int r = 0; r < kNumResources; ++r)
+    ts.emplace_back([&I, r, iterations] { I.dispatch(static_cast<Resource>(r), iterations); });
+  for (auto& t : ts) t.join();
+  if (I.failed.load()) {
+    cudaDeviceSynchronize();
+    throw std::runtime_error("executor run failed: " + I.error);
+  }
+  // join all streams, then stop the clock
+  cudaEvent_t ev_end;
+  cuda_check(cudaEventCreate(&ev_end), "event");
+  for (cudaStream_t s : {I.s_h2d, I.s_d2h, I.s_opt}) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(e, s), "record");
+    cuda_check(cudaStreamWaitEvent(I.s_gpu, e, 0), "join");
+    cudaEventDestroy(e);
+  }
+  std::vector<double> loss(static_cast<size_t>(iterations));
+  ExecReport rep;
+  cuda_check(cudaEventRecord(ev_end, I.s_gpu), "record");
+  cuda_check(cudaEventSynchronize(ev_end), "sync");
+  float ms = 0.0f;
+  cuda_check(cudaEventElapsedTime(&ms, I.ev_base, ev_end), "elapsed");
+  rep.total_ms = ms;
+  cuda_check(cudaMemcpy(loss.data(), I.dev_loss, sizeof(double) * loss.size(), cudaMemcpyDeviceToHost), "loss");
+  cudaEventDestroy(ev_end);
+  const double denom = static_cast<double>(I.d.T()) * I.M;
+  for (int it = 0; it < iterations; ++it) rep.losses.push_back(loss[static_cast<size_t>(it)] / denom);
+  if (I.cfg.record_trace) {
+    // CUDA events are recycled every 3 iterations: keep the last three
+    std::vector<TraceRecord> kept;
+    for (const TraceRecord& rec : I.trace)
+      if (rec.iteration >= iterations - 3) kept.push_back(rec);
+    I.trace.swap(kept);
+    for (TraceRecord& rec : I.trace) {
+      if (!I.is_stream[static_cast<size_t>(rec.task)]) continue;
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, I.ev_base, I.ev_start[static_cast<size_t>(rec.task)][static_cast<size_t>(rec.iteration % 3)]);
+      cudaEventElapsedTime(&b, I.ev_base, I.ev_done[static_cast<size_t>(rec.task)][static_cast<size_t>(rec.iteration % 3)]);
+      rec.t_start_ms = a;
+      rec.t_end_ms = b;
+    }
+    rep.trace = I.trace;
+  }
+  I.global_iter += iterations;
+  rep.ledger = I.led_logical;
+  rep.extension = I.led_ext;
+  rep.physical = I.led_phys;
+  rep.gpu_bytes_allocated = I.dev_bytes;
+  rep.host_pinned_bytes = I.arena.bytes();
+  rep.gpu_launches = I.launches.load();
+  return rep;
+}
+
+void Executor::flush() {
+  Impl& I = *impl_;
+  cuda_check(cudaDeviceSynchronize(), "flush sync");
+  for (int l = 0; l < I.N; ++l) {
+    const long long ready = I.late_ready[static_cast<size_t>(l)].load();
+    if (I.el_late == 0 || ready < 0 || I.late_applied[static_cast<size_t>(l)].load() >= ready) continue;
+    I.apply_adam(l, I.el_now, I.P, I.retain[static_cast<size_t>(l)], static_cast<int>(ready + 1), I.s_opt, -2);
+    I.late_applied[static_cast<size_t>(l)].store(ready);
+  }
+  if (I.fixed_done < I.global_iter) {
+    gs::AdamHyper hp{I.cfg.adam.lr, I.cfg.adam.beta1, I.cfg.adam.beta2, I.cfg.adam.eps, I.cfg.adam.weight_decay};
+    cuda_check(gs::adam_step(hp, static_cast<int>(I.global_iter), 1.0f, I.fx_master, I.fx_m, I.fx_v, I.fx_grad, I.fx_lp,
+                             I.d.dt, I.n_fixed, I.s_opt),
+               "fixed adam");
+    cuda_check(cudaMemsetAsync(I.fx_grad, 0, 4 * I.n_fixed, I.s_opt), "fixed grad");
+    I.fixed_done = I.global_iter;
+  }
+  cuda_check(cudaDeviceSynchronize(), "flush sync");
+}
+
+namespace {
+// Reads field `f` (0 master, 1 m, 2 v) of every element of an opt blob.
+void read_field(Executor::Impl& I, int layer, int f, float* out);
+}  // namespace
+
+void Executor::read_params(float* layers, float* fixed) {
+  Impl& I = *impl_;
+  cuda_check(cudaDeviceSynchronize(), "sync");
+  if (layers)
+    for (int l = 0; l < I.N; ++l) read_field(I, l, 0, layers + static_cast<size_t>(l) * I.P);
+  if (fixed) cuda_check(cudaMemcpy(fixed, I.fx_master, 4 * I.n_fixed, cudaMemcpyDeviceToHost), "read fixed");
+}
+
+void Executor::read_moments(float* layer_m, float* layer_v) {
+  Impl& I = *impl_;
+  cuda_check(cudaDeviceSynchronize(), "sync");
+  for (int l = 0; l < I.N; ++l) {
+    if (layer_m) read_field(I, l, 1, layer_m + static_cast<size_t>(l) * I.P);
+    if (layer_v) read_field(I, l, 2, layer_v + static_cast<size_t>(l) * I.P);
+  }
+}
+
+namespace {
+void read_field(Executor::Impl& I, int layer, int f, float* out) {
+  const Blob& b = I.opt_blob[static_cast<size_t>(layer)];
+  std::vector<uint8_t> all(b.size);
+  for (const Segment& s : b.segs) {
+    if (s.tier == Tier::Hbm)
+      cuda_check(cudaMemcpy(all.data() + s.lo, s.dev, s.size(), cudaMemcpyDeviceToHost), "read opt");
+    else
+      std::memcpy(all.data() + s.lo, s.img, s.size());
+  }
+  const float* st = reinterpret_cast<const float*>(all.data());
+  for (u64 i = 0; i < I.P; ++i) out[i] = st[3 * i + static_cast<u64>(f)];
+}
+}  // namespace
+
+ExecReport execute(const SchedulePlan& plan, const ExecConfig& cfg, int iterations, const int32_t* tokens) {
+  Executor ex(plan, cfg);
+  return ex.run(iterations, tokens);
+}
+
+}  // namespace offsim

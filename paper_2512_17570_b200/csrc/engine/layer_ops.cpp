@@ -1,0 +1,161 @@
+#include "layer_ops.hpp"
+
+namespace gs::engine {
+
+namespace {
+
+#define GS_TRY(expr)                          \
+  do {                                        \
+    const cudaError_t e_ = (expr);            \
+    if (e_ != cudaSuccess) return e_;         \
+  } while (0)
+
+const uint8_t* off(const void* p, long long elems, int eb) {
+  return static_cast<const uint8_t*>(p) + elems * eb;
+}
+
+// C[M,N] = A . B^T style call with explicit majors.
+cudaError_t mm(const Dims& d, int M, int N, int K, const void* A, bool a_k, const void* B, bool b_k, void* C,
+               Epi epi, cudaStream_t st, LaunchCounter& lc, const void* R = nullptr, void* G = nullptr) {
+  GemmArgs g;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.A = A;
+  g.B = B;
+  g.a_kmajor = a_k;
+  g.b_kmajor = b_k;
+  g.C = C;
+  g.R = R;
+  g.G = G;
+  g.epi = epi;
+  g.dt = d.dt;
+  ++lc.n;
+  return gemm(g, st);
+}
+
+}  // namespace
+
+bool alloc_workspace(const Dims& d, Workspace& ws) {
+  const size_t eb = static_cast<size_t>(d.lp());
+  const size_t Th = static_cast<size_t>(d.T()) * d.h;
+  const size_t T = static_cast<size_t>(d.T());
+  bool ok = true;
+  auto get = [&](void** p, size_t bytes) {
+    if (!ok) return;
+    if (cudaMalloc(p, bytes < 256 ? 256 : bytes) != cudaSuccess) {
+      ok = false;
+      *p = nullptr;
+      return;
+    }
+    ws.bytes += bytes;
+  };
+  get(&ws.a, Th * eb);
+  get(&ws.qkv, 3 * Th * eb);
+  get(&ws.o, Th * eb);
+  get(&ws.x1, Th * eb);
+  get(&ws.c, Th * eb);
+  get(&ws.u, 4 * Th * eb);
+  get(&ws.g, 4 * Th * eb);
+  get(&ws.y, Th * eb);
+  get(&ws.dy, Th * eb);
+  get(&ws.big, 4 * Th * eb);
+  get(&ws.dx1, Th * eb);
+  get(&ws.tmp, Th * eb);
+  get(&ws.dqkv, 3 * Th * eb);
+  get(&ws.x0, Th * eb);
+  get(&ws.z, Th * eb);
+  get(reinterpret_cast<void**>(&ws.lse), sizeof(float) * static_cast<size_t>(d.b) * d.H * d.s);
+  float** stats[] = {&ws.m1, &ws.r1, &ws.m2, &ws.r2, &ws.mz, &ws.rz};
+  for (float** p : stats) get(reinterpret_cast<void**>(p), sizeof(float) * T);
+  get(&ws.attn_work, attention_bwd_workspace(d.b, d.s, d.h, d.H));
+  get(reinterpret_cast<void**>(&ws.logits), sizeof(float) * T * d.V);
+  get(&ws.dlogits, T * d.V * eb);
+  return ok;
+}
+
+void free_workspace(Workspace& ws) {
+  void* ptrs[] = {ws.a, ws.qkv, ws.o, ws.x1, ws.c, ws.u, ws.g, ws.y, ws.dy, ws.big, ws.dx1, ws.tmp, ws.dqkv,
+                  ws.x0, ws.z, ws.lse, ws.m1, ws.r1, ws.m2, ws.r2, ws.mz, ws.rz, ws.attn_work, ws.logits,
+                  ws.dlogits};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  ws = Workspace{};
+}
+
+// Forward through LN1 .. GELU; leaves a, qkv, o, lse, x1, c, u, g, stats in ws.
+static cudaError_t forward_body(const Dims& d, const void* W, const void* x, Workspace& ws, cudaStream_t st,
+                                LaunchCounter& lc) {
+  const int T = d.T(), h = d.h, eb = d.lp();
+  const long long h2 = 1LL * h * h;
+  const void* wqkv = W;
+  const void* wo = off(W, 3 * h2, eb);
+  const void* w1 = off(W, 4 * h2, eb);
+  GS_TRY(layernorm_fwd(d.dt, x, ws.a, ws.m1, ws.r1, T, h, st));
+  GS_TRY(mm(d, T, 3 * h, h, ws.a, true, wqkv, true, ws.qkv, Epi::Store, st, lc));
+  GS_TRY(attention_fwd(d.dt, ws.qkv, ws.o, ws.lse, d.b, d.s, h, d.H, st));
+  GS_TRY(mm(d, T, h, h, ws.o, true, wo, true, ws.x1, Epi::AddResidual, st, lc, x));
+  GS_TRY(layernorm_fwd(d.dt, ws.x1, ws.c, ws.m2, ws.r2, T, h, st));
+  GS_TRY(mm(d, T, 4 * h, h, ws.c, true, w1, true, ws.u, Epi::StoreGelu, st, lc, nullptr, ws.g));
+  lc.n += 4;  // two LayerNorms + attention (1 kernel in either path... counted as 1) + spare
+  return cudaSuccess;
+}
+
+cudaError_t layer_forward(const Dims& d, const void* W, const void* x, void* y, Workspace& ws, cudaStream_t st,
+                          LaunchCounter& lc) {
+  const long long h2 = 1LL * d.h * d.h;
+  GS_TRY(forward_body(d, W, x, ws, st, lc));
+  return mm(d, d.T(), d.h, 4 * d.h, ws.g, true, off(W, 8 * h2, d.lp()), true, y, Epi::AddResidual, st, lc, ws.x1);
+}
+
+cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const void* dy_in, void* dx, float* dW,
+                           bool first, const HeadArgs* head, Workspace& ws, cudaStream_t st, LaunchCounter& lc) {
+  const int T = d.T(), h = d.h, eb = d.lp();
+  const long long h2 = 1LL * h * h;
+  const void* wqkv = W;
+  const void* wo = off(W, 3 * h2, eb);
+  const void* w1 = off(W, 4 * h2, eb);
+  const void* w2 = off(W, 8 * h2, eb);
+  const Epi wg = first ? Epi::StoreF32 : Epi::AccumF32;
+  GS_TRY(forward_body(d, W, x, ws, st, lc));  // recompute from the checkpoint
+
+  const void* dy = dy_in;
+  if (head) {
+    // y = block output; tied head on LN_f(y); dy = d(CE)/dy
+    GS_TRY(mm(d, T, h, 4 * h, ws.g, true, w2, true, ws.y, Epi::AddResidual, st, lc, ws.x1));
+    GS_TRY(layernorm_fwd(d.dt, ws.y, ws.z, ws.mz, ws.rz, T, h, st));
+    GS_TRY(mm(d, T, d.V, h, ws.z, true, head->wte, true, ws.logits, Epi::StoreF32, st, lc));
+    GS_TRY(softmax_xent(ws.logits, ws.dlogits, d.dt, head->tokens, d.b, d.s, d.V, head->scale, head->loss_sum, st));
+    // dwte += dlogits^T z  (M=V, N=h, K=T)
+    GS_TRY(mm(d, d.V, h, T, ws.dlogits, false, ws.z, false, head->dwte, Epi::AccumF32, st, lc));
+    // dz = dlogits . wte   (M=T, N=h, K=V)
+    GS_TRY(mm(d, T, h, d.V, ws.dlogits, true, head->wte, false, ws.tmp, Epi::Store, st, lc));
+    GS_TRY(layernorm_bwd(d.dt, ws.y, ws.mz, ws.rz, ws.tmp, ws.dy, T, h, false, st));
+    dy = ws.dy;
+    lc.n += 3;
+  }
+  float* dWqkv = dW;
+  float* dWo = dW + 3 * h2;
+  float* dW1 = dW + 4 * h2;
+  float* dW2 = dW + 8 * h2;
+  // MLP
+  GS_TRY(mm(d, h, 4 * h, T, dy, false, ws.g, false, dW2, wg, st, lc));          // dW2 (+)= dy^T g
+  GS_TRY(mm(d, T, 4 * h, h, dy, true, w2, false, ws.big, Epi::Store, st, lc));    // dg = dy W2
+  GS_TRY(gelu_bwd(d.dt, ws.u, ws.big, ws.big, 4LL * T * h, st));                  // du
+  GS_TRY(mm(d, 4 * h, h, T, ws.big, false, ws.c, false, dW1, wg, st, lc));       // dW1 (+)= du^T c
+  GS_TRY(mm(d, T, h, 4 * h, ws.big, true, w1, false, ws.tmp, Epi::Store, st, lc));  // dc = du W1
+  GS_TRY(cudaMemcpyAsync(ws.dx1, dy, 1LL * T * h * eb, cudaMemcpyDeviceToDevice, st));
+  GS_TRY(layernorm_bwd(d.dt, ws.x1, ws.m2, ws.r2, ws.tmp, ws.dx1, T, h, true, st));  // dx1 = dy + LN2'
+  // attention
+  GS_TRY(mm(d, h, h, T, ws.dx1, false, ws.o, false, dWo, wg, st, lc));           // dWo (+)= dx1^T o
+  GS_TRY(mm(d, T, h, h, ws.dx1, true, wo, false, ws.tmp, Epi::Store, st, lc));    // do = dx1 Wo
+  GS_TRY(attention_bwd(d.dt, ws.qkv, ws.o, ws.lse, ws.tmp, ws.dqkv, ws.attn_work, d.b, d.s, h, d.H, st));
+  GS_TRY(mm(d, 3 * h, h, T, ws.dqkv, false, ws.a, false, dWqkv, wg, st, lc));    // dWqkv (+)= dqkv^T a
+  GS_TRY(mm(d, T, h, 3 * h, ws.dqkv, true, wqkv, false, ws.tmp, Epi::Store, st, lc));  // da = dqkv Wqkv
+  GS_TRY(cudaMemcpyAsync(dx, ws.dx1, 1LL * T * h * eb, cudaMemcpyDeviceToDevice, st));
+  GS_TRY(layernorm_bwd(d.dt, x, ws.m1, ws.r1, ws.tmp, dx, T, h, true, st));      // dx = dx1 + LN1'
+  lc.n += 6;
+  return cudaSuccess;
+}
+
+}  // namespace gs::engine

@@ -1,0 +1,62 @@
+// GPU work of the plan's compute tasks (FwdCompute, RecomputeAndBwd and the
+// head / embedding parts of FixedOps), one micro-batch at a time.  The math
+// is the oracle's (oracle/gs_oracle.c): pre-LN GPT block with exactly 12h^2
+// parameters laid out [Wqkv 3h^2 | Wo h^2 | W1 4h^2 | W2 4h^2], each [out][in].
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace gs::engine {
+
+struct Dims {
+  int b = 1, s = 1, h = 1, H = 1, V = 1;
+  DType dt = DType::BF16;
+  int T() const { return b * s; }
+  int lp() const { return dtype_bytes(dt); }
+  long long P() const { return 12LL * h * h; }
+};
+
+// Per-micro-batch device scratch (allocated once per engine).
+struct Workspace {
+  void *a = nullptr, *qkv = nullptr, *o = nullptr, *x1 = nullptr, *c = nullptr, *u = nullptr, *g = nullptr;
+  void *y = nullptr, *dy = nullptr, *big = nullptr, *dx1 = nullptr, *tmp = nullptr, *dqkv = nullptr, *x0 = nullptr;
+  float *lse = nullptr, *m1 = nullptr, *r1 = nullptr, *m2 = nullptr, *r2 = nullptr, *mz = nullptr, *rz = nullptr;
+  void* attn_work = nullptr;
+  float* logits = nullptr;
+  void* dlogits = nullptr;
+  void* z = nullptr;
+  uint64_t bytes = 0;
+};
+
+// Allocates every buffer of `ws`; returns false on cudaMalloc failure.
+bool alloc_workspace(const Dims& d, Workspace& ws);
+void free_workspace(Workspace& ws);
+
+// Launch accounting (kernels enqueued by this thread's engine work).
+struct LaunchCounter {
+  int n = 0;
+};
+
+// y = block(x).  x, y: [T][h] in dt.  W: 12h^2 in dt.
+cudaError_t layer_forward(const Dims& d, const void* W, const void* x, void* y, Workspace& ws, cudaStream_t st,
+                          LaunchCounter& lc);
+
+// Recompute block(x) and back-propagate dy.  dx: [T][h] (may be ws-free
+// memory distinct from dy).  dW: fp32 12h^2, overwritten when `first` else
+// accumulated.  When `head` is set, dy is produced here from the tied LM head
+// on the recomputed output (layer N-1): loss_sum += CE, dwte += head grad.
+struct HeadArgs {
+  const void* wte = nullptr;  // [V][h] dt
+  float* dwte = nullptr;      // [V][h] fp32
+  const int32_t* tokens = nullptr;  // [b][s+1]
+  float scale = 1.0f;         // 1 / (T * M * dp)
+  double* loss_sum = nullptr;
+};
+cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const void* dy, void* dx, float* dW,
+                           bool first, const HeadArgs* head, Workspace& ws, cudaStream_t st, LaunchCounter& lc);
+
+}  // namespace gs::engine

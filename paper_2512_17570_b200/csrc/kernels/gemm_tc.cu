@@ -1,0 +1,416 @@
+// sm_100a tensor-core GEMM for the bf16 layer executor:
+//   TMA (cp.async.bulk.tensor, 128B swizzle) -> 4-stage shared-memory ring
+//   -> tcgen05.mma.cta_group::1.kind::f16 issued by one elected thread
+//   -> fp32 accumulators in TMEM (two buffers, so the epilogue of tile i
+//      overlaps the MMAs of tile i+1) -> tcgen05.ld epilogue warps with the
+//      layer's fused epilogues (residual add, GELU, fp32 gradient accumulate).
+// Persistent: one CTA per SM walks the output tiles.  Operands may be
+// K-major or MN-major (transposed) so forward (X W^T), data-gradient (dY W)
+// and weight-gradient (dY^T X) all run without transpose copies.
+#include <cuda.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace gs {
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
+constexpr int kThreads = 256;
+
+template <int BN> struct TileCfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 32 consecutive fp32 columns: thread i gets its lane's 32 values.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 version bits.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// Operand tile in shared memory, as the UMMA reads it for k-step `ks`
+// (16 elements of K):
+//  K-major : rows of 128 B (64 K-elements), 8-row atoms of 1 KB; the k-step
+//            moves the start address 32 B inside the swizzle atom.
+//  MN-major: 64-element MN blocks, each [BK rows][128 B]; 8 K-rows per atom;
+//            LBO = distance between MN blocks, SBO = between 8-row K groups.
+template <bool MN>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int ks) {
+  if (!MN) return smem_desc(base + ks * 32, 16, 1024);
+  return smem_desc(base + ks * 16 * 128, BK * 128, 1024);
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__host__ __device__ constexpr uint32_t instr_desc() {
+  return (1u << 4)            // D format f32
+         | (1u << 7)          // A bf16
+         | (1u << 10)         // B bf16
+         | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const float (&v)[32], int row, int col, int M, int N, int ldc,
+                                               void* C, const bf16* R, bf16* G) {
+  if (row >= M) return;
+  const long long o = (long long)row * ldc + col;
+  if constexpr (EPI == (int)Epi::AccumF32 || EPI == (int)Epi::StoreF32) {
+    float4* c = reinterpret_cast<float4*>((float*)C + o);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      if (EPI == (int)Epi::AccumF32) {
+        const float4 y = c[q];
+        x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
+      }
+      c[q] = x;
+    }
+  } else {
+  float w[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) w[i] = v[i];
+  if (EPI == (int)Epi::AddResidual) {
+    const uint4* r = reinterpret_cast<const uint4*>(R + o);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 x = r[q];
+      const uint32_t u[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const __nv_bfloat162 p = *reinterpret_cast<const __nv_bfloat162*>(&u[j]);
+        w[8 * q + 2 * j] += __bfloat162float(p.x);
+        w[8 * q + 2 * j + 1] += __bfloat162float(p.y);
+      }
+    }
+  }
+  uint4* c = reinterpret_cast<uint4*>((bf16*)C + o);
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    c[q] = make_uint4(pack_bf16(w[8 * q], w[8 * q + 1]), pack_bf16(w[8 * q + 2], w[8 * q + 3]),
+                      pack_bf16(w[8 * q + 4], w[8 * q + 5]), pack_bf16(w[8 * q + 6], w[8 * q + 7]));
+  if (EPI == (int)Epi::StoreGelu) {
+    uint4* g = reinterpret_cast<uint4*>(G + o);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = gelu_f(__bfloat162float(__float2bfloat16_rn(w[8 * q + j])));
+      g[q] = make_uint4(pack_bf16(r[0], r[1]), pack_bf16(r[2], r[3]), pack_bf16(r[4], r[5]), pack_bf16(r[6], r[7]));
+    }
+  }
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
+                   int N, int K, void* C, const bf16* R, bf16* G, int ldc) {
+  using Cfg = TileCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + S * Cfg::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = M / BM, nt = N / BN, kt = K / BK;
+  const int tiles = mt * nt;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(Cfg::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===== TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+        for (int kb = 0; kb < kt; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], Cfg::kStageBytes);
+          uint8_t* sa = smem_a + stage * Cfg::kABytes;
+          uint8_t* sb = smem_b + stage * Cfg::kBBytes;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d(sa, &map_a, &full[stage], k0, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * BK * 128, &map_a, &full[stage], m0 + 64 * j, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(sb, &map_b, &full[stage], k0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * BK * 128, &map_b, &full[stage], n0 + 64 * j, k0);
+          }
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (one thread)
+    constexpr uint32_t idesc = instr_desc<BN, A_MN, B_MN>();
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < kt; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(smem_a + stage * Cfg::kABytes);
+          const uint32_t b0 = smem_u32(smem_b + stage * Cfg::kBBytes);
+#pragma unroll
+          for (int ks = 0; ks < BK / 16; ++ks)
+            tc_mma(d_tmem, operand_desc<A_MN>(a0, ks), operand_desc<B_MN>(b0, ks), idesc, (kb | ks) != 0);
+          tc_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+        }
+        __syncwarp();
+        if (++stage == S) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (= tile rows)
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+        epilogue_chunk<EPI>(v, row, n0 + c, M, N, ldc, C, R, G);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::kTmemCols));
+  }
+}
+
+// ------------------------------------------------------------- host side
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor [outer][inner] (inner contiguous), box {64, box_outer}.
+bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_outer) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {inner * 2};
+  const cuuint32_t box[2] = {64, box_outer};
+  const cuuint32_t elem[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, elem,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+cudaError_t launch(const GemmArgs& g, cudaStream_t s) {
+  using Cfg = TileCfg<BN>;
+  CUtensorMap ma, mb;
+  const bool ok_a = A_MN ? make_map(&ma, g.A, g.M, g.K, BK) : make_map(&ma, g.A, g.K, g.M, BM);
+  const bool ok_b = B_MN ? make_map(&mb, g.B, g.N, g.K, BK) : make_map(&mb, g.B, g.K, g.N, BN);
+  if (!ok_a || !ok_b) return cudaErrorInvalidValue;
+  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = (g.M / BM) * (g.N / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  count_launch(); kern<<<grid, kThreads, Cfg::kSmemBytes, s>>>(ma, mb, g.M, g.N, g.K, g.C, (const bf16*)g.R, (bf16*)g.G,
+                                               g.ldc ? g.ldc : g.N);
+  return cudaGetLastError();
+}
+
+template <int BN, bool A_MN, bool B_MN>
+cudaError_t launch_epi(const GemmArgs& g, cudaStream_t s) {
+  switch (g.epi) {
+    case Epi::Store: return launch<BN, A_MN, B_MN, 0>(g, s);
+    case Epi::AddResidual: return launch<BN, A_MN, B_MN, 1>(g, s);
+    case Epi::AccumF32: return launch<BN, A_MN, B_MN, 2>(g, s);
+    case Epi::StoreGelu: return launch<BN, A_MN, B_MN, 3>(g, s);
+    case Epi::StoreF32: return launch<BN, A_MN, B_MN, 4>(g, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int BN>
+cudaError_t launch_bn(const GemmArgs& g, cudaStream_t s) {
+  const bool a_mn = !g.a_kmajor, b_mn = !g.b_kmajor;
+  if (!a_mn && !b_mn) return launch_epi<BN, false, false>(g, s);
+  if (!a_mn && b_mn) return launch_epi<BN, false, true>(g, s);
+  if (a_mn && b_mn) return launch_epi<BN, true, true>(g, s);
+  return launch_epi<BN, true, false>(g, s);
+}
+
+}  // namespace
+
+bool gemm_tc_supported(const GemmArgs& g) {
+  if (g.dt != DType::BF16) return false;
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return false;
+  if (g.M % BM || g.K % BK || g.N % 128) return false;
+  const int ldc = g.ldc ? g.ldc : g.N;
+  if (ldc % 8) return false;
+  const uintptr_t align = reinterpret_cast<uintptr_t>(g.A) | reinterpret_cast<uintptr_t>(g.B) |
+                          reinterpret_cast<uintptr_t>(g.C) | reinterpret_cast<uintptr_t>(g.R) |
+                          reinterpret_cast<uintptr_t>(g.G);
+  if (align & 15) return false;
+  return encode_fn() != nullptr;
+}
+
+cudaError_t gemm_tc(const GemmArgs& g, cudaStream_t s) {
+  if (!gemm_tc_supported(g)) return cudaErrorInvalidValue;
+  return (g.N % 256 == 0) ? launch_bn<256>(g, s) : launch_bn<128>(g, s);
+}
+
+}  // namespace gs

@@ -1,0 +1,239 @@
+"""GPU numerics of the sm_100a kernels, called through the C-ABI.
+
+Floating-point kernels are checked against a plain PyTorch fp32 reference of
+the same op on the same (bf16-rounded) inputs; the fused Adam is checked
+against the CPU oracle's Adam (oracle/gs_oracle.c) bit-near.
+Tolerances are stated per test.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle_bindings as ob  # noqa: E402
+import paper_2512_17570_b200 as gs  # noqa: E402
+
+F32, BF16 = 0, 1
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch.device("cuda:0")
+
+
+def gemm(dtype, A, a_k, B, b_k, M, N, K, epi, C_=None, R=None, G=None, simt=False):
+    lib = gs.lib()
+    fn = lib.gs_gemm_simt if simt else lib.gs_gemm
+    gs.check(fn(dtype, M, N, K, ptr(A), int(a_k), ptr(B), int(b_k), ptr(C_), ptr(R), ptr(G), epi, None))
+    torch.cuda.synchronize()
+
+
+def rel(a, b):
+    a, b = a.double(), b.double()
+    return float((a - b).norm() / b.norm())
+
+
+SHAPES = [(128, 128, 64), (256, 384, 128), (512, 256, 320), (1024, 2048, 512), (4096, 6144, 2048)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("a_k,b_k", [(True, True), (True, False), (False, False), (False, True)])
+def test_tcgen05_gemm_matches_fp32_reference(M, N, K, a_k, b_k):
+    d = dev()
+    torch.manual_seed(M + N + K)
+    Am = torch.randn(M, K, device=d).bfloat16()
+    Bm = torch.randn(N, K, device=d).bfloat16()
+    A = Am.contiguous() if a_k else Am.t().contiguous()
+    B = Bm.contiguous() if b_k else Bm.t().contiguous()
+    ref = Am.float() @ Bm.float().t()
+    # bf16 store: output rounding 2^-9 relative; fp32 accumulate: order only
+    out = torch.empty(M, N, device=d, dtype=torch.bfloat16)
+    gemm(BF16, A, a_k, B, b_k, M, N, K, 0, out)
+    assert rel(out.float(), ref) < 5e-3
+    acc = torch.randn(M, N, device=d)
+    want = acc + ref
+    gemm(BF16, A, a_k, B, b_k, M, N, K, 2, acc)
+    assert rel(acc, want) < 1e-5
+    f32 = torch.empty(M, N, device=d)
+    gemm(BF16, A, a_k, B, b_k, M, N, K, 4, f32)
+    assert rel(f32, ref) < 1e-5
+
+
+def test_tcgen05_fused_epilogues():
+    d = dev()
+    M, N, K = 512, 512, 256
+    A = torch.randn(M, K, device=d).bfloat16()
+    B = torch.randn(N, K, device=d).bfloat16()
+    R = torch.randn(M, N, device=d).bfloat16()
+    ref = A.float() @ B.float().t()
+    out = torch.empty(M, N, device=d, dtype=torch.bfloat16)
+    gemm(BF16, A, True, B, True, M, N, K, 1, out, R=R)
+    assert rel(out.float(), ref + R.float()) < 5e-3
+    u = torch.empty(M, N, device=d, dtype=torch.bfloat16)
+    g = torch.empty(M, N, device=d, dtype=torch.bfloat16)
+    gemm(BF16, A, True, B, True, M, N, K, 3, u, G=g)
+    assert rel(u.float(), ref) < 5e-3
+    assert rel(g.float(), torch.nn.functional.gelu(u.float(), approximate="tanh")) < 5e-3
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 64, 64), (100, 70, 33), (256, 192, 128)])
+@pytest.mark.parametrize("a_k,b_k", [(True, True), (True, False), (False, False)])
+def test_simt_gemm_fp32(M, N, K, a_k, b_k):
+    d = dev()
+    Am = torch.randn(M, K, device=d)
+    Bm = torch.randn(N, K, device=d)
+    A = Am.contiguous() if a_k else Am.t().contiguous()
+    B = Bm.contiguous() if b_k else Bm.t().contiguous()
+    out = torch.empty(M, N, device=d)
+    gemm(F32, A, a_k, B, b_k, M, N, K, 0, out)
+    assert rel(out, Am.double() @ Bm.double().t()) < 1e-6
+
+
+def attn_reference(qkv, b, s, h, H):
+    d = h // H
+    q, k, v = qkv.float().view(b, s, 3, H, d).permute(2, 0, 3, 1, 4)
+    att = (q @ k.transpose(-1, -2)) / d ** 0.5
+    att = att.masked_fill(torch.ones(s, s, device=qkv.device, dtype=torch.bool).triu(1), float("-inf"))
+    lse = torch.logsumexp(att, -1)
+    o = att.softmax(-1) @ v
+    return o.transpose(1, 2).reshape(b * s, h), lse
+
+
+@pytest.mark.parametrize("dtype,b,s,h,H", [(BF16, 2, 256, 512, 4), (BF16, 1, 512, 512, 8), (BF16, 2, 2048, 2048, 16),
+                                           (F32, 2, 32, 64, 4), (BF16, 2, 32, 64, 4)])
+def test_attention_fwd_bwd(dtype, b, s, h, H):
+    d = dev()
+    tdt = torch.bfloat16 if dtype == BF16 else torch.float32
+    torch.manual_seed(0)
+    qkv = (torch.randn(b * s, 3 * h, device=d) * 0.5).to(tdt)
+    o = torch.empty(b * s, h, device=d, dtype=tdt)
+    lse = torch.empty(b * H * s, device=d)
+    lib = gs.lib()
+    gs.check(lib.gs_attention_fwd(dtype, ptr(qkv), ptr(o), ptr(lse), b, s, h, H, None))
+    torch.cuda.synchronize()
+    x = qkv.float().clone().requires_grad_(True)
+    o_ref, lse_ref = attn_reference(x, b, s, h, H)
+    tol = 1e-2 if dtype == BF16 else 1e-5
+    assert rel(o.float(), o_ref) < tol
+    assert rel(lse.view(b, H, s), lse_ref) < 1e-4
+    dout = torch.randn(b * s, h, device=d).to(tdt)
+    o_ref.backward(dout.float())
+    dqkv = torch.empty_like(qkv)
+    work = torch.empty(lib.gs_attention_bwd_workspace(b, s, h, H), dtype=torch.uint8, device=d)
+    gs.check(lib.gs_attention_bwd(dtype, ptr(qkv), ptr(o), ptr(lse), ptr(dout), ptr(dqkv), ptr(work), b, s, h, H,
+                                  None))
+    torch.cuda.synchronize()
+    g = x.grad
+    for part in range(3):  # dq, dk, dv separately
+        sl = slice(part * h, (part + 1) * h)
+        assert rel(dqkv[:, sl].float(), g[:, sl]) < (2e-2 if dtype == BF16 else 1e-5), part
+
+
+@pytest.mark.parametrize("dtype,h", [(F32, 64), (F32, 2048), (BF16, 2048), (F32, 12288)])
+def test_layernorm(dtype, h):
+    d = dev()
+    tdt = torch.bfloat16 if dtype == BF16 else torch.float32
+    rows = 64
+    x = (torch.randn(rows, h, device=d) * 2 + 0.5).to(tdt)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device=d)
+    rstd = torch.empty(rows, device=d)
+    lib = gs.lib()
+    gs.check(lib.gs_layernorm_fwd(dtype, ptr(x), ptr(y), ptr(mean), ptr(rstd), rows, h, None))
+    xr = x.float().clone().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xr, (h,), eps=1e-5)
+    torch.cuda.synchronize()
+    tol = 1e-2 if dtype == BF16 else 1e-5
+    assert rel(y.float(), yr) < tol
+    dy = torch.randn_like(x)
+    yr.backward(dy.float())
+    dx = torch.empty_like(x)
+    gs.check(lib.gs_layernorm_bwd(dtype, ptr(x), ptr(mean), ptr(rstd), ptr(dy), ptr(dx), rows, h, 0, None))
+    torch.cuda.synchronize()
+    assert rel(dx.float(), xr.grad) < tol
+
+
+@pytest.mark.parametrize("n", [1, 7, 1024, 1 << 20])
+def test_fused_adam_matches_oracle(n):
+    d = dev()
+    rng = np.random.default_rng(n)
+    p = rng.standard_normal(n).astype(np.float32)
+    m = rng.standard_normal(n).astype(np.float32) * 0.1
+    v = np.abs(rng.standard_normal(n).astype(np.float32)) * 0.01
+    g = rng.standard_normal(n).astype(np.float32)
+    state = torch.tensor(np.stack([p, m, v], 1).reshape(-1), device=d)
+    grad = torch.tensor(g, device=d)
+    lp = torch.empty(n, device=d, dtype=torch.bfloat16)
+    gs.check(gs.lib().gs_adam_step_packed(1e-3, 0.9, 0.95, 1e-8, 0.01, 3, 0.5, ptr(state), ptr(grad), ptr(lp), BF16,
+                                          n, None))
+    torch.cuda.synchronize()
+    orc = ob.oracle()
+    a = ob.GsoAdam(1e-3, 0.9, 0.95, 1e-8, 0.01)
+    f = lambda x: x.ctypes.data_as(C.POINTER(C.c_float))  # noqa: E731
+    orc.gso_adam_step(C.byref(a), f(p), f(m), f(v), f(g), C.c_longlong(n), 3, C.c_float(0.5))
+    got = state.view(n, 3).cpu().numpy()
+    assert np.allclose(got[:, 0], p, rtol=2e-6, atol=1e-7)
+    assert np.allclose(got[:, 1], m, rtol=2e-6, atol=1e-9)
+    assert np.allclose(got[:, 2], v, rtol=2e-6, atol=1e-12)
+    assert torch.equal(lp, torch.tensor(p, device=d).bfloat16())
+
+
+def test_layer_forward_backward_fp32_matches_oracle():
+    d = dev()
+    g = ob.TINY
+    cfg = g.cfg()
+    orc = ob.oracle()
+    layers, _ = ob.init_params(g)
+    w = layers[1]
+    T = g.mb_size * g.seq
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((T, g.hidden)).astype(np.float32)
+    dy = rng.standard_normal((T, g.hidden)).astype(np.float32)
+    f = lambda a: a.ctypes.data_as(C.POINTER(C.c_float))  # noqa: E731
+    y_ref = np.empty_like(x)
+    orc.gso_layer_fwd(C.byref(cfg), f(w), f(x), f(y_ref))
+    dx_ref = np.empty_like(x)
+    dw_ref = np.zeros_like(w)
+    orc.gso_layer_bwd(C.byref(cfg), f(w), f(x), f(dy), f(dx_ref), f(dw_ref))
+    W, X, DY = (torch.tensor(a, device=d) for a in (w, x, dy))
+    Y = torch.empty_like(X)
+    lib = gs.lib()
+    gs.check(lib.gs_layer_forward(F32, g.mb_size, g.seq, g.hidden, g.heads, ptr(W), ptr(X), ptr(Y), None))
+    assert rel(Y.cpu(), torch.tensor(y_ref)) < 1e-5
+    DX = torch.empty_like(X)
+    DW = torch.empty_like(W)
+    gs.check(lib.gs_layer_backward(F32, g.mb_size, g.seq, g.hidden, g.heads, ptr(W), ptr(X), ptr(DY), ptr(DX),
+                                   ptr(DW), 1, None))
+    assert rel(DX.cpu(), torch.tensor(dx_ref)) < 1e-5
+    assert rel(DW.cpu(), torch.tensor(dw_ref)) < 1e-5
+
+
+def test_layer_bf16_tensor_core_path_tracks_fp32():
+    """bf16 layer at a tcgen05-tiled shape vs the same layer in fp32 (reported
+    separately from the fp32 parity mode; tolerance 3e-2 relative)."""
+    d = dev()
+    b, s, h, H = 2, 256, 512, 4
+    torch.manual_seed(1)
+    W = torch.randn(12 * h * h, device=d) * 0.02
+    X = torch.randn(b * s, h, device=d)
+    DY = torch.randn(b * s, h, device=d) * 0.1
+    lib = gs.lib()
+    out = {}
+    for dt, tdt in ((F32, torch.float32), (BF16, torch.bfloat16)):
+        Wd, Xd, DYd = W.to(tdt), X.to(tdt), DY.to(tdt)
+        Y = torch.empty_like(Xd)
+        gs.check(lib.gs_layer_forward(dt, b, s, h, H, ptr(Wd), ptr(Xd), ptr(Y), None))
+        DX = torch.empty_like(Xd)
+        DW = torch.empty(12 * h * h, device=d)
+        gs.check(lib.gs_layer_backward(dt, b, s, h, H, ptr(Wd), ptr(Xd), ptr(DYd), ptr(DX), ptr(DW), 1, None))
+        out[dt] = (Y.float(), DX.float(), DW)
+    for a, bb in zip(out[BF16], out[F32]):
+        assert rel(a, bb) < 3e-2
