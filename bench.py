@@ -1,0 +1,319 @@
+"""bench.py — throughput of the GreedySnake hot path on B200.
+
+A step is one training iteration of the vertical (snake) plan with the
+alpha-delayed optimizer step, executed by the B200 executor through the
+C-ABI (gs_engine_run): every plan task runs for real (tcgen05 GEMMs, flash
+attention, fused Adam, PCIe DMA of params / checkpoints / gradients, NVMe I/O
+when the split puts data on SSD).
+
+Workload (BASELINE.json configs[1]; GPT-65B, the metric's headline model, does
+not fit this box's 196 GB DRAM / 80 GB disk): GPT-1.3B (N=24, h=2048, 16 heads,
+s=2048, b=2, vocab 50304), M=16 micro-batches per iteration, split (1,1,1)
+(all params / checkpoints / optimizer state CPU-resident), alpha=0.2, bf16.
+
+--impl reference times the reference CPU path on the host cores: the
+reference's offsim carries no training arithmetic, so the timed CPU
+implementation is the C oracle port (oracle/gs_oracle.c, fp32, OpenMP) on a
+bounded sample (one layer's forward + recompute + backward at the workload's
+b*s tokens... see `cpu_sample`), extrapolated to the model.
+
+Multi-GPU: one process per GPU (torchrun); each rank runs its own replica of
+the workload (dp sharding with NCCL is not wired into the executor yet, so
+scaling is "weak", replicas only) and rank 0 reports max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+CONFIGS = {
+    # name: (N, h, heads, s, b, vocab, M, split, alpha)
+    "gpt1.3b": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2),
+    "gpt1.3b-ssd-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 0.0), 0.2),
+    "tiny": (4, 64, 4, 32, 2, 128, 4, (0.0, 0.0, 0.0), 0.25),
+}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        loaded = [x for x in sm if x > 500] or sm
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for name, v in zip(names, r[3:]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def pcie_bandwidth(torch, nbytes=1 << 30):
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    out = {}
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(3):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        out[name] = 3 * nbytes / (a.elapsed_time(b) / 1e3)
+    del h, d
+    return out
+
+
+def cpu_sample(cfg_name: str, budget_s: float = 20.0):
+    """Time the oracle port (fp32 C, OpenMP, all host threads) on one layer's
+    forward + recompute-and-backward at the workload's micro-batch geometry.
+    Returns (seconds per layer-microbatch, tokens, threads, description)."""
+    import oracle_bindings as ob
+    N, h, H, s, b, V, M, split, alpha = CONFIGS[cfg_name]
+    # bounded: b=1 and a shorter sequence keep one sample ~10 s on 16 cores
+    sb, ss = 1, min(s, 1024)
+    g = ob.Geometry(n_layers=N, hidden=h, heads=H, seq=ss, mb_size=sb, vocab=V)
+    cfg = g.cfg()
+    lib = ob.oracle()
+    rng = np.random.default_rng(0)
+    w = (rng.standard_normal(12 * h * h) * 0.02).astype(np.float32)
+    x = rng.standard_normal(sb * ss * h).astype(np.float32)
+    dy = rng.standard_normal(sb * ss * h).astype(np.float32) * 0.01
+    y = np.empty_like(x)
+    dx = np.empty_like(x)
+    dw = np.zeros_like(w)
+    f = lambda a: a.ctypes.data_as(C.POINTER(C.c_float))  # noqa: E731
+    t0 = time.perf_counter()
+    lib.gso_layer_fwd(C.byref(cfg), f(w), f(x), f(y))
+    lib.gso_layer_bwd(C.byref(cfg), f(w), f(x), f(dy), f(dx), f(dw))
+    dt = time.perf_counter() - t0
+    desc = (f"oracle C fp32 port, {lib.gso_num_threads()} threads: 1 layer fwd + recompute+bwd at b={sb}, s={ss} "
+            f"(h={h}); tokens/s = b*s / (N * t_layer); head, embedding and Adam not included")
+    return dt, sb * ss, lib.gso_num_threads(), desc
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    N, h, H, s, b, V, M, split, alpha = CONFIGS[args.config]
+    for _ in range(args.warmup if args.config == "tiny" else 0):
+        cpu_sample(args.config)
+    times = []
+    for _ in range(args.steps):
+        dt, toks, threads, desc = cpu_sample(args.config)
+        times.append(dt)
+    t_layer = float(np.mean(times))
+    value = toks / (N * t_layer)
+    line = {"impl": "reference", "metric": "tokens/sec (GPT-1.3B vertical schedule, 1 B200 vs host CPU)",
+            "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_layer * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": config_dict(args),
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": desc},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args):
+    N, h, H, s, b, V, M, split, alpha = CONFIGS[args.config]
+    return {"workload": f"{args.config}: GPT N={N} h={h} heads={H} s={s} b={b} vocab={V}, vertical schedule, "
+                        f"M={M} micro-batches/iteration, split(x_ckpt,x_param,x_opt)={split}, alpha={alpha}",
+            "global_batch": M * b * max(args.gpus, 1), "seq_len": s, "microbatches": M, "alpha": alpha,
+            "split": list(split), "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single",
+            "l2": "working set (2.4 GB params/iteration streamed) >> 126 MB L2; no flush needed"}
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    import paper_2512_17570_b200 as gs
+    import oracle_bindings as ob
+    N, h, H, s, b, V, M, split, alpha = CONFIGS[args.config]
+    M = args.microbatches or M
+    model = gs.ModelSpec(N, h, H, s, b, 2, 4, 3, 1)
+    plan = gs.build_vertical(model, M, gs.StorageSplit(*split), alpha)
+    nvme = os.environ.get("GS_NVME_DIR", "/tmp")
+    eng = gs.Engine(plan, model, V, gs.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0), seed=1234 + rank,
+                    device=torch.cuda.current_device(), nvme_dir=nvme, opt_tier=0, profile=True)
+    g = ob.Geometry(n_layers=N, hidden=h, heads=H, seq=s, mb_size=b, vocab=V)
+    K, W = args.steps, args.warmup
+    tokens = ob.make_tokens(g, W + 2 * K, M, seed=7 + rank)
+    # warm-up (untimed)
+    eng.run(tokens[:W])
+    # device-resident tokens: `value`
+    dtok = torch.tensor(tokens[W:W + K], device="cuda")
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        rep = eng.run(None, iterations=K, tokens_on_device=True, device_ptr=dtok.data_ptr())
+    torch.cuda.synchronize()
+    barrier(world)
+    dev_ms = max_over_ranks(rep.total_ms, world)
+    # end-to-end through the public call: host tokens, losses read back
+    barrier(world)
+    t0 = time.perf_counter()
+    rep_e2e = eng.run(tokens[W + K:W + 2 * K])
+    e2e_wall = time.perf_counter() - t0
+    e2e_ms = max_over_ranks(rep_e2e.total_ms, world)
+    barrier(world)
+    prof = eng.kernel_profile()
+    eng.close()
+    if rank != 0:
+        return
+    tokens_per_step = M * b * s
+    value = world * K * tokens_per_step / (dev_ms / 1e3)
+    e2e_value = world * K * tokens_per_step / (e2e_ms / 1e3)
+    hbm, tf_burst, tf_sust, src = peaks()
+    # dominant kernel: the tcgen05 GEMM (fp32 accumulate, bf16 operands)
+    gemm_flops, gemm_ms, gemm_launches = prof.get("gemm", (0.0, 0.0, 0))
+    achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    roof = {"bound": "tensor", "achieved": achieved, "peak": tf_sust, "unit": "TFLOP/s",
+            "frac": achieved / tf_sust, "traffic": None, "kernel": "tc_gemm_kernel (tcgen05, all layer GEMMs)",
+            "launches": gemm_launches, "avg_launch_ms": gemm_ms / max(gemm_launches, 1),
+            "flops_per_launch": gemm_flops / max(gemm_launches, 1),
+            "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)"}
+    # iteration roofline (north star): max of compute at peak and ledger bytes over measured links
+    bw = pcie_bandwidth(torch)
+    led = rep.ledger
+    flops_iter = N * 4 * (24 * h * h + 2 * s * h) * tokens_per_step
+    t_comp = flops_iter / (tf_sust * 1e12)
+    t_h2d = float(led[0].sum()) / bw["h2d"]
+    t_d2h = float(led[1].sum()) / bw["d2h"]
+    t_roof = max(t_comp, t_h2d, t_d2h)
+    ms_step = dev_ms / K
+    other = {k: v for k, v in prof.items() if k != "gemm"}
+    line = {"metric": "tokens/sec (GPT-1.3B vertical schedule + alpha-delayed optimizer, BASELINE configs[1])",
+            "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic tokens (uniform ids), random-init N(0,0.02) weights",
+            "config": config_dict(args),
+            "e2e": {"value": e2e_value, "unit": "tokens/s", "wall_s": e2e_wall,
+                    "h2d_bytes_per_step": int(M * b * (s + 1) * 4 + led[0].sum() + rep.extension[0].sum()),
+                    "d2h_bytes_per_step": int(8 + led[1].sum() + rep.extension[1].sum()),
+                    "note": "tokens from pageable host memory copied per step; PCIe bytes are the plan's offload "
+                            "traffic + GPU-optimizer extension, all inside the timed region"},
+            "gpu_launches": rep.gpu_launches,
+            "roofline": roof,
+            "iteration_roofline": {"t_roof_ms": t_roof * 1e3, "t_measured_ms": ms_step, "frac": t_roof / (ms_step / 1e3),
+                                   "t_compute_ms": t_comp * 1e3, "t_pcie_h2d_ms": t_h2d * 1e3,
+                                   "t_pcie_d2h_ms": t_d2h * 1e3, "pcie_h2d_gbs": bw["h2d"] / 1e9,
+                                   "pcie_d2h_gbs": bw["d2h"] / 1e9, "flops_per_iteration": flops_iter,
+                                   "compute_roofline_tokens_s": tokens_per_step / t_comp},
+            "offload_gb_per_iteration": {"ledger_h2d": float(led[0].sum()) / 1e9, "ledger_d2h": float(led[1].sum()) / 1e9,
+                                         "ssd_read": float(led[2].sum()) / 1e9, "ssd_write": float(led[3].sum()) / 1e9,
+                                         "extension_h2d": float(rep.extension[0].sum()) / 1e9,
+                                         "extension_d2h": float(rep.extension[1].sum()) / 1e9},
+            "ledger_equals_plan": bool(np.array_equal(led, gs.plan_traffic(plan))),
+            "kernel_ms_per_step": {k: v[1] / K for k, v in prof.items()},
+            "losses": rep.losses,
+            "clocks": clk.summary()}
+    if not args.no_cpu_baseline:
+        dt, toks, threads, desc = cpu_sample(args.config)
+        line["cpu_baseline"] = {"value": toks / (N * dt), "unit": "tokens/s", "cores": threads, "kind": "port",
+                                "sample": desc}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="gpt1.3b", choices=sorted(CONFIGS))
+    ap.add_argument("--microbatches", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

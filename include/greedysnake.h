@@ -106,6 +106,7 @@ typedef struct gs_engine_config {
   int odirect;             /* 1: O_DIRECT on the NVMe tier */
   int opt_tier;            /* 0 auto, 1 HBM, 2 pinned host */
   int record_trace;
+  int profile_kernels;     /* CUDA-event timing per kernel class (gs_engine_kernel_profile) */
 } gs_engine_config;
 
 typedef struct gs_run_report {
@@ -140,6 +141,9 @@ int gs_engine_flush(gs_engine* engine);
 /* fp32 master weights: layers [N][12 h^2], fixed [(V + s) h]; either may be NULL */
 int gs_engine_read_params(gs_engine* engine, float* layers, float* fixed);
 int gs_engine_read_moments(gs_engine* engine, float* layer_m, float* layer_v);
+/* per kernel class of the last run: 0 gemm, 1 attention_fwd, 2 attention_bwd,
+   3 layernorm, 4 other — algorithmic flops, CUDA-event ms, launches */
+int gs_engine_kernel_profile(gs_engine* engine, double flops[5], double ms[5], int launches[5]);
 /* trace of the last run (last <= 3 iterations when record_trace was set) */
 int gs_engine_trace(gs_engine* engine, gs_trace_record* out, int cap, int* n);
 

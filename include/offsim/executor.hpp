@@ -51,6 +51,7 @@ struct ExecConfig {
   bool odirect = true;
   OptTier opt_tier = OptTier::Auto;
   bool record_trace = false;   // per-task timestamps (adds event records)
+  bool profile_kernels = false;  // CUDA-event timing per kernel class on the compute stream
   int rank = 0, world = 1;     // data parallel (model.data_parallel_degree == world)
 };
 
@@ -96,6 +97,15 @@ class Executor {
   void read_params(float* layers, float* fixed);
   // fp32 optimizer moments, same layout as read_params.
   void read_moments(float* layer_m, float* layer_v);
+  // Per kernel class of the last run (profile_kernels): algorithmic flops,
+  // summed CUDA-event milliseconds and launches.  Classes: gemm,
+  // attention_fwd, attention_bwd, layernorm, other.
+  struct KernelTotals {
+    double flops[5];
+    double ms[5];
+    int launches[5];
+  };
+  KernelTotals kernel_profile() const;
 
   const SchedulePlan& plan() const;
   const ExecConfig& config() const;

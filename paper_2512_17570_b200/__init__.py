@@ -86,7 +86,7 @@ class _EngineConfig(C.Structure):
     _fields_ = [("model", _ModelSpec), ("vocab_size", C.c_int), ("lr", C.c_float), ("beta1", C.c_float),
                 ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float), ("seed", C.c_uint64),
                 ("device", C.c_int), ("nvme_dir", C.c_char_p), ("odirect", C.c_int), ("opt_tier", C.c_int),
-                ("record_trace", C.c_int)]
+                ("record_trace", C.c_int), ("profile_kernels", C.c_int)]
 
 
 class _RunReport(C.Structure):
@@ -328,14 +328,14 @@ class Engine:
 
     def __init__(self, plan: SchedulePlan, model: ModelSpec, vocab_size: int, adam: AdamConfig = AdamConfig(),
                  seed: int = 42, device: int = 0, nvme_dir: str = "/tmp", odirect: bool = True, opt_tier: int = 0,
-                 record_trace: bool = False):
+                 record_trace: bool = False, profile: bool = False):
         self.model = model
         self.vocab_size = vocab_size
         self.plan = plan
         self.microbatches = plan.as_dict()["microbatches"] if len(plan) < 20000 else None
         self._nvme = nvme_dir.encode()
         cfg = _EngineConfig(model._c(), vocab_size, adam.lr, adam.beta1, adam.beta2, adam.eps, adam.weight_decay,
-                            seed, device, self._nvme, int(odirect), opt_tier, int(record_trace))
+                            seed, device, self._nvme, int(odirect), opt_tier, int(record_trace), int(profile))
         h = C.c_void_p()
         check(lib().gs_engine_create(plan.handle, C.byref(cfg), C.byref(h)))
         self._h = h
@@ -372,6 +372,13 @@ class Engine:
                           t_end_ms=r.t_end_ms, bytes=r.bytes, physical_bytes=r.physical_bytes) for r in arr]
         return RunReport(rep.total_ms, rep.iterations, rep.gpu_launches, list(losses), _ledger(rep.ledger),
                          _ledger(rep.extension), _ledger(rep.physical), rep.gpu_bytes, rep.host_pinned_bytes, trace)
+
+    def kernel_profile(self) -> dict:
+        """{class: (flops, ms, launches)} of the last run (profile=True)."""
+        f, m, n = (C.c_double * 5)(), (C.c_double * 5)(), (C.c_int * 5)()
+        check(lib().gs_engine_kernel_profile(self._h, f, m, n))
+        names = ("gemm", "attention_fwd", "attention_bwd", "layernorm", "other")
+        return {k: (f[i], m[i], n[i]) for i, k in enumerate(names) if n[i]}
 
     def flush(self) -> None:
         check(lib().gs_engine_flush(self._h))

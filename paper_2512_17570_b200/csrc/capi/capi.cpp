@@ -212,6 +212,7 @@ int gs_engine_create(const gs_plan* plan, const gs_engine_config* c, gs_engine**
     cfg.odirect = c->odirect != 0;
     cfg.opt_tier = static_cast<offsim::OptTier>(c->opt_tier);
     cfg.record_trace = c->record_trace != 0;
+    cfg.profile_kernels = c->profile_kernels != 0;
     auto e = std::make_unique<gs_engine>();
     e->ex = std::make_unique<offsim::Executor>(plan->plan, cfg);
     *out = e.release();
@@ -245,6 +246,16 @@ int gs_engine_read_params(gs_engine* engine, float* layers, float* fixed) {
 }
 int gs_engine_read_moments(gs_engine* engine, float* m, float* v) {
   return guarded([&] { engine->ex->read_moments(m, v); });
+}
+int gs_engine_kernel_profile(gs_engine* engine, double flops[5], double ms[5], int launches[5]) {
+  return guarded([&] {
+    const offsim::Executor::KernelTotals t = engine->ex->kernel_profile();
+    for (int i = 0; i < 5; ++i) {
+      flops[i] = t.flops[i];
+      ms[i] = t.ms[i];
+      launches[i] = t.launches[i];
+    }
+  });
 }
 int gs_engine_trace(gs_engine* engine, gs_trace_record* out, int cap, int* n) {
   return guarded([&] {

@@ -142,6 +142,7 @@ struct Executor::Impl {
   void* fx_lp = nullptr;
   long long n_fixed = 0;
   Workspace ws;
+  KernelProfiler prof;
   std::vector<void*> in_x, out_y, in_g, out_g;  // [2*M] each, index p*M+m
   int32_t* dev_tok[2] = {nullptr, nullptr};
   double* dev_loss = nullptr;  // [loss_cap] per run iteration
@@ -220,7 +221,10 @@ struct Executor::Impl {
   // forward-phase optimizer work (CpuStep, OptState I/O, Param SSD write) is
   // the delayed alpha slice of the previous iteration's step
   bool delayed(const Task& t) const { return fwd_phase[static_cast<size_t>(t.id)] != 0; }
-  void apply_adam(int layer, u64 e0, u64 e1, const float* grad, int step, cudaStream_t st, int it);
+  // src: where SSD-resident state is read from — the NVMe read staging for
+  // plan steps (a plan SSD read precedes each), the image for flush().
+  void apply_adam(int layer, u64 e0, u64 e1, const float* grad, int step, cudaStream_t st, int it,
+                  Src src = Src::ReadStaging);
   void note_ledger(int it, const Task& t, u64 phys);
   void note_ext(int it, LinkKind l, DataKind dk, u64 bytes);
 };
@@ -261,6 +265,7 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   el_now = P - el_late;
 
   cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice");
+  (void)cudaGetLastError();  // do not inherit a stale error of an earlier, unrelated call
   cuda_check(cudaStreamCreateWithFlags(&s_gpu, cudaStreamNonBlocking), "stream");
   cuda_check(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking), "stream");
   cuda_check(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking), "stream");
@@ -291,6 +296,7 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   fx_grad = static_cast<float*>(dmalloc(4 * n_fixed));
   fx_lp = dmalloc(static_cast<u64>(n_fixed) * d.lp());
   if (!alloc_workspace(d, ws)) throw InfeasibleError("executor: device workspace allocation failed");
+  if (cfg.profile_kernels) ws.prof = &prof;
   dev_bytes += ws.bytes;
   for (int i = 0; i < 2 * M; ++i) {
     in_x.push_back(dmalloc(cb));
@@ -337,7 +343,8 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
 Executor::Impl::~Impl() {
   cudaDeviceSynchronize();
   for (auto& a : ev_done)
-    for (cudaEvent_t e : a) cudaEventDestroy(e);
+    for (cudaEvent_t e : a)
+      if (e) cudaEventDestroy(e);
   for (auto& a : ev_start)
     for (cudaEvent_t e : a)
       if (e) cudaEventDestroy(e);
@@ -450,11 +457,18 @@ void Executor::Impl::build_tasks() {
   fwd_phase.assign(n, 0);
   chunk_lo.assign(n, 0);
   {
+    // The backward loop (schedule.cpp:431) starts with layer N-1's parameter
+    // fetch: its SSD read at stage N-2 or, without SSD bytes, its first PCIe
+    // chunk at stage N-1 (the forward fetched layer N-1 at stages N-3 / N-2).
+    // Everything emitted earlier is forward-phase, including the delayed
+    // slice of the previous iteration's optimizer step.
     bool fwd = true;
     std::map<std::pair<int, int>, u64> next_lo;  // (layer, stage) -> running chunk offset
     for (size_t i = 0; i < n; ++i) {
       const Task& t = plan.tasks[i];
-      if (t.kind == TaskKind::RecomputeAndBwd) fwd = false;
+      if (fwd && t.kind == TaskKind::Xfer && t.data == DataKind::Param && t.layer == N - 1 &&
+          ((t.link == LinkKind::SSD_Read && t.stage == N - 2) || (t.link == LinkKind::PCIe_H2D && t.stage == N - 1)))
+        fwd = false;
       fwd_phase[i] = fwd ? 1 : 0;
       if (t.kind == TaskKind::Xfer && t.data == DataKind::Param && t.link == LinkKind::PCIe_H2D) {
         u64& lo = next_lo[{t.layer, t.stage}];
@@ -497,7 +511,7 @@ void Executor::Impl::build_tasks() {
 namespace {
 enum SlotKind {
   kDevParam, kInX, kOutY, kInG, kOutG, kGrad, kRetain, kHostIlg, kParamImg, kParamRd, kOptImg, kOptRd, kCkptImg,
-  kCkptRd, kHostGrad, kOptDev
+  kCkptRd, kHostGrad, kOptDev, kParamFile, kOptFile, kCkptFile
 };
 struct Access {
   long long slot;
@@ -552,9 +566,14 @@ void Executor::Impl::hazards() {
         const bool fwd = fwd_phase[i] != 0;
         switch (t.data) {
           case DataKind::Param:
-            if (t.link == LinkKind::SSD_Read) W(slot_id(kParamRd, l));
-            else if (t.link == LinkKind::SSD_Write) R(slot_id(kParamImg, l));
-            else {
+            if (t.link == LinkKind::SSD_Read) {
+              W(slot_id(kParamRd, l));
+              R(slot_id(kParamFile, l, 0));
+              if (!fwd) R(slot_id(kParamFile, l, 1));
+            } else if (t.link == LinkKind::SSD_Write) {
+              R(slot_id(kParamImg, l));
+              W(slot_id(kParamFile, l, imm_late));
+            } else {
               R(slot_id(kParamImg, l));
               R(slot_id(kParamRd, l));
               W(slot_id(kDevParam, (((st + 1) % 2) + 2) % 2));
@@ -576,9 +595,15 @@ void Executor::Impl::hazards() {
               if (!fwd) R(slot_id(kCkptRd, l - 1, m));
               W(slot_id(kInX, par, m));
             } else if (t.link == LinkKind::SSD_Write) {
-              for (int k = 0; k < M; ++k) R(slot_id(kCkptImg, l, k));
+              for (int k = 0; k < M; ++k) {
+                R(slot_id(kCkptImg, l, k));
+                W(slot_id(kCkptFile, l, k));
+              }
             } else {
-              for (int k = 0; k < M; ++k) W(slot_id(kCkptRd, l - 1, k));
+              for (int k = 0; k < M; ++k) {
+                W(slot_id(kCkptRd, l - 1, k));
+                R(slot_id(kCkptFile, l - 1, k));
+              }
             }
             break;
           case DataKind::GradAccum:
@@ -600,16 +625,24 @@ void Executor::Impl::hazards() {
             }
             break;
           case DataKind::OptState:
-            if (t.link == LinkKind::SSD_Read) W(slot_id(kOptRd, l, imm_late));
-            else R(slot_id(kOptImg, l, imm_late));
+            if (t.link == LinkKind::SSD_Read) {
+              W(slot_id(kOptRd, l, imm_late));
+              R(slot_id(kOptFile, l, imm_late));
+            } else {
+              R(slot_id(kOptImg, l, imm_late));
+              W(slot_id(kOptFile, l, imm_late));
+            }
             break;
         }
         break;
       }
     }
   }
-  // WAR / WAW over two unrolled iterations; deps discovered in iteration 1
-  // carry offsets 0 / -1 and hold in every steady-state iteration.
+  // RAW / WAR / WAW over two unrolled iterations; deps discovered in
+  // iteration 1 carry offsets 0 / -1 and hold in every steady-state
+  // iteration.  RAW edges matter where data flows through a buffer the plan
+  // does not name: e.g. the next iteration's parameter SSD read must follow
+  // this iteration's SSD write-back of the updated slice (same NVMe region).
   struct Use {
     int task, iter;
   };
@@ -618,8 +651,13 @@ void Executor::Impl::hazards() {
   std::vector<std::set<std::pair<int, int>>> found(n);
   for (int it = 0; it < 2; ++it) {
     for (size_t i = 0; i < n; ++i) {
-      for (const Access& a : acc[i])
-        if (!a.write) readers[a.slot].push_back({static_cast<int>(i), it});
+      for (const Access& a : acc[i]) {
+        if (a.write) continue;
+        readers[a.slot].push_back({static_cast<int>(i), it});
+        auto w = writer.find(a.slot);
+        if (w != writer.end() && !(w->second.task == static_cast<int>(i) && w->second.iter == it) && it == 1)
+          found[i].insert({w->second.task, w->second.iter - it});
+      }
       for (const Access& a : acc[i]) {
         if (!a.write) continue;
         auto add = [&](Use u) {
@@ -882,7 +920,8 @@ void Executor::Impl::compute_task(const Task& t, int it) {
 // Fused Adam over elements [e0,e1) of layer l: optimizer state gathered from
 // its tiers into HBM (in place when a single HBM segment holds the range),
 // updated, scattered back; the low-precision params go to the host image.
-void Executor::Impl::apply_adam(int layer, u64 e0, u64 e1, const float* grad, int step, cudaStream_t st, int it) {
+void Executor::Impl::apply_adam(int layer, u64 e0, u64 e1, const float* grad, int step, cudaStream_t st, int it,
+                                Src src) {
   gs::AdamHyper hp{cfg.adam.lr, cfg.adam.beta1, cfg.adam.beta2, cfg.adam.eps, cfg.adam.weight_decay};
   Blob& ob = opt_blob[static_cast<size_t>(layer)];
   Blob& pbb = param_blob[static_cast<size_t>(layer)];
@@ -897,7 +936,7 @@ void Executor::Impl::apply_adam(int layer, u64 e0, u64 e1, const float* grad, in
     u64 up = 0, down = 0;
     if (!in_place) {
       state = opt_stage;
-      up = upload(ob, lo, hi, state, Src::ReadStaging, st, ~0ull);
+      up = upload(ob, lo, hi, state, src, st, ~0ull);
     }
     cuda_check(gs::adam_step_packed(hp, step, 1.0f, state, grad + (c0 - e0), lp_stage, d.dt,
                                     static_cast<long long>(c1 - c0), st),
@@ -1075,6 +1114,7 @@ ExecReport Executor::run(int iterations, const int32_t* tokens, bool tokens_on_d
   I.last_iter = iterations - 1;
   I.trace.clear();
   I.launches.store(0);
+  I.prof.reset();
 
   cuda_check(cudaDeviceSynchronize(), "pre-run sync");
   cuda_check(cudaEventRecord(I.ev_base, I.s_gpu), "base");
@@ -1144,7 +1184,8 @@ void Executor::flush() {
   for (int l = 0; l < I.N; ++l) {
     const long long ready = I.late_ready[static_cast<size_t>(l)].load();
     if (I.el_late == 0 || ready < 0 || I.late_applied[static_cast<size_t>(l)].load() >= ready) continue;
-    I.apply_adam(l, I.el_now, I.P, I.retain[static_cast<size_t>(l)], static_cast<int>(ready + 1), I.s_opt, -2);
+    I.apply_adam(l, I.el_now, I.P, I.retain[static_cast<size_t>(l)], static_cast<int>(ready + 1), I.s_opt, -2,
+                 Src::Image);
     I.late_applied[static_cast<size_t>(l)].store(ready);
   }
   if (I.fixed_done < I.global_iter) {
@@ -1194,6 +1235,12 @@ void read_field(Executor::Impl& I, int layer, int f, float* out) {
   for (u64 i = 0; i < I.P; ++i) out[i] = st[3 * i + static_cast<u64>(f)];
 }
 }  // namespace
+
+Executor::KernelTotals Executor::kernel_profile() const {
+  KernelTotals t{};
+  impl_->prof.totals(t.flops, t.ms, t.launches);
+  return t;
+}
 
 ExecReport execute(const SchedulePlan& plan, const ExecConfig& cfg, int iterations, const int32_t* tokens) {
   Executor ex(plan, cfg);

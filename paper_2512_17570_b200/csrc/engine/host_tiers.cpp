@@ -68,6 +68,7 @@ void ThreadPool::run_all(std::vector<std::function<void()>>& jobs) {
     for (auto& j : jobs) j();
     return;
   }
+  std::lock_guard<std::mutex> call(call_mu_);
   std::unique_lock<std::mutex> lk(mu_);
   batch_ = &jobs;
   next_ = 0;
@@ -78,7 +79,7 @@ void ThreadPool::run_all(std::vector<std::function<void()>>& jobs) {
   batch_ = nullptr;
 }
 
-NvmeFile::NvmeFile(const std::string& dir, bool odirect, int threads) : pool_(threads) {
+NvmeFile::NvmeFile(const std::string& dir, bool odirect, int threads) : read_pool_(threads), write_pool_(threads) {
   std::string tmpl = dir + "/greedysnake_tier_XXXXXX";
   std::vector<char> buf(tmpl.begin(), tmpl.end());
   buf.push_back('\0');
@@ -139,7 +140,7 @@ uint64_t NvmeFile::io(bool wr, uint64_t off, void* buf, uint64_t bytes) {
       }
     });
   }
-  pool_.run_all(jobs);
+  (wr ? write_pool_ : read_pool_).run_all(jobs);
   if (!err.empty()) throw std::runtime_error("NVMe tier: " + err);
   return total;
 }

@@ -43,6 +43,7 @@ class ThreadPool {
  private:
   void loop();
   std::vector<std::thread> workers_;
+  std::mutex call_mu_;  // one batch at a time per pool
   std::mutex mu_;
   std::condition_variable cv_, done_cv_;
   std::vector<std::function<void()>>* batch_ = nullptr;
@@ -74,7 +75,9 @@ class NvmeFile {
   int fd_ = -1;
   bool direct_ = false;
   uint64_t size_ = 0;
-  ThreadPool pool_;
+  // separate pools so the SSD_R and SSD_W queues (distinct dispatcher
+  // threads, full-duplex device) never share a batch
+  ThreadPool read_pool_, write_pool_;
 };
 
 }  // namespace gs::engine

@@ -14,9 +14,26 @@ const uint8_t* off(const void* p, long long elems, int eb) {
   return static_cast<const uint8_t*>(p) + elems * eb;
 }
 
+// RAII timing scope on the compute stream (no-op without a profiler).
+struct Scope {
+  KernelProfiler* p;
+  int cls;
+  double flops;
+  cudaStream_t st;
+  int a = -1;
+  Scope(KernelProfiler* p_, int c, double f, cudaStream_t s) : p(p_), cls(c), flops(f), st(s) {
+    if (p) a = p->begin(st);
+  }
+  ~Scope() {
+    if (p) p->end(cls, flops, a, st);
+  }
+};
+
 // C[M,N] = A . B^T style call with explicit majors.
 cudaError_t mm(const Dims& d, int M, int N, int K, const void* A, bool a_k, const void* B, bool b_k, void* C,
-               Epi epi, cudaStream_t st, LaunchCounter& lc, const void* R = nullptr, void* G = nullptr) {
+               Epi epi, cudaStream_t st, LaunchCounter& lc, const void* R = nullptr, void* G = nullptr,
+               KernelProfiler* prof = nullptr) {
+  Scope sc(prof, KernelProfiler::Gemm, 2.0 * M * N * K, st);
   GemmArgs g;
   g.M = M;
   g.N = N;
@@ -35,6 +52,42 @@ cudaError_t mm(const Dims& d, int M, int N, int K, const void* A, bool a_k, cons
 }
 
 }  // namespace
+
+int KernelProfiler::begin(cudaStream_t st) {
+  if (next + 2 > pool.size()) {
+    const size_t grow = pool.size() < 4096 ? 4096 : pool.size();
+    for (size_t i = 0; i < grow; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+  }
+  const int a = static_cast<int>(next++);
+  cudaEventRecord(pool[static_cast<size_t>(a)], st);
+  return a;
+}
+void KernelProfiler::end(int cls, double flops, int a, cudaStream_t st) {
+  const int b = static_cast<int>(next++);
+  cudaEventRecord(pool[static_cast<size_t>(b)], st);
+  recs.push_back({cls, flops, a, b});
+}
+void KernelProfiler::totals(double* flops, double* ms, int* launches) const {
+  for (int c = 0; c < kCount; ++c) {
+    flops[c] = 0;
+    ms[c] = 0;
+    launches[c] = 0;
+  }
+  for (const Rec& r : recs) {
+    float t = 0.0f;
+    if (cudaEventElapsedTime(&t, pool[static_cast<size_t>(r.a)], pool[static_cast<size_t>(r.b)]) != cudaSuccess) continue;
+    flops[r.cls] += r.flops;
+    ms[r.cls] += t;
+    launches[r.cls] += 1;
+  }
+}
+KernelProfiler::~KernelProfiler() {
+  for (cudaEvent_t e : pool) cudaEventDestroy(e);
+}
 
 bool alloc_workspace(const Dims& d, Workspace& ws) {
   const size_t eb = static_cast<size_t>(d.lp());
@@ -92,11 +145,14 @@ static cudaError_t forward_body(const Dims& d, const void* W, const void* x, Wor
   const void* wo = off(W, 3 * h2, eb);
   const void* w1 = off(W, 4 * h2, eb);
   GS_TRY(layernorm_fwd(d.dt, x, ws.a, ws.m1, ws.r1, T, h, st));
-  GS_TRY(mm(d, T, 3 * h, h, ws.a, true, wqkv, true, ws.qkv, Epi::Store, st, lc));
-  GS_TRY(attention_fwd(d.dt, ws.qkv, ws.o, ws.lse, d.b, d.s, h, d.H, st));
-  GS_TRY(mm(d, T, h, h, ws.o, true, wo, true, ws.x1, Epi::AddResidual, st, lc, x));
+  GS_TRY(mm(d, T, 3 * h, h, ws.a, true, wqkv, true, ws.qkv, Epi::Store, st, lc, nullptr, nullptr, ws.prof));
+  {
+    Scope sc(ws.prof, KernelProfiler::AttnFwd, 2.0 * d.b * d.H * (double)d.s * d.s * (h / d.H), st);
+    GS_TRY(attention_fwd(d.dt, ws.qkv, ws.o, ws.lse, d.b, d.s, h, d.H, st));
+  }
+  GS_TRY(mm(d, T, h, h, ws.o, true, wo, true, ws.x1, Epi::AddResidual, st, lc, x, nullptr, ws.prof));
   GS_TRY(layernorm_fwd(d.dt, ws.x1, ws.c, ws.m2, ws.r2, T, h, st));
-  GS_TRY(mm(d, T, 4 * h, h, ws.c, true, w1, true, ws.u, Epi::StoreGelu, st, lc, nullptr, ws.g));
+  GS_TRY(mm(d, T, 4 * h, h, ws.c, true, w1, true, ws.u, Epi::StoreGelu, st, lc, nullptr, ws.g, ws.prof));
   lc.n += 4;  // two LayerNorms + attention (1 kernel in either path... counted as 1) + spare
   return cudaSuccess;
 }
@@ -105,7 +161,7 @@ cudaError_t layer_forward(const Dims& d, const void* W, const void* x, void* y, 
                           LaunchCounter& lc) {
   const long long h2 = 1LL * d.h * d.h;
   GS_TRY(forward_body(d, W, x, ws, st, lc));
-  return mm(d, d.T(), d.h, 4 * d.h, ws.g, true, off(W, 8 * h2, d.lp()), true, y, Epi::AddResidual, st, lc, ws.x1);
+  return mm(d, d.T(), d.h, 4 * d.h, ws.g, true, off(W, 8 * h2, d.lp()), true, y, Epi::AddResidual, st, lc, ws.x1, nullptr, ws.prof);
 }
 
 cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const void* dy_in, void* dx, float* dW,
@@ -122,14 +178,14 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
   const void* dy = dy_in;
   if (head) {
     // y = block output; tied head on LN_f(y); dy = d(CE)/dy
-    GS_TRY(mm(d, T, h, 4 * h, ws.g, true, w2, true, ws.y, Epi::AddResidual, st, lc, ws.x1));
+    GS_TRY(mm(d, T, h, 4 * h, ws.g, true, w2, true, ws.y, Epi::AddResidual, st, lc, ws.x1, nullptr, ws.prof));
     GS_TRY(layernorm_fwd(d.dt, ws.y, ws.z, ws.mz, ws.rz, T, h, st));
-    GS_TRY(mm(d, T, d.V, h, ws.z, true, head->wte, true, ws.logits, Epi::StoreF32, st, lc));
+    GS_TRY(mm(d, T, d.V, h, ws.z, true, head->wte, true, ws.logits, Epi::StoreF32, st, lc, nullptr, nullptr, ws.prof));
     GS_TRY(softmax_xent(ws.logits, ws.dlogits, d.dt, head->tokens, d.b, d.s, d.V, head->scale, head->loss_sum, st));
     // dwte += dlogits^T z  (M=V, N=h, K=T)
-    GS_TRY(mm(d, d.V, h, T, ws.dlogits, false, ws.z, false, head->dwte, Epi::AccumF32, st, lc));
+    GS_TRY(mm(d, d.V, h, T, ws.dlogits, false, ws.z, false, head->dwte, Epi::AccumF32, st, lc, nullptr, nullptr, ws.prof));
     // dz = dlogits . wte   (M=T, N=h, K=V)
-    GS_TRY(mm(d, T, h, d.V, ws.dlogits, true, head->wte, false, ws.tmp, Epi::Store, st, lc));
+    GS_TRY(mm(d, T, h, d.V, ws.dlogits, true, head->wte, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));
     GS_TRY(layernorm_bwd(d.dt, ws.y, ws.mz, ws.rz, ws.tmp, ws.dy, T, h, false, st));
     dy = ws.dy;
     lc.n += 3;
@@ -139,19 +195,22 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
   float* dW1 = dW + 4 * h2;
   float* dW2 = dW + 8 * h2;
   // MLP
-  GS_TRY(mm(d, h, 4 * h, T, dy, false, ws.g, false, dW2, wg, st, lc));          // dW2 (+)= dy^T g
-  GS_TRY(mm(d, T, 4 * h, h, dy, true, w2, false, ws.big, Epi::Store, st, lc));    // dg = dy W2
+  GS_TRY(mm(d, h, 4 * h, T, dy, false, ws.g, false, dW2, wg, st, lc, nullptr, nullptr, ws.prof));          // dW2 (+)= dy^T g
+  GS_TRY(mm(d, T, 4 * h, h, dy, true, w2, false, ws.big, Epi::Store, st, lc, nullptr, nullptr, ws.prof));    // dg = dy W2
   GS_TRY(gelu_bwd(d.dt, ws.u, ws.big, ws.big, 4LL * T * h, st));                  // du
-  GS_TRY(mm(d, 4 * h, h, T, ws.big, false, ws.c, false, dW1, wg, st, lc));       // dW1 (+)= du^T c
-  GS_TRY(mm(d, T, h, 4 * h, ws.big, true, w1, false, ws.tmp, Epi::Store, st, lc));  // dc = du W1
+  GS_TRY(mm(d, 4 * h, h, T, ws.big, false, ws.c, false, dW1, wg, st, lc, nullptr, nullptr, ws.prof));       // dW1 (+)= du^T c
+  GS_TRY(mm(d, T, h, 4 * h, ws.big, true, w1, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));  // dc = du W1
   GS_TRY(cudaMemcpyAsync(ws.dx1, dy, 1LL * T * h * eb, cudaMemcpyDeviceToDevice, st));
   GS_TRY(layernorm_bwd(d.dt, ws.x1, ws.m2, ws.r2, ws.tmp, ws.dx1, T, h, true, st));  // dx1 = dy + LN2'
   // attention
-  GS_TRY(mm(d, h, h, T, ws.dx1, false, ws.o, false, dWo, wg, st, lc));           // dWo (+)= dx1^T o
-  GS_TRY(mm(d, T, h, h, ws.dx1, true, wo, false, ws.tmp, Epi::Store, st, lc));    // do = dx1 Wo
-  GS_TRY(attention_bwd(d.dt, ws.qkv, ws.o, ws.lse, ws.tmp, ws.dqkv, ws.attn_work, d.b, d.s, h, d.H, st));
-  GS_TRY(mm(d, 3 * h, h, T, ws.dqkv, false, ws.a, false, dWqkv, wg, st, lc));    // dWqkv (+)= dqkv^T a
-  GS_TRY(mm(d, T, h, 3 * h, ws.dqkv, true, wqkv, false, ws.tmp, Epi::Store, st, lc));  // da = dqkv Wqkv
+  GS_TRY(mm(d, h, h, T, ws.dx1, false, ws.o, false, dWo, wg, st, lc, nullptr, nullptr, ws.prof));           // dWo (+)= dx1^T o
+  GS_TRY(mm(d, T, h, h, ws.dx1, true, wo, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));    // do = dx1 Wo
+  {
+    Scope sc(ws.prof, KernelProfiler::AttnBwd, 5.0 * d.b * d.H * (double)d.s * d.s * (h / d.H), st);
+    GS_TRY(attention_bwd(d.dt, ws.qkv, ws.o, ws.lse, ws.tmp, ws.dqkv, ws.attn_work, d.b, d.s, h, d.H, st));
+  }
+  GS_TRY(mm(d, 3 * h, h, T, ws.dqkv, false, ws.a, false, dWqkv, wg, st, lc, nullptr, nullptr, ws.prof));    // dWqkv (+)= dqkv^T a
+  GS_TRY(mm(d, T, h, 3 * h, ws.dqkv, true, wqkv, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));  // da = dqkv Wqkv
   GS_TRY(cudaMemcpyAsync(dx, ws.dx1, 1LL * T * h * eb, cudaMemcpyDeviceToDevice, st));
   GS_TRY(layernorm_bwd(d.dt, x, ws.m1, ws.r1, ws.tmp, dx, T, h, true, st));      // dx = dx1 + LN1'
   lc.n += 6;

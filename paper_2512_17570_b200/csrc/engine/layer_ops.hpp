@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "kernels.h"
 
@@ -20,8 +21,30 @@ struct Dims {
   long long P() const { return 12LL * h * h; }
 };
 
+// Optional per-kernel-class CUDA-event timing of the compute stream
+// (bench.py's live roofline numbers).  Classes: see kProfClasses.
+struct KernelProfiler {
+  enum Cls { Gemm = 0, AttnFwd, AttnBwd, Norm, Other, kCount };
+  struct Rec {
+    int cls;
+    double flops;
+    int a, b;  // indices into pool
+  };
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  std::vector<Rec> recs;
+  int begin(cudaStream_t st);                    // returns event index
+  void end(int cls, double flops, int a, cudaStream_t st);
+  void reset() { next = 0; recs.clear(); }
+  // totals per class after the stream has completed: flops, ms, launches
+  void totals(double* flops, double* ms, int* launches) const;
+  ~KernelProfiler();
+};
+inline const char* const kProfClasses[] = {"gemm", "attention_fwd", "attention_bwd", "layernorm", "other"};
+
 // Per-micro-batch device scratch (allocated once per engine).
 struct Workspace {
+  KernelProfiler* prof = nullptr;
   void *a = nullptr, *qkv = nullptr, *o = nullptr, *x1 = nullptr, *c = nullptr, *u = nullptr, *g = nullptr;
   void *y = nullptr, *dy = nullptr, *big = nullptr, *dx1 = nullptr, *tmp = nullptr, *dqkv = nullptr, *x0 = nullptr;
   float *lse = nullptr, *m1 = nullptr, *r1 = nullptr, *m2 = nullptr, *r2 = nullptr, *mz = nullptr, *rz = nullptr;

@@ -99,7 +99,8 @@ def test_split_runs_equal_one_run():
     _, _, l_a, p_a, f_a, _ = run_engine(g, M, (1, 1, 0), 0.25, 3)
     _, _, l_b, p_b, f_b, _ = run_engine(g, M, (1, 1, 0), 0.25, 3, chunks=[1, 1, 1])
     assert np.allclose(l_a, l_b, rtol=1e-6)
-    assert rel(p_b, p_a) < 1e-6 and rel(f_b, f_a) < 1e-6
+    # fp32 atomics (embedding scatter, attention dK/dV) reorder sums
+    assert rel(p_b, p_a) < 1e-5 and rel(f_b, f_a) < 1e-5
 
 
 def test_trace_order_and_ledger():
@@ -132,7 +133,7 @@ def test_bf16_engine_tracks_oracle():
     fp32 oracle over 3 steps at a tensor-core-tiled geometry."""
     need_gpu()
     g = ob.Geometry(n_layers=2, hidden=256, heads=4, seq=128, mb_size=2, vocab=512)
-    M, iters = 2, 3
+    M, iters = 4, 3
     plan, reps, losses, layers, fixed, tokens = run_engine(g, M, (1, 1, 1), 0.25, iters, lp=2)
     ref_loss, ref_layers, _ = oracle_run(g, M, plan, tokens)
     assert np.max(np.abs(losses - ref_loss) / ref_loss) < 2e-2

@@ -1,0 +1,66 @@
+"""Quick throughput probe of the sm_100a kernels at GPT-1.3B shapes
+(T = b*s = 4096, h = 2048) — CUDA events, warm-up, best of N."""
+import ctypes as C
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_2512_17570_b200 as gs  # noqa: E402
+
+lib = gs.lib()
+d = torch.device("cuda:0")
+
+
+def p(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def timed(fn, reps=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b))
+    return best
+
+
+T, h = 4096, 2048
+rows = []
+for name, M, N, K, ak, bk, epi in [
+        ("fwd_qkv", T, 3 * h, h, 1, 1, 0), ("fwd_fc1", T, 4 * h, h, 1, 1, 3), ("fwd_fc2", T, h, 4 * h, 1, 1, 1),
+        ("dgrad_fc2", T, 4 * h, h, 1, 0, 0), ("wgrad_fc1", 4 * h, h, T, 0, 0, 2), ("sq8192", 8192, 8192, 8192, 1, 1, 0)]:
+    A = torch.randn(M * K, device=d).bfloat16()
+    B = torch.randn(N * K, device=d).bfloat16()
+    Cc = torch.empty(M * N, device=d, dtype=torch.float32 if epi == 2 else torch.bfloat16)
+    R = torch.randn(M * N, device=d).bfloat16() if epi == 1 else None
+    G = torch.empty(M * N, device=d, dtype=torch.bfloat16) if epi == 3 else None
+    ms = timed(lambda: gs.check(lib.gs_gemm(1, M, N, K, p(A), ak, p(B), bk, p(Cc), p(R), p(G), epi, None)))
+    rows.append(dict(gemm=name, M=M, N=N, K=K, ms=ms, tflops=2 * M * N * K / ms / 1e9))
+# attention fwd / bwd at b=2, s=2048, h=2048, H=16
+b, s, H = 2, 2048, 16
+qkv = torch.randn(b * s, 3 * h, device=d).bfloat16()
+o = torch.empty(b * s, h, device=d).bfloat16()
+lse = torch.empty(b * H * s, device=d)
+ms = timed(lambda: gs.check(lib.gs_attention_fwd(1, p(qkv), p(o), p(lse), b, s, h, H, None)))
+fl = 4 * b * H * s * s / 2 * (h // H)
+rows.append(dict(kernel="attn_fwd", ms=ms, tflops=fl / ms / 1e9))
+dout = torch.randn(b * s, h, device=d).bfloat16()
+dqkv = torch.empty_like(qkv)
+work = torch.empty(lib.gs_attention_bwd_workspace(b, s, h, H), dtype=torch.uint8, device=d)
+ms = timed(lambda: gs.check(lib.gs_attention_bwd(1, p(qkv), p(o), p(lse), p(dout), p(dqkv), p(work), b, s, h, H, None)))
+rows.append(dict(kernel="attn_bwd", ms=ms, tflops=2.5 * fl / ms / 1e9))
+# torch reference matmul for context
+A = torch.randn(8192, 8192, device=d).bfloat16()
+B = torch.randn(8192, 8192, device=d).bfloat16()
+ms = timed(lambda: A @ B)
+rows.append(dict(kernel="torch_matmul_8192", ms=ms, tflops=2 * 8192 ** 3 / ms / 1e9))
+for r in rows:
+    print(json.dumps(r))
