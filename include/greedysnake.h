@@ -142,8 +142,12 @@ int gs_engine_flush(gs_engine* engine);
 int gs_engine_read_params(gs_engine* engine, float* layers, float* fixed);
 int gs_engine_read_moments(gs_engine* engine, float* layer_m, float* layer_v);
 /* per kernel class of the last run: 0 gemm, 1 attention_fwd, 2 attention_bwd,
-   3 layernorm, 4 other — algorithmic flops, CUDA-event ms, launches */
-int gs_engine_kernel_profile(gs_engine* engine, double flops[5], double ms[5], int launches[5]);
+   3 layernorm, 4 other — algorithmic flops, CUDA-event ms and count of the
+   sampled launches, and all launches of the class */
+int gs_engine_kernel_profile(gs_engine* engine, double flops[5], double ms[5], int launches[5],
+                             int64_t total_launches[5]);
+/* time one launch in `stride` per kernel class during later runs (0 = off) */
+int gs_engine_set_profiling(gs_engine* engine, int stride);
 /* trace of the last run (last <= 3 iterations when record_trace was set) */
 int gs_engine_trace(gs_engine* engine, gs_trace_record* out, int cap, int* n);
 

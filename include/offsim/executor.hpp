@@ -101,11 +101,14 @@ class Executor {
   // summed CUDA-event milliseconds and launches.  Classes: gemm,
   // attention_fwd, attention_bwd, layernorm, other.
   struct KernelTotals {
-    double flops[5];
-    double ms[5];
-    int launches[5];
+    double flops[5];       // sampled launches
+    double ms[5];          // sampled launches
+    int launches[5];       // sampled launches
+    long long total[5];    // all launches of the class
   };
   KernelTotals kernel_profile() const;
+  // 0 disables per-kernel timing; n times one launch in n per class.
+  void set_profiling(int stride);
 
   const SchedulePlan& plan() const;
   const ExecConfig& config() const;

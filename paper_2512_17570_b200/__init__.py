@@ -374,11 +374,15 @@ class Engine:
                          _ledger(rep.extension), _ledger(rep.physical), rep.gpu_bytes, rep.host_pinned_bytes, trace)
 
     def kernel_profile(self) -> dict:
-        """{class: (flops, ms, launches)} of the last run (profile=True)."""
-        f, m, n = (C.c_double * 5)(), (C.c_double * 5)(), (C.c_int * 5)()
-        check(lib().gs_engine_kernel_profile(self._h, f, m, n))
+        """{class: (sampled flops, sampled ms, sampled launches, all launches)}
+        of the last run (profiling on)."""
+        f, m, n, t = (C.c_double * 5)(), (C.c_double * 5)(), (C.c_int * 5)(), (C.c_int64 * 5)()
+        check(lib().gs_engine_kernel_profile(self._h, f, m, n, t))
         names = ("gemm", "attention_fwd", "attention_bwd", "layernorm", "other")
-        return {k: (f[i], m[i], n[i]) for i, k in enumerate(names) if n[i]}
+        return {k: (f[i], m[i], n[i], t[i]) for i, k in enumerate(names) if n[i]}
+
+    def set_profiling(self, stride: int) -> None:
+        check(lib().gs_engine_set_profiling(self._h, int(stride)))
 
     def flush(self) -> None:
         check(lib().gs_engine_flush(self._h))

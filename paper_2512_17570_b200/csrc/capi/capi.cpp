@@ -247,15 +247,20 @@ int gs_engine_read_params(gs_engine* engine, float* layers, float* fixed) {
 int gs_engine_read_moments(gs_engine* engine, float* m, float* v) {
   return guarded([&] { engine->ex->read_moments(m, v); });
 }
-int gs_engine_kernel_profile(gs_engine* engine, double flops[5], double ms[5], int launches[5]) {
+int gs_engine_kernel_profile(gs_engine* engine, double flops[5], double ms[5], int launches[5],
+                             int64_t total_launches[5]) {
   return guarded([&] {
     const offsim::Executor::KernelTotals t = engine->ex->kernel_profile();
     for (int i = 0; i < 5; ++i) {
       flops[i] = t.flops[i];
       ms[i] = t.ms[i];
       launches[i] = t.launches[i];
+      if (total_launches) total_launches[i] = t.total[i];
     }
   });
+}
+int gs_engine_set_profiling(gs_engine* engine, int stride) {
+  return guarded([&] { engine->ex->set_profiling(stride); });
 }
 int gs_engine_trace(gs_engine* engine, gs_trace_record* out, int cap, int* n) {
   return guarded([&] {

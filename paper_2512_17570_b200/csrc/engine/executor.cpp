@@ -1238,8 +1238,13 @@ void read_field(Executor::Impl& I, int layer, int f, float* out) {
 
 Executor::KernelTotals Executor::kernel_profile() const {
   KernelTotals t{};
-  impl_->prof.totals(t.flops, t.ms, t.launches);
+  impl_->prof.totals(t.flops, t.ms, t.launches, t.total);
   return t;
+}
+
+void Executor::set_profiling(int stride) {
+  impl_->prof.stride = stride > 0 ? stride : 1;
+  impl_->ws.prof = stride > 0 ? &impl_->prof : nullptr;
 }
 
 ExecReport execute(const SchedulePlan& plan, const ExecConfig& cfg, int iterations, const int32_t* tokens) {

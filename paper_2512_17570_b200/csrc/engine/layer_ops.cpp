@@ -22,10 +22,10 @@ struct Scope {
   cudaStream_t st;
   int a = -1;
   Scope(KernelProfiler* p_, int c, double f, cudaStream_t s) : p(p_), cls(c), flops(f), st(s) {
-    if (p) a = p->begin(st);
+    if (p) a = p->begin(st, cls);
   }
   ~Scope() {
-    if (p) p->end(cls, flops, a, st);
+    if (p && a >= 0) p->end(cls, flops, a, st);
   }
 };
 
@@ -53,7 +53,16 @@ cudaError_t mm(const Dims& d, int M, int N, int K, const void* A, bool a_k, cons
 
 }  // namespace
 
-int KernelProfiler::begin(cudaStream_t st) {
+// Time one non-GEMM launch sequence under class `cls` when profiling.
+#define GS_PROF(cls, expr)                                     \
+  do {                                                         \
+    Scope sc_(ws.prof, KernelProfiler::cls, 0.0, st);          \
+    GS_TRY(expr);                                              \
+  } while (0)
+
+int KernelProfiler::begin(cudaStream_t st, int cls) {
+  ++all_launches[cls];
+  if (seen[cls]++ % (stride > 0 ? stride : 1) != 0) return -1;
   if (next + 2 > pool.size()) {
     const size_t grow = pool.size() < 4096 ? 4096 : pool.size();
     for (size_t i = 0; i < grow; ++i) {
@@ -71,11 +80,12 @@ void KernelProfiler::end(int cls, double flops, int a, cudaStream_t st) {
   cudaEventRecord(pool[static_cast<size_t>(b)], st);
   recs.push_back({cls, flops, a, b});
 }
-void KernelProfiler::totals(double* flops, double* ms, int* launches) const {
+void KernelProfiler::totals(double* flops, double* ms, int* launches, long long* total) const {
   for (int c = 0; c < kCount; ++c) {
     flops[c] = 0;
     ms[c] = 0;
     launches[c] = 0;
+    total[c] = all_launches[c];
   }
   for (const Rec& r : recs) {
     float t = 0.0f;
@@ -144,14 +154,14 @@ static cudaError_t forward_body(const Dims& d, const void* W, const void* x, Wor
   const void* wqkv = W;
   const void* wo = off(W, 3 * h2, eb);
   const void* w1 = off(W, 4 * h2, eb);
-  GS_TRY(layernorm_fwd(d.dt, x, ws.a, ws.m1, ws.r1, T, h, st));
+  GS_PROF(Norm, layernorm_fwd(d.dt, x, ws.a, ws.m1, ws.r1, T, h, st));
   GS_TRY(mm(d, T, 3 * h, h, ws.a, true, wqkv, true, ws.qkv, Epi::Store, st, lc, nullptr, nullptr, ws.prof));
   {
     Scope sc(ws.prof, KernelProfiler::AttnFwd, 2.0 * d.b * d.H * (double)d.s * d.s * (h / d.H), st);
     GS_TRY(attention_fwd(d.dt, ws.qkv, ws.o, ws.lse, d.b, d.s, h, d.H, st));
   }
   GS_TRY(mm(d, T, h, h, ws.o, true, wo, true, ws.x1, Epi::AddResidual, st, lc, x, nullptr, ws.prof));
-  GS_TRY(layernorm_fwd(d.dt, ws.x1, ws.c, ws.m2, ws.r2, T, h, st));
+  GS_PROF(Norm, layernorm_fwd(d.dt, ws.x1, ws.c, ws.m2, ws.r2, T, h, st));
   GS_TRY(mm(d, T, 4 * h, h, ws.c, true, w1, true, ws.u, Epi::StoreGelu, st, lc, nullptr, ws.g, ws.prof));
   lc.n += 4;  // two LayerNorms + attention (1 kernel in either path... counted as 1) + spare
   return cudaSuccess;
@@ -179,14 +189,14 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
   if (head) {
     // y = block output; tied head on LN_f(y); dy = d(CE)/dy
     GS_TRY(mm(d, T, h, 4 * h, ws.g, true, w2, true, ws.y, Epi::AddResidual, st, lc, ws.x1, nullptr, ws.prof));
-    GS_TRY(layernorm_fwd(d.dt, ws.y, ws.z, ws.mz, ws.rz, T, h, st));
+    GS_PROF(Norm, layernorm_fwd(d.dt, ws.y, ws.z, ws.mz, ws.rz, T, h, st));
     GS_TRY(mm(d, T, d.V, h, ws.z, true, head->wte, true, ws.logits, Epi::StoreF32, st, lc, nullptr, nullptr, ws.prof));
-    GS_TRY(softmax_xent(ws.logits, ws.dlogits, d.dt, head->tokens, d.b, d.s, d.V, head->scale, head->loss_sum, st));
+    GS_PROF(Other, softmax_xent(ws.logits, ws.dlogits, d.dt, head->tokens, d.b, d.s, d.V, head->scale, head->loss_sum, st));
     // dwte += dlogits^T z  (M=V, N=h, K=T)
     GS_TRY(mm(d, d.V, h, T, ws.dlogits, false, ws.z, false, head->dwte, Epi::AccumF32, st, lc, nullptr, nullptr, ws.prof));
     // dz = dlogits . wte   (M=T, N=h, K=V)
     GS_TRY(mm(d, T, h, d.V, ws.dlogits, true, head->wte, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));
-    GS_TRY(layernorm_bwd(d.dt, ws.y, ws.mz, ws.rz, ws.tmp, ws.dy, T, h, false, st));
+    GS_PROF(Norm, layernorm_bwd(d.dt, ws.y, ws.mz, ws.rz, ws.tmp, ws.dy, T, h, false, st));
     dy = ws.dy;
     lc.n += 3;
   }
@@ -197,11 +207,11 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
   // MLP
   GS_TRY(mm(d, h, 4 * h, T, dy, false, ws.g, false, dW2, wg, st, lc, nullptr, nullptr, ws.prof));          // dW2 (+)= dy^T g
   GS_TRY(mm(d, T, 4 * h, h, dy, true, w2, false, ws.big, Epi::Store, st, lc, nullptr, nullptr, ws.prof));    // dg = dy W2
-  GS_TRY(gelu_bwd(d.dt, ws.u, ws.big, ws.big, 4LL * T * h, st));                  // du
+  GS_PROF(Other, gelu_bwd(d.dt, ws.u, ws.big, ws.big, 4LL * T * h, st));                  // du
   GS_TRY(mm(d, 4 * h, h, T, ws.big, false, ws.c, false, dW1, wg, st, lc, nullptr, nullptr, ws.prof));       // dW1 (+)= du^T c
   GS_TRY(mm(d, T, h, 4 * h, ws.big, true, w1, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));  // dc = du W1
-  GS_TRY(cudaMemcpyAsync(ws.dx1, dy, 1LL * T * h * eb, cudaMemcpyDeviceToDevice, st));
-  GS_TRY(layernorm_bwd(d.dt, ws.x1, ws.m2, ws.r2, ws.tmp, ws.dx1, T, h, true, st));  // dx1 = dy + LN2'
+  GS_PROF(Other, cudaMemcpyAsync(ws.dx1, dy, 1LL * T * h * eb, cudaMemcpyDeviceToDevice, st));
+  GS_PROF(Norm, layernorm_bwd(d.dt, ws.x1, ws.m2, ws.r2, ws.tmp, ws.dx1, T, h, true, st));  // dx1 = dy + LN2'
   // attention
   GS_TRY(mm(d, h, h, T, ws.dx1, false, ws.o, false, dWo, wg, st, lc, nullptr, nullptr, ws.prof));           // dWo (+)= dx1^T o
   GS_TRY(mm(d, T, h, h, ws.dx1, true, wo, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));    // do = dx1 Wo
@@ -211,8 +221,8 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
   }
   GS_TRY(mm(d, 3 * h, h, T, ws.dqkv, false, ws.a, false, dWqkv, wg, st, lc, nullptr, nullptr, ws.prof));    // dWqkv (+)= dqkv^T a
   GS_TRY(mm(d, T, h, 3 * h, ws.dqkv, true, wqkv, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));  // da = dqkv Wqkv
-  GS_TRY(cudaMemcpyAsync(dx, ws.dx1, 1LL * T * h * eb, cudaMemcpyDeviceToDevice, st));
-  GS_TRY(layernorm_bwd(d.dt, x, ws.m1, ws.r1, ws.tmp, dx, T, h, true, st));      // dx = dx1 + LN1'
+  GS_PROF(Other, cudaMemcpyAsync(dx, ws.dx1, 1LL * T * h * eb, cudaMemcpyDeviceToDevice, st));
+  GS_PROF(Norm, layernorm_bwd(d.dt, x, ws.m1, ws.r1, ws.tmp, dx, T, h, true, st));      // dx = dx1 + LN1'
   lc.n += 6;
   return cudaSuccess;
 }

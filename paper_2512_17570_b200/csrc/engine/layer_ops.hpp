@@ -33,11 +33,21 @@ struct KernelProfiler {
   std::vector<cudaEvent_t> pool;
   size_t next = 0;
   std::vector<Rec> recs;
-  int begin(cudaStream_t st);                    // returns event index
+  // Time one launch in `stride` per class (an event pair between back-to-back
+  // persistent kernels costs a pipeline drain); totals are ratio estimates.
+  int stride = 16;
+  long long seen[kCount] = {};
+  long long all_launches[kCount] = {};
+  int begin(cudaStream_t st, int cls);           // event index, or -1 when not sampled
   void end(int cls, double flops, int a, cudaStream_t st);
-  void reset() { next = 0; recs.clear(); }
-  // totals per class after the stream has completed: flops, ms, launches
-  void totals(double* flops, double* ms, int* launches) const;
+  void reset() {
+    next = 0;
+    recs.clear();
+    for (int c = 0; c < kCount; ++c) seen[c] = all_launches[c] = 0;
+  }
+  // per class after the stream has completed: sampled flops, sampled ms,
+  // sampled launches, all launches
+  void totals(double* flops, double* ms, int* launches, long long* total) const;
   ~KernelProfiler();
 };
 inline const char* const kProfClasses[] = {"gemm", "attention_fwd", "attention_bwd", "layernorm", "other"};

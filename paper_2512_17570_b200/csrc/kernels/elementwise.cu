@@ -36,17 +36,20 @@ __device__ __forceinline__ float block_max256(float v, float* red) {
 constexpr int kRowThreads = 256;
 constexpr int kMaxPerThread = 48;  // h <= 12288
 
-template <typename T>
+// Row kernels hold E = ceil(h / 256) values per thread in registers (E is a
+// template parameter so occupancy follows h; a fixed 48-wide array for
+// h <= 12288 left one block per SM and made these launches latency-bound).
+template <typename T, int E>
 __global__ void __launch_bounds__(kRowThreads) ln_fwd_kernel(const T* __restrict__ x, T* __restrict__ y,
                                                              float* __restrict__ mean,
                                                              float* __restrict__ rstd, int h) {
   __shared__ float red[8];
   const long long row = blockIdx.x;
   const T* xr = x + row * h;
-  float v[kMaxPerThread];
+  float v[E];
   float s = 0.0f;
 #pragma unroll
-  for (int k = 0; k < kMaxPerThread; ++k) {
+  for (int k = 0; k < E; ++k) {
     const int i = threadIdx.x + k * kRowThreads;
     v[k] = i < h ? ld(xr + i) : 0.0f;
     s += v[k];
@@ -54,14 +57,14 @@ __global__ void __launch_bounds__(kRowThreads) ln_fwd_kernel(const T* __restrict
   const float mu = block_sum256(s, red) / h;
   float ss = 0.0f;
 #pragma unroll
-  for (int k = 0; k < kMaxPerThread; ++k) {
+  for (int k = 0; k < E; ++k) {
     const int i = threadIdx.x + k * kRowThreads;
     if (i < h) ss += (v[k] - mu) * (v[k] - mu);
   }
   const float rs = rsqrtf(block_sum256(ss, red) / h + kLnEps);
   T* yr = y + row * h;
 #pragma unroll
-  for (int k = 0; k < kMaxPerThread; ++k) {
+  for (int k = 0; k < E; ++k) {
     const int i = threadIdx.x + k * kRowThreads;
     if (i < h) st(yr + i, (v[k] - mu) * rs);
   }
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_fwd_kernel(const T* __restrict
   }
 }
 
-template <typename T>
+template <typename T, int E>
 __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(const T* __restrict__ x,
                                                              const float* __restrict__ mean,
                                                              const float* __restrict__ rstd,
@@ -82,10 +85,10 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(const T* __restrict
   const float mu = mean[row], rs = rstd[row];
   const T* xr = x + row * h;
   const T* gr = dy + row * h;
-  float xh[kMaxPerThread], g[kMaxPerThread];
+  float xh[E], g[E];
   float sg = 0.0f, sgx = 0.0f;
 #pragma unroll
-  for (int k = 0; k < kMaxPerThread; ++k) {
+  for (int k = 0; k < E; ++k) {
     const int i = threadIdx.x + k * kRowThreads;
     xh[k] = i < h ? (ld(xr + i) - mu) * rs : 0.0f;
     g[k] = i < h ? ld(gr + i) : 0.0f;
@@ -96,7 +99,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(const T* __restrict
   const float mgx = block_sum256(sgx, red) / h;
   T* dr = dx + row * h;
 #pragma unroll
-  for (int k = 0; k < kMaxPerThread; ++k) {
+  for (int k = 0; k < E; ++k) {
     const int i = threadIdx.x + k * kRowThreads;
     if (i < h) {
       const float d = rs * (g[k] - mg - xh[k] * mgx);
@@ -104,6 +107,20 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(const T* __restrict
     }
   }
 }
+
+// E in {1,2,4,8,16,24,32,48}: smallest covering h
+#define GS_ROW_E(h, ...)                                  \
+  do {                                                    \
+    const int e_ = ((h) + kRowThreads - 1) / kRowThreads; \
+    if (e_ <= 1) { constexpr int E = 1; __VA_ARGS__; }    \
+    else if (e_ <= 2) { constexpr int E = 2; __VA_ARGS__; } \
+    else if (e_ <= 4) { constexpr int E = 4; __VA_ARGS__; } \
+    else if (e_ <= 8) { constexpr int E = 8; __VA_ARGS__; } \
+    else if (e_ <= 16) { constexpr int E = 16; __VA_ARGS__; } \
+    else if (e_ <= 24) { constexpr int E = 24; __VA_ARGS__; } \
+    else if (e_ <= 32) { constexpr int E = 32; __VA_ARGS__; } \
+    else { constexpr int E = 48; __VA_ARGS__; }           \
+  } while (0)
 
 template <typename T>
 __global__ void gelu_fwd_kernel(const T* __restrict__ u, T* __restrict__ g, long long n) {
@@ -261,7 +278,7 @@ cudaError_t layernorm_fwd(DType dt, const void* x, void* y, float* mean, float* 
                           cudaStream_t s) {
   if (h > kRowThreads * kMaxPerThread) return cudaErrorInvalidValue;
   if (rows == 0) return cudaSuccess;
-  GS_DISPATCH(dt, ln_fwd_kernel<T><<<rows, kRowThreads, 0, s>>>((const T*)x, (T*)y, mean, rstd, h));
+  GS_DISPATCH(dt, GS_ROW_E(h, ln_fwd_kernel<T, E><<<rows, kRowThreads, 0, s>>>((const T*)x, (T*)y, mean, rstd, h)));
   count_launch();
   return cudaGetLastError();
 }
@@ -270,8 +287,8 @@ cudaError_t layernorm_bwd(DType dt, const void* x, const float* mean, const floa
                           void* dx, int rows, int h, bool accumulate, cudaStream_t s) {
   if (h > kRowThreads * kMaxPerThread) return cudaErrorInvalidValue;
   if (rows == 0) return cudaSuccess;
-  GS_DISPATCH(dt, ln_bwd_kernel<T><<<rows, kRowThreads, 0, s>>>((const T*)x, mean, rstd, (const T*)dy,
-                                                                (T*)dx, h, accumulate));
+  GS_DISPATCH(dt, GS_ROW_E(h, ln_bwd_kernel<T, E><<<rows, kRowThreads, 0, s>>>((const T*)x, mean, rstd,
+                                                                            (const T*)dy, (T*)dx, h, accumulate)));
   count_launch();
   return cudaGetLastError();
 }

@@ -1,0 +1,47 @@
+"""Per-resource busy time and the largest compute-stream gaps of one
+iteration of the GPT-1.3B bench workload (executor trace, CUDA events)."""
+import json
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "."); sys.path.insert(0, "tests")
+import oracle_bindings as ob  # noqa: E402
+import paper_2512_17570_b200 as gs  # noqa: E402
+
+N, h, H, s, b, V, M = 24, 2048, 16, 2048, 2, 50304, int(sys.argv[1]) if len(sys.argv) > 1 else 16
+alpha = 0.2
+model = gs.ModelSpec(N, h, H, s, b, 2, 4, 3, 1)
+plan = gs.build_vertical(model, M, gs.StorageSplit(1, 1, 1), alpha)
+eng = gs.Engine(plan, model, V, gs.AdamConfig(1e-4), record_trace=True)
+g = ob.Geometry(n_layers=N, hidden=h, heads=H, seq=s, mb_size=b, vocab=V)
+tok = ob.make_tokens(g, 3, M)
+rep = eng.run(tok)
+print("total ms", rep.total_ms, "per iteration", rep.total_ms / 3)
+tasks = [plan.task(i) for i in range(len(plan))]
+it = 1
+recs = [r for r in rep.trace if r["iteration"] == it]
+t0 = min(r["t_start_ms"] for r in recs); t1 = max(r["t_end_ms"] for r in recs)
+print("iteration", it, "span ms", t1 - t0)
+for res in gs.RESOURCES:
+    rr = sorted([r for r in recs if r["resource"] == res], key=lambda r: r["t_start_ms"])
+    if not rr:
+        continue
+    busy = sum(r["t_end_ms"] - r["t_start_ms"] for r in rr)
+    print(f"{res:10s} tasks {len(rr):5d} busy {busy:9.1f} ms  first {rr[0]['t_start_ms']-t0:8.1f} last {rr[-1]['t_end_ms']-t0:8.1f}")
+gpu = sorted([r for r in recs if r["resource"] == "compute"], key=lambda r: r["t_start_ms"])
+gaps = []
+for a, c in zip(gpu, gpu[1:]):
+    gaps.append((c["t_start_ms"] - a["t_end_ms"], a["task"], c["task"]))
+gaps.sort(reverse=True)
+print("compute gaps total ms", sum(g_[0] for g_ in gaps))
+for gap, a, c in gaps[:15]:
+    ta, tc = tasks[a], tasks[c]
+    print(f"gap {gap:7.2f} ms after {ta['kind']} L{ta['layer']} mb{ta['microbatch']} st{ta['stage']} -> {tc['kind']} L{tc['layer']} mb{tc['microbatch']} st{tc['stage']}")
+# task durations by kind
+for kind in ("fwd", "bwd", "fixed_ops"):
+    d = [r["t_end_ms"] - r["t_start_ms"] for r in gpu if tasks[r["task"]]["kind"] == kind]
+    if d:
+        print(kind, "n", len(d), "mean ms", np.mean(d), "max", np.max(d), "sum", np.sum(d))
+cpu = [r for r in recs if r["resource"] == "cpu_step"]
+print("cpu_step sum ms", sum(r["t_end_ms"] - r["t_start_ms"] for r in cpu))
