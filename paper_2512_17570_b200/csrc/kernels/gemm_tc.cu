@@ -9,6 +9,7 @@
 // and weight-gradient (dY^T X) all run without transpose copies.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -22,14 +23,19 @@ using bf16 = __nv_bfloat16;
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
-constexpr int kThreads = 256;
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, one per column half
+constexpr int kThreads = 128 + 32 * kEpiWarps;
 
-template <int BN> struct TileCfg {
-  static constexpr int kStages = BN == 256 ? 4 : 6;
+// CG = 1: one CTA computes a 128 x BN tile.  CG = 2: a CTA pair (cluster of
+// 2, tcgen05 cta_group::2) computes 256 x BN; each SM stages 128 rows of A and
+// BN/2 rows of B, the MMA exchanges B halves between the pair.
+template <int BN, int CG = 1> struct TileCfg {
   static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kBBytes = (BN / CG) * BK * 2;
+  static constexpr int kStages = (kABytes + kBBytes) <= 32768 ? 6 : 4;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  // double-buffered accumulator; allocations are powers of two >= 32 columns
+  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -63,6 +69,45 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// 2-SM form: executed by both CTAs of the pair; bytes land in the issuing
+// CTA's smem and complete on CTA 0's barrier (peer bit 24 cleared).
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the barrier at the same smem offset in cluster CTA `rank`
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
@@ -122,13 +167,13 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int ks) {
   return smem_desc(base + ks * 16 * 128, BK * 128, 1024);
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int CG = 1>
 __host__ __device__ constexpr uint32_t instr_desc() {
   return (1u << 4)            // D format f32
          | (1u << 7)          // A bf16
          | (1u << 10)         // B bf16
          | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
-         ((uint32_t)(BM >> 4) << 24);
+         ((uint32_t)((BM * CG) >> 4) << 24);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -188,11 +233,11 @@ __device__ __forceinline__ void epilogue_chunk(const float (&v)[32], int row, in
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
                    int N, int K, void* C, const bf16* R, bf16* G, int ldc) {
-  using Cfg = TileCfg<BN>;
+  using Cfg = TileCfg<BN, CG>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -205,8 +250,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = M / BM, nt = N / BN, kt = K / BK;
+  const int mt = M / (BM * CG), nt = N / BN, kt = K / BK;
   const int tiles = mt * nt;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;  // CTA within the pair
+  const int unit = CG == 2 ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+  const int units = CG == 2 ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
+  constexpr int kBN_local = BN / CG;  // B rows staged by this CTA
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
@@ -217,17 +266,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 32 * kEpiWarps * CG);  // epilogue threads of both CTAs release the accumulator
     }
     fence_barrier_init();
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(Cfg::kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(Cfg::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(Cfg::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -236,38 +291,44 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+      auto load = [&](void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+        if constexpr (CG == 2) tma_load_2d_2sm(dst, map, bar, c0, c1);
+        else tma_load_2d(dst, map, bar, c0, c1);
+      };
+      for (int t = unit; t < tiles; t += units) {
+        const int m0 = (t % mt) * BM * CG + static_cast<int>(rank) * BM;
+        const int n0 = (t / mt) * BN + static_cast<int>(rank) * kBN_local;
         for (int kb = 0; kb < kt; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], Cfg::kStageBytes);
+          // CTA 0's barrier collects the bytes of both CTAs of a pair
+          if (rank == 0) mbar_expect_tx(&full[stage], Cfg::kStageBytes * CG);
           uint8_t* sa = smem_a + stage * Cfg::kABytes;
           uint8_t* sb = smem_b + stage * Cfg::kBBytes;
           const int k0 = kb * BK;
           if (!A_MN) {
-            tma_load_2d(sa, &map_a, &full[stage], k0, m0);
+            load(sa, &map_a, &full[stage], k0, m0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * BK * 128, &map_a, &full[stage], m0 + 64 * j, k0);
+            for (int j = 0; j < BM / 64; ++j) load(sa + j * BK * 128, &map_a, &full[stage], m0 + 64 * j, k0);
           }
           if (!B_MN) {
-            tma_load_2d(sb, &map_b, &full[stage], k0, n0);
+            load(sb, &map_b, &full[stage], k0, n0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * BK * 128, &map_b, &full[stage], n0 + 64 * j, k0);
+            for (int j = 0; j < kBN_local / 64; ++j) load(sb + j * BK * 128, &map_b, &full[stage], n0 + 64 * j, k0);
           }
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
-    // ===== MMA issuer (one thread)
-    constexpr uint32_t idesc = instr_desc<BN, A_MN, B_MN>();
+  } else if (warp == 1 && rank == 0) {
+    // ===== MMA issuer (one thread; CTA 0 of a pair issues for both SMs)
+    constexpr uint32_t idesc = instr_desc<BN, A_MN, B_MN, CG>();
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (int t = unit; t < tiles; t += units) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -278,45 +339,57 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t a0 = smem_u32(smem_a + stage * Cfg::kABytes);
           const uint32_t b0 = smem_u32(smem_b + stage * Cfg::kBBytes);
 #pragma unroll
-          for (int ks = 0; ks < BK / 16; ++ks)
-            tc_mma(d_tmem, operand_desc<A_MN>(a0, ks), operand_desc<B_MN>(b0, ks), idesc, (kb | ks) != 0);
-          tc_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+          for (int ks = 0; ks < BK / 16; ++ks) {
+            if constexpr (CG == 2)
+              tc_mma_pair(d_tmem, operand_desc<A_MN>(a0, ks), operand_desc<B_MN>(b0, ks), idesc, (kb | ks) != 0);
+            else
+              tc_mma(d_tmem, operand_desc<A_MN>(a0, ks), operand_desc<B_MN>(b0, ks), idesc, (kb | ks) != 0);
+          }
+          // frees the smem slot (of both CTAs) when these MMAs retire
+          if constexpr (CG == 2) tc_commit_pair(&empty[stage]); else tc_commit(&empty[stage]);
         }
         __syncwarp();
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
-      if (lane == 0) tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+      if (lane == 0) {  // accumulator ready for the epilogue(s)
+        if constexpr (CG == 2) tc_commit_pair(&tfull[acc]); else tc_commit(&tfull[acc]);
+      }
       __syncwarp();
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
   } else if (warp >= 4) {
-    // ===== epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (= tile rows)
+    // ===== epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (= tile rows);
+    // warps 4-7 take the first half of the columns, warps 8-11 the second
     const int q = warp & 3;
+    const int c_begin = ((warp - 4) / 4) * (BN / 2);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+    for (int t = unit; t < tiles; t += units) {
+      const int m0 = (t % mt) * BM * CG + static_cast<int>(rank) * BM, n0 = (t / mt) * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = c_begin; c < c_begin + BN / 2; c += 32) {
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
         epilogue_chunk<EPI>(v, row, n0 + c, M, N, ldc, C, R, G);
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (CG == 2) mbar_arrive_cluster(&tempty[acc], 0); else mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::kTmemCols));
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::kTmemCols));
   }
 }
 
@@ -351,46 +424,72 @@ bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 cudaError_t launch(const GemmArgs& g, cudaStream_t s) {
-  using Cfg = TileCfg<BN>;
+  using Cfg = TileCfg<BN, CG>;
+  constexpr int kBNl = BN / CG;
   CUtensorMap ma, mb;
   const bool ok_a = A_MN ? make_map(&ma, g.A, g.M, g.K, BK) : make_map(&ma, g.A, g.K, g.M, BM);
-  const bool ok_b = B_MN ? make_map(&mb, g.B, g.N, g.K, BK) : make_map(&mb, g.B, g.K, g.N, BN);
+  const bool ok_b = B_MN ? make_map(&mb, g.B, g.N, g.K, BK) : make_map(&mb, g.B, g.K, g.N, kBNl);
   if (!ok_a || !ok_b) return cudaErrorInvalidValue;
-  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, EPI>;
+  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, EPI, CG>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
+    if (CG == 2) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
     attr_set = true;
   }
-  const int tiles = (g.M / BM) * (g.N / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  count_launch(); kern<<<grid, kThreads, Cfg::kSmemBytes, s>>>(ma, mb, g.M, g.N, g.K, g.C, (const bf16*)g.R, (bf16*)g.G,
-                                               g.ldc ? g.ldc : g.N);
-  return cudaGetLastError();
+  const int tiles = (g.M / (BM * CG)) * (g.N / BN);
+  int grid = tiles * CG < num_sms() ? tiles * CG : num_sms();
+  grid = grid / CG * CG;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, g.M, g.N, g.K, g.C, (const bf16*)g.R, (bf16*)g.G,
+                            g.ldc ? g.ldc : g.N);
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int CG>
 cudaError_t launch_epi(const GemmArgs& g, cudaStream_t s) {
   switch (g.epi) {
-    case Epi::Store: return launch<BN, A_MN, B_MN, 0>(g, s);
-    case Epi::AddResidual: return launch<BN, A_MN, B_MN, 1>(g, s);
-    case Epi::AccumF32: return launch<BN, A_MN, B_MN, 2>(g, s);
-    case Epi::StoreGelu: return launch<BN, A_MN, B_MN, 3>(g, s);
-    case Epi::StoreF32: return launch<BN, A_MN, B_MN, 4>(g, s);
+    case Epi::Store: return launch<BN, A_MN, B_MN, 0, CG>(g, s);
+    case Epi::AddResidual: return launch<BN, A_MN, B_MN, 1, CG>(g, s);
+    case Epi::AccumF32: return launch<BN, A_MN, B_MN, 2, CG>(g, s);
+    case Epi::StoreGelu: return launch<BN, A_MN, B_MN, 3, CG>(g, s);
+    case Epi::StoreF32: return launch<BN, A_MN, B_MN, 4, CG>(g, s);
   }
   return cudaErrorInvalidValue;
 }
 
-template <int BN>
+template <int BN, int CG>
 cudaError_t launch_bn(const GemmArgs& g, cudaStream_t s) {
   const bool a_mn = !g.a_kmajor, b_mn = !g.b_kmajor;
-  if (!a_mn && !b_mn) return launch_epi<BN, false, false>(g, s);
-  if (!a_mn && b_mn) return launch_epi<BN, false, true>(g, s);
-  if (a_mn && b_mn) return launch_epi<BN, true, true>(g, s);
-  return launch_epi<BN, true, false>(g, s);
+  if (!a_mn && !b_mn) return launch_epi<BN, false, false, CG>(g, s);
+  if (!a_mn && b_mn) return launch_epi<BN, false, true, CG>(g, s);
+  if (a_mn && b_mn) return launch_epi<BN, true, true, CG>(g, s);
+  return launch_epi<BN, true, false, CG>(g, s);
+}
+
+int pair_mode() {  // GS_GEMM_PAIR=0 forces the single-CTA kernel (A/B tests)
+  static int v = [] {
+    const char* e = getenv("GS_GEMM_PAIR");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
 }
 
 }  // namespace
@@ -410,7 +509,14 @@ bool gemm_tc_supported(const GemmArgs& g) {
 
 cudaError_t gemm_tc(const GemmArgs& g, cudaStream_t s) {
   if (!gemm_tc_supported(g)) return cudaErrorInvalidValue;
-  return (g.N % 256 == 0) ? launch_bn<256>(g, s) : launch_bn<128>(g, s);
+  // Pair tiles 256 x 256 whenever N allows (measured: smaller N tiles lose
+  // more per-tile efficiency than they win back in wave quantisation).
+  if (pair_mode() && g.M % (2 * BM) == 0) {
+    if (g.N % 256 == 0) return launch_bn<256, 2>(g, s);
+    if (g.N % 192 == 0 && g.b_kmajor) return launch_bn<192, 2>(g, s);
+    if (g.N % 128 == 0) return launch_bn<128, 2>(g, s);
+  }
+  return (g.N % 256 == 0) ? launch_bn<256, 1>(g, s) : launch_bn<128, 1>(g, s);
 }
 
 }  // namespace gs

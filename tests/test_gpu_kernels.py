@@ -42,7 +42,8 @@ def rel(a, b):
     return float((a - b).norm() / b.norm())
 
 
-SHAPES = [(128, 128, 64), (256, 384, 128), (512, 256, 320), (1024, 2048, 512), (4096, 6144, 2048)]
+SHAPES = [(128, 128, 64), (256, 384, 128), (512, 256, 320), (512, 768, 256), (256, 640, 128), (1024, 2048, 512),
+          (4096, 6144, 2048)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
