@@ -598,6 +598,7 @@ size_t attention_bwd_workspace(int b, int s, int h, int H) {
 cudaError_t attention_fwd(DType dt, const void* qkv, void* o, float* lse, int b, int s, int h, int H,
                           cudaStream_t st) {
   if (h % H || h / H > 128) return cudaErrorInvalidValue;
+  if (attention_tc_supported(dt, s, h, H)) return attention_fwd_tc(qkv, o, lse, b, s, h, H, st);
   if (fa_ok(dt, s, h, H)) {
     if (h / H == 128) return fa_fwd<128>((const bf16*)qkv, (bf16*)o, lse, b, s, h, H, st);
     return fa_fwd<64>((const bf16*)qkv, (bf16*)o, lse, b, s, h, H, st);

@@ -1,0 +1,363 @@
+// Causal attention forward on the 5th-generation tensor cores (sm_100a).
+//
+// One CTA per (128-query tile, batch x head), head_dim 128, bf16:
+//   TMA (128B swizzle) loads Q once and K/V blocks of 128 keys into a
+//   double-buffered ring; one elected thread issues
+//     S_j = Q K_j^T      (tcgen05.mma kind::f16, M=128 N=128, fp32 in TMEM,
+//                         two S buffers so S_{j+1} overlaps softmax_j)
+//     O  += P_j V_j      (A = P from shared memory, B = V as an MN-major
+//                         operand: no transpose)
+//   four softmax warps own one query row (= one TMEM lane) each: tcgen05.ld
+//   the S row, online softmax in registers (log2 domain), rescale O in TMEM
+//   (tcgen05.ld / st) when the running max moves, write P in the UMMA
+//   128B-swizzled K-major layout, and finally normalise O and write O / lse.
+// Same layouts and semantics as the mma.sync path in attention.cu:
+// qkv [b*s][3h] (q | k | v column blocks, head j at columns j*d),
+// o [b*s][h], lse [b][H][s] natural log of the 1/sqrt(d)-scaled scores.
+#include <cuda.h>
+
+#include <cstdlib>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace gs {
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+constexpr int kD = 128;       // head dim
+constexpr int kBQ = 128;      // queries per CTA
+constexpr int kBK = 128;      // keys per block
+constexpr int kTile = kBQ * kD * 2;  // 32 KB: one 128 x 128 bf16 tile
+constexpr int kThreadsFa = 256;      // warp 0 TMA, 1 MMA, 2 TMEM alloc, 4-7 softmax
+
+// ---------------------------------------------------------------- PTX
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, uint64_t* b, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(su32(b)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tst32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tst_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// SWIZZLE_128B smem descriptor (sm_100 version bits).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr & 0x3FFFF) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+// K-major 128 x 128 tile stored as two 64-wide swizzle chunks of 16 KB;
+// k-step ks (16 elements) = chunk ks/4, +32 B inside the swizzle row.
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t base, int ks) {
+  return sdesc(base + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024);
+}
+// MN-major operand (V: keys x d with d contiguous): two 64-wide MN blocks of
+// [128 k-rows][128 B] (LBO = 16 KB), 8-row K groups (SBO = 1 KB); k-step ks
+// advances 16 rows.
+__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int ks) {
+  return sdesc(base + ks * 16 * 128, 16384, 1024);
+}
+constexpr uint32_t idesc(bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(128 >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ uint32_t pack(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+struct FaSmem {
+  // tiles (1024-aligned): Q, K[2], V[2], P
+  uint8_t tiles[6][kTile];
+  uint64_t q_full, k_full[2], v_full[2], kv_empty[2], s_full[2], p_full, o_done;
+  uint32_t tmem;
+};
+
+__global__ void __launch_bounds__(kThreadsFa, 1)
+    fa_fwd_tc_kernel(const __grid_constant__ CUtensorMap map, bf16* __restrict__ o, float* __restrict__ lse, int s,
+                     int h, int H, float scale_log2) {
+  extern __shared__ uint8_t raw[];
+  FaSmem& sm = *reinterpret_cast<FaSmem*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* Qs = sm.tiles[0];
+  uint8_t* Ks[2] = {sm.tiles[1], sm.tiles[2]};
+  uint8_t* Vs[2] = {sm.tiles[3], sm.tiles[4]};
+  uint8_t* Ps = sm.tiles[5];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qb = gridDim.x - 1 - blockIdx.x;  // heavy tiles first
+  const int bh = blockIdx.y, bi = bh / H, j = bh % H;
+  const int row0 = bi * s;                   // first token row of this sequence
+  const int q0 = qb * kBQ;
+  const int nblk = qb + 1;                   // causal: key blocks 0..qb
+
+  if (threadIdx.x == 0) {
+    bar_init(&sm.q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&sm.k_full[i], 1);
+      bar_init(&sm.v_full[i], 1);
+      bar_init(&sm.kv_empty[i], 1);
+      bar_init(&sm.s_full[i], 1);
+    }
+    bar_init(&sm.p_full, 128);
+    bar_init(&sm.o_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = sm.tmem;  // S0: cols 0-127, S1: 128-255, O: 256-383
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map)) : "memory");
+      bar_expect(&sm.q_full, kTile);
+      for (int c = 0; c < 2; ++c) tma2d(Qs + c * 16384, &map, &sm.q_full, j * kD + 64 * c, row0 + q0);
+      for (int kb = 0; kb < nblk; ++kb) {
+        const int buf = kb & 1;
+        bar_wait(&sm.kv_empty[buf], ((kb >> 1) & 1) ^ 1);
+        bar_expect(&sm.k_full[buf], kTile);
+        for (int c = 0; c < 2; ++c)
+          tma2d(Ks[buf] + c * 16384, &map, &sm.k_full[buf], h + j * kD + 64 * c, row0 + kb * kBK);
+        bar_expect(&sm.v_full[buf], kTile);
+        for (int c = 0; c < 2; ++c)
+          tma2d(Vs[buf] + c * 16384, &map, &sm.v_full[buf], 2 * h + j * kD + 64 * c, row0 + kb * kBK);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t qa = su32(Qs), pa = su32(Ps);
+      bar_wait(&sm.q_full, 0);
+      auto issue_s = [&](int kb) {
+        const int buf = kb & 1;
+        bar_wait(&sm.k_full[buf], (kb >> 1) & 1);
+        fence_after();
+        const uint32_t ka = su32(Ks[buf]);
+#pragma unroll
+        for (int ks = 0; ks < kD / 16; ++ks)
+          mma(tmem + buf * 128, desc_kmajor(qa, ks), desc_kmajor(ka, ks), idesc(false), ks != 0);
+        commit(&sm.s_full[buf]);
+      };
+      issue_s(0);
+      for (int kb = 0; kb < nblk; ++kb) {
+        const int buf = kb & 1;
+        if (kb + 1 < nblk) issue_s(kb + 1);  // overlaps softmax of block kb
+        bar_wait(&sm.p_full, kb & 1);        // P_kb in smem, O rescaled
+        bar_wait(&sm.v_full[buf], (kb >> 1) & 1);
+        fence_after();
+        const uint32_t va = su32(Vs[buf]);
+#pragma unroll
+        for (int ks = 0; ks < kBK / 16; ++ks)
+          mma(tmem + 256, desc_kmajor(pa, ks), desc_mnmajor(va, ks), idesc(true), (kb | ks) != 0);
+        commit(&sm.o_done);          // P consumed, O updated
+        commit(&sm.kv_empty[buf]);   // K/V slot free
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== softmax: thread t owns query row r = t (TMEM lane)
+    const int r = (warp - 4) * 32 + lane;
+    const int qrow = q0 + r;
+    const uint32_t lane_base = ((uint32_t)((warp - 4) * 32)) << 16;
+    float m_run = -INFINITY, l_run = 0.0f;
+    const uint32_t swz = (uint32_t)(r & 7);
+    uint8_t* prow = Ps + (r >> 3) * 1024 + (r & 7) * 128;
+    for (int kb = 0; kb < nblk; ++kb) {
+      const int buf = kb & 1;
+      bar_wait(&sm.s_full[buf], (kb >> 1) & 1);
+      fence_after();
+      float sv[kBK];
+#pragma unroll
+      for (int c = 0; c < kBK / 32; ++c) {
+        uint32_t rr[32];
+        tld32(tmem + lane_base + buf * 128 + c * 32, rr);
+        tld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(rr[i]) * scale_log2;
+      }
+      const bool diag = kb == qb;
+      float mx = m_run;
+#pragma unroll
+      for (int i = 0; i < kBK; ++i) {
+        if (diag && kb * kBK + i > qrow) sv[i] = -INFINITY;
+        mx = fmaxf(mx, sv[i]);
+      }
+      const float corr = exp2f(m_run - mx);
+      float rs = 0.0f;
+#pragma unroll
+      for (int i = 0; i < kBK; ++i) {
+        sv[i] = exp2f(sv[i] - mx);
+        rs += sv[i];
+      }
+      l_run = l_run * corr + rs;
+      m_run = mx;
+      // previous PV must be done before P is overwritten and O rescaled
+      if (kb > 0) {
+        bar_wait(&sm.o_done, (kb - 1) & 1);
+        fence_after();
+        // tcgen05.ld/st are warp-collective: rescale when any row of the warp moved
+        if (__any_sync(0xffffffffu, corr != 1.0f)) {
+#pragma unroll
+          for (int c = 0; c < kD / 32; ++c) {
+            uint32_t rr[32];
+            tld32(tmem + lane_base + 256 + c * 32, rr);
+            tld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * corr);
+            tst32(tmem + lane_base + 256 + c * 32, rr);
+          }
+          tst_wait();
+        }
+      }
+      // P row -> K-major 128B-swizzled tile: chunk c (keys 64c..), 16-byte
+      // piece p (8 keys) stored at slot p ^ (row % 8)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const float* v = sv + c * 64 + p * 8;
+          uint4 w = make_uint4(pack(v[0], v[1]), pack(v[2], v[3]), pack(v[4], v[5]), pack(v[6], v[7]));
+          *reinterpret_cast<uint4*>(prow + c * 16384 + ((p ^ swz) << 4)) = w;
+        }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
+      fence_before();
+      bar_arrive(&sm.p_full);
+    }
+    // epilogue: wait for the last PV, normalise, write O and lse
+    bar_wait(&sm.o_done, (nblk - 1) & 1);
+    fence_after();
+    const float inv = 1.0f / l_run;
+    bf16* orow = o + (long long)(row0 + qrow) * h + j * kD;
+#pragma unroll
+    for (int c = 0; c < kD / 32; ++c) {
+      uint32_t rr[32];
+      tld32(tmem + lane_base + 256 + c * 32, rr);
+      tld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack(__uint_as_float(rr[8 * q]) * inv, __uint_as_float(rr[8 * q + 1]) * inv);
+        w.y = pack(__uint_as_float(rr[8 * q + 2]) * inv, __uint_as_float(rr[8 * q + 3]) * inv);
+        w.z = pack(__uint_as_float(rr[8 * q + 4]) * inv, __uint_as_float(rr[8 * q + 5]) * inv);
+        w.w = pack(__uint_as_float(rr[8 * q + 6]) * inv, __uint_as_float(rr[8 * q + 7]) * inv);
+        *reinterpret_cast<uint4*>(orow + c * 32 + 8 * q) = w;
+      }
+    }
+    lse[(long long)bh * s + qrow] = (m_run + log2f(l_run)) * 0.6931471805599453f;
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encoder() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+}  // namespace
+
+bool attention_tc_supported(DType dt, int s, int h, int H) {
+  static const bool off = [] {
+    const char* e = getenv("GS_ATTN_TC");
+    return e && atoi(e) == 0;
+  }();
+  return !off && dt == DType::BF16 && h / H == kD && h % H == 0 && s % kBQ == 0 && encoder() != nullptr;
+}
+
+cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s, int h, int H, cudaStream_t st) {
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)3 * h, (cuuint64_t)b * s};
+  const cuuint64_t strides[1] = {(cuuint64_t)3 * h * 2};
+  const cuuint32_t box[2] = {64, 128};
+  const cuuint32_t elem[2] = {1, 1};
+  if (encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims, strides, box, elem,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  const int smem = (int)sizeof(FaSmem) + 1024;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(fa_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)kD);
+  count_launch();
+  fa_fwd_tc_kernel<<<dim3(s / kBQ, b * H), kThreadsFa, smem, st>>>(map, (bf16*)o, lse, s, h, H, scale_log2);
+  return cudaGetLastError();
+}
+
+}  // namespace gs
