@@ -580,8 +580,14 @@ cudaError_t fa_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16*
   if (e != cudaSuccess) return e;
   const long long rows = (long long)b * H * s;
   count_launch(); fa_dot_kernel<HD><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(o, dout, D, b, s, h, H);
-  const dim3 grid(s / kFaBN, b * H);
-  count_launch(); fa_bwd_kernel<HD><<<grid, 128, bwd_smem<HD>(), st>>>(qkv, dout, lse, D, dqkv, dq, s, h, H, 1.0f / sqrtf((float)HD));
+  if (HD == 128 && attention_tc_supported(DType::BF16, s, h, H)) {
+    e = attention_bwd_tc(qkv, dout, lse, D, dqkv, dq, b, s, h, H, st);
+    if (e != cudaSuccess) return e;
+  } else {
+    const dim3 grid(s / kFaBN, b * H);
+    count_launch();
+    fa_bwd_kernel<HD><<<grid, 128, bwd_smem<HD>(), st>>>(qkv, dout, lse, D, dqkv, dq, s, h, H, 1.0f / sqrtf((float)HD));
+  }
   count_launch(); dq_store_kernel<<<grid_for((long long)b * s * h, 256, 4), 256, 0, st>>>(dq, dqkv, (long long)b * s, h);
   return cudaGetLastError();
 }

@@ -311,6 +311,226 @@ __global__ void __launch_bounds__(kThreadsFa, 1)
   }
 }
 
+// ============================================================== backward
+// One CTA per (128-key block, batch x head); loop over 64-query blocks from
+// the diagonal down.  Per block (TMEM columns in brackets):
+//   S^T  = K Q^T            [0,64)     dP^T = V dO^T          [64,128)
+//   P^T  = exp(S^T*scale - lse_q), dS^T = P^T (dP^T - D_q)   (registers,
+//          thread = key row; written bf16 to shared memory)
+//   dV  += P^T dO           [128,256)  dK  += dS^T Q          [256,384)
+//   dQ^T = K^T dS^T         [384,448)  -> fp32 red.add into dq_acc
+// The dS^T bytes serve as the K-major A operand of dK and as the MN-major
+// operand of dQ^T.  lse and D (= rowsum(dO*O)) of each query block arrive by
+// bulk copy with the Q / dO tiles.
+constexpr int kBQb = 64;                      // queries per backward block
+constexpr int kHalf = kBQb * kD * 2;          // 16 KB: 64 x 128 bf16
+constexpr int kPT = kBK * kBQb * 2;           // 16 KB: 128 keys x 64 queries bf16
+
+struct FaBwdSmem {
+  uint8_t K[kTile], V[kTile];
+  uint8_t Q[2][kHalf], dO[2][kHalf];
+  uint8_t PT[kPT], dST[kPT];
+  float L[2][kBQb], D[2][kBQb];
+  uint64_t kv_full, q_full[2], q_empty[2], s_full, ps_full, dq_full;
+  uint32_t tmem;
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(b))
+               : "memory");
+}
+// K-major tile of 64-element K chunks, `rows` rows per chunk (chunk stride
+// rows*128 B); k-step ks moves 32 B inside the swizzle row.
+__device__ __forceinline__ uint64_t desc_k(uint32_t base, int ks, int rows) {
+  return sdesc(base + (ks >> 2) * rows * 128 + (ks & 3) * 32, 16, 1024);
+}
+// MN-major operand: 64-element MN blocks of [k-rows][128 B] (LBO = block
+// stride), k-step of 16 rows.
+__device__ __forceinline__ uint64_t desc_mn(uint32_t base, int ks, uint32_t lbo) {
+  return sdesc(base + ks * 16 * 128, lbo, 1024);
+}
+constexpr uint32_t idesc2(int n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__global__ void __launch_bounds__(kThreadsFa, 1)
+    fa_bwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_q,
+                     const __grid_constant__ CUtensorMap map_do,
+                     const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv,
+                     float* __restrict__ dq_acc, int s, int h, int H, float scale) {
+  extern __shared__ uint8_t raw[];
+  FaBwdSmem& sm = *reinterpret_cast<FaBwdSmem*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkb = gridDim.x;
+  const int kb = nkb - 1 - blockIdx.x;          // few query blocks last
+  const int bh = blockIdx.y, bi = bh / H, j = bh % H;
+  const int row0 = bi * s;
+  const int k0 = kb * kBK;
+  const int qb0 = k0 / kBQb, nq = s / kBQb - qb0;  // query blocks from the diagonal
+  const float scale_log2 = scale * 1.4426950408889634f;
+
+  if (threadIdx.x == 0) {
+    bar_init(&sm.kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&sm.q_full[i], 1);
+      bar_init(&sm.q_empty[i], 1);
+    }
+    bar_init(&sm.s_full, 1);
+    bar_init(&sm.ps_full, 128);
+    bar_init(&sm.dq_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = sm.tmem;
+  constexpr uint32_t kST = 0, kDPT = 64, kDV = 128, kDK = 256, kDQ = 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_do)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_q)) : "memory");
+      bar_expect(&sm.kv_full, 2 * kTile);
+      for (int c = 0; c < 2; ++c) {
+        tma2d(sm.K + c * 16384, &map_qkv, &sm.kv_full, h + j * kD + 64 * c, row0 + k0);
+        tma2d(sm.V + c * 16384, &map_qkv, &sm.kv_full, 2 * h + j * kD + 64 * c, row0 + k0);
+      }
+      for (int i = 0; i < nq; ++i) {
+        const int buf = i & 1, q0 = (qb0 + i) * kBQb;
+        bar_wait(&sm.q_empty[buf], ((i >> 1) & 1) ^ 1);
+        bar_expect(&sm.q_full[buf], 2 * kHalf + 2 * kBQb * 4);
+        for (int c = 0; c < 2; ++c) {
+          tma2d(sm.Q[buf] + c * 8192, &map_q, &sm.q_full[buf], j * kD + 64 * c, row0 + q0);
+          tma2d(sm.dO[buf] + c * 8192, &map_do, &sm.q_full[buf], j * kD + 64 * c, row0 + q0);
+        }
+        bulk_g2s(sm.L[buf], lse + (long long)bh * s + q0, kBQb * 4, &sm.q_full[buf]);
+        bulk_g2s(sm.D[buf], Dg + (long long)bh * s + q0, kBQb * 4, &sm.q_full[buf]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t ka = su32(sm.K), va = su32(sm.V), pa = su32(sm.PT), da = su32(sm.dST);
+      bar_wait(&sm.kv_full, 0);
+      for (int i = 0; i < nq; ++i) {
+        const int buf = i & 1;
+        const uint32_t qa = su32(sm.Q[buf]), oa = su32(sm.dO[buf]);
+        bar_wait(&sm.q_full[buf], (i >> 1) & 1);
+        fence_after();
+        // S^T and dP^T (TMEM of block i-1 was read before ps_full(i-1))
+#pragma unroll
+        for (int ks = 0; ks < kD / 16; ++ks) {
+          mma(tmem + kST, desc_k(ka, ks, 128), desc_k(qa, ks, 64), idesc2(64, false, false), ks != 0);
+          mma(tmem + kDPT, desc_k(va, ks, 128), desc_k(oa, ks, 64), idesc2(64, false, false), ks != 0);
+        }
+        commit(&sm.s_full);
+        bar_wait(&sm.ps_full, i & 1);
+        fence_after();
+#pragma unroll
+        for (int ks = 0; ks < kBQb / 16; ++ks) {
+          mma(tmem + kDV, desc_k(pa, ks, 128), desc_mn(oa, ks, 8192), idesc2(128, false, true), (i | ks) != 0);
+          mma(tmem + kDK, desc_k(da, ks, 128), desc_mn(qa, ks, 8192), idesc2(128, false, true), (i | ks) != 0);
+        }
+#pragma unroll
+        for (int ks = 0; ks < kBK / 16; ++ks)
+          mma(tmem + kDQ, desc_mn(ka, ks, 16384), desc_mn(da, ks, 8192), idesc2(64, true, true), ks != 0);
+        commit(&sm.dq_full);
+        commit(&sm.q_empty[buf]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane;          // key row (S^T, dP^T, dK, dV) / d lane (dQ^T)
+    const uint32_t lb = ((uint32_t)((warp - 4) * 32)) << 16;
+    const int key = k0 + r;
+    const uint32_t swz = (uint32_t)(r & 7);
+    const int rowoff = (r >> 3) * 1024 + (r & 7) * 128;
+    auto drain_dq = [&](int i) {  // dQ^T of block i -> fp32 red.add
+      bar_wait(&sm.dq_full, i & 1);
+      fence_after();
+      const int q0 = (qb0 + i) * kBQb;
+      float* dst = dq_acc + (long long)(row0 + q0) * h + j * kD + r;
+#pragma unroll
+      for (int c = 0; c < kBQb / 32; ++c) {
+        uint32_t rr[32];
+        tld32(tmem + lb + kDQ + c * 32, rr);
+        tld_wait();
+#pragma unroll
+        for (int q = 0; q < 32; ++q) atomicAdd(dst + (long long)(c * 32 + q) * h, __uint_as_float(rr[q]) * scale);
+      }
+    };
+    for (int i = 0; i < nq; ++i) {
+      const int buf = i & 1, q0 = (qb0 + i) * kBQb;
+      bar_wait(&sm.q_full[buf], (i >> 1) & 1);  // L, D of this block
+      bar_wait(&sm.s_full, i & 1);
+      fence_after();
+      float p[kBQb], ds[kBQb];
+#pragma unroll
+      for (int c = 0; c < kBQb / 32; ++c) {
+        uint32_t a[32], b[32];
+        tld32(tmem + lb + kST + c * 32, a);
+        tld32(tmem + lb + kDPT + c * 32, b);
+        tld_wait();
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int qi = c * 32 + q;
+          float pv = exp2f(__uint_as_float(a[q]) * scale_log2 - sm.L[buf][qi] * 1.4426950408889634f);
+          if (q0 + qi < key) pv = 0.0f;  // causal
+          p[qi] = pv;
+          ds[qi] = pv * (__uint_as_float(b[q]) - sm.D[buf][qi]);
+        }
+      }
+      if (i > 0) drain_dq(i - 1);  // also: MMAs of block i-1 finished reading P^T / dS^T
+#pragma unroll
+      for (int pc = 0; pc < 8; ++pc) {
+        const float* v = p + pc * 8;
+        const float* w = ds + pc * 8;
+        *reinterpret_cast<uint4*>(sm.PT + rowoff + ((pc ^ swz) << 4)) =
+            make_uint4(pack(v[0], v[1]), pack(v[2], v[3]), pack(v[4], v[5]), pack(v[6], v[7]));
+        *reinterpret_cast<uint4*>(sm.dST + rowoff + ((pc ^ swz) << 4)) =
+            make_uint4(pack(w[0], w[1]), pack(w[2], w[3]), pack(w[4], w[5]), pack(w[6], w[7]));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      fence_before();
+      bar_arrive(&sm.ps_full);
+    }
+    drain_dq(nq - 1);  // dq_full of the last block also covers dK / dV
+    bf16* krow = dqkv + (long long)(row0 + key) * 3 * h + h + j * kD;
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {  // 0: dK (scaled), 1: dV
+      bf16* out = krow + part * h;
+      const float f = part == 0 ? scale : 1.0f;
+#pragma unroll
+      for (int c = 0; c < kD / 32; ++c) {
+        uint32_t rr[32];
+        tld32(tmem + lb + (part == 0 ? kDK : kDV) + c * 32, rr);
+        tld_wait();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          w.x = pack(__uint_as_float(rr[8 * q]) * f, __uint_as_float(rr[8 * q + 1]) * f);
+          w.y = pack(__uint_as_float(rr[8 * q + 2]) * f, __uint_as_float(rr[8 * q + 3]) * f);
+          w.z = pack(__uint_as_float(rr[8 * q + 4]) * f, __uint_as_float(rr[8 * q + 5]) * f);
+          w.w = pack(__uint_as_float(rr[8 * q + 6]) * f, __uint_as_float(rr[8 * q + 7]) * f);
+          *reinterpret_cast<uint4*>(out + c * 32 + 8 * q) = w;
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -357,6 +577,43 @@ cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s,
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)kD);
   count_launch();
   fa_fwd_tc_kernel<<<dim3(s / kBQ, b * H), kThreadsFa, smem, st>>>(map, (bf16*)o, lse, s, h, H, scale_log2);
+  return cudaGetLastError();
+}
+
+// dqkv: writes the dK / dV columns; dq_acc (fp32 [b*s][h], zeroed by the
+// caller) receives dQ; D = rowsum(dO * O) per (bh, q).
+cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* D, void* dqkv,
+                             float* dq_acc, int b, int s, int h, int H, cudaStream_t st) {
+  CUtensorMap mq, mq64, md;
+  const cuuint32_t elem[2] = {1, 1};
+  for (int rows : {128, 64}) {
+    const cuuint64_t dims[2] = {(cuuint64_t)3 * h, (cuuint64_t)b * s};
+    const cuuint64_t strides[1] = {(cuuint64_t)3 * h * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)rows};
+    if (encoder()(rows == 128 ? &mq : &mq64, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims,
+                  strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)h, (cuuint64_t)b * s};
+    const cuuint64_t strides[1] = {(cuuint64_t)h * 2};
+    const cuuint32_t box[2] = {64, 64};
+    if (encoder()(&md, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(dout), dims, strides, box, elem,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  const int smem = (int)sizeof(FaBwdSmem) + 1024;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(fa_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  count_launch();
+  fa_bwd_tc_kernel<<<dim3(s / kBK, b * H), kThreadsFa, smem, st>>>(mq, mq64, md, lse, D, (bf16*)dqkv, dq_acc, s, h, H,
+                                                                    1.0f / sqrtf((float)kD));
   return cudaGetLastError();
 }
 
