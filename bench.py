@@ -38,6 +38,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
+# one metric string for both arms (the driver computes the ours/reference ratio)
+METRIC = "tokens/sec (GPT-1.3B training, vertical schedule + alpha-delayed optimizer step, BASELINE configs[1])"
+
 CONFIGS = {
     # name: (N, h, heads, s, b, vocab, M, split, alpha)
     "gpt1.3b": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2),
@@ -183,7 +186,7 @@ def run_reference(args):
         times.append(dt)
     t_layer = float(np.mean(times))
     value = toks / (N * t_layer)
-    line = {"impl": "reference", "metric": "tokens/sec (GPT-1.3B vertical schedule, 1 B200 vs host CPU)",
+    line = {"impl": "reference", "metric": METRIC,
             "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_layer * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
@@ -195,8 +198,11 @@ def run_reference(args):
 
 def config_dict(args):
     N, h, H, s, b, V, M, split, alpha = CONFIGS[args.config]
-    return {"workload": f"{args.config}: GPT N={N} h={h} heads={H} s={s} b={b} vocab={V}, vertical schedule, "
+    M = args.microbatches or M
+    alpha = alpha if args.schedule == "vertical" else 0.0
+    return {"workload": f"{args.config}: GPT N={N} h={h} heads={H} s={s} b={b} vocab={V}, {args.schedule} schedule, "
                         f"M={M} micro-batches/iteration, split(x_ckpt,x_param,x_opt)={split}, alpha={alpha}",
+            "schedule": args.schedule,
             "global_batch": M * b * max(args.gpus, 1), "seq_len": s, "microbatches": M, "alpha": alpha,
             "split": list(split), "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single",
             "l2": "working set (2.4 GB params/iteration streamed) >> 126 MB L2; no flush needed"}
@@ -216,7 +222,11 @@ def run_ours(args):
     N, h, H, s, b, V, M, split, alpha = CONFIGS[args.config]
     M = args.microbatches or M
     model = gs.ModelSpec(N, h, H, s, b, 2, 4, 3, 1)
-    plan = gs.build_vertical(model, M, gs.StorageSplit(*split), alpha)
+    if args.schedule == "horizontal":
+        alpha = 0.0
+        plan = gs.build_horizontal(model, M, gs.StorageSplit(*split))
+    else:
+        plan = gs.build_vertical(model, M, gs.StorageSplit(*split), alpha)
     nvme = os.environ.get("GS_NVME_DIR", "/tmp")
     eng = gs.Engine(plan, model, V, gs.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0), seed=1234 + rank,
                     device=torch.cuda.current_device(), nvme_dir=nvme, opt_tier=0, profile=True)
@@ -273,7 +283,7 @@ def run_ours(args):
     t_roof = max(t_comp, t_h2d, t_d2h)
     ms_step = dev_ms / K
     other = {k: v for k, v in prof.items() if k != "gemm"}
-    line = {"metric": "tokens/sec (GPT-1.3B vertical schedule + alpha-delayed optimizer, BASELINE configs[1])",
+    line = {"metric": METRIC,
             "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic tokens (uniform ids), random-init N(0,0.02) weights",
@@ -313,6 +323,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="gpt1.3b", choices=sorted(CONFIGS))
     ap.add_argument("--microbatches", type=int, default=0)
+    ap.add_argument("--schedule", default="vertical", choices=["vertical", "horizontal"],
+                    help="horizontal = the micro-batch-major ablation baseline (BASELINE configs[1])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -237,7 +237,6 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   if (plan.kind.variant == ScheduleVariant::SingleFB)
     throw ValidationError("executor: single-fb plans are outside the hot path");
   horizontal = plan.kind.variant == ScheduleVariant::Horizontal;
-  if (horizontal) throw ValidationError("executor: horizontal plans are not executable yet (vertical hot path only)");
   if (ms.low_precision_bytes != 2 && ms.low_precision_bytes != 4)
     throw ValidationError("executor: low_precision_bytes must be 2 (bf16) or 4 (fp32)");
   if (ms.full_precision_bytes != 4 || ms.optimizer_states_per_element != 3)
@@ -466,6 +465,7 @@ void Executor::Impl::build_tasks() {
     std::map<std::pair<int, int>, u64> next_lo;  // (layer, stage) -> running chunk offset
     for (size_t i = 0; i < n; ++i) {
       const Task& t = plan.tasks[i];
+      if (horizontal) fwd = false;  // no delayed slice; every SSD read refreshes the whole tier
       if (fwd && t.kind == TaskKind::Xfer && t.data == DataKind::Param && t.layer == N - 1 &&
           ((t.link == LinkKind::SSD_Read && t.stage == N - 2) || (t.link == LinkKind::PCIe_H2D && t.stage == N - 1)))
         fwd = false;
@@ -536,13 +536,21 @@ void Executor::Impl::hazards() {
       case TaskKind::FixedOps: break;
       case TaskKind::FwdCompute:
         R(slot_id(kDevParam, par));
-        if (!horizontal && l > 0) R(m == first_mb(st) ? slot_id(kOutY, parm1, m) : slot_id(kInX, par, m));
-        W(slot_id(kOutY, horizontal ? 0 : par, m));
+        if (horizontal) {  // activation carried in HBM layer to layer; input staged for the ckpt D2H
+          if (l > 0) R(slot_id(kInG, parm1, 0));
+          W(slot_id(kInG, par, 0));
+          W(slot_id(kOutY, par, 0));
+          break;
+        }
+        if (l > 0) R(m == first_mb(st) ? slot_id(kOutY, parm1, m) : slot_id(kInX, par, m));
+        W(slot_id(kOutY, par, m));
         break;
       case TaskKind::RecomputeAndBwd:
         R(slot_id(kDevParam, par));
         if (horizontal) {
-          R(slot_id(kInX, 0, m));
+          R(slot_id(kInX, par, 0));
+          if (l < N - 1) R(slot_id(kOutG, parm1, 0));
+          W(slot_id(kOutG, par, 0));
           R(slot_id(kGrad, l % grad_ring));
           W(slot_id(kGrad, l % grad_ring));
           break;
@@ -580,11 +588,21 @@ void Executor::Impl::hazards() {
             }
             break;
           case DataKind::Ckpt:
-            if (horizontal) {
-              if (t.link == LinkKind::PCIe_D2H) { R(slot_id(kOutY, 0, m)); W(slot_id(kCkptImg, l, m)); }
-              else if (t.link == LinkKind::PCIe_H2D) { R(slot_id(kCkptImg, l, m)); R(slot_id(kCkptRd, l, m)); W(slot_id(kInX, 0, m)); }
-              else if (t.link == LinkKind::SSD_Write) R(slot_id(kCkptImg, l, m));
-              else W(slot_id(kCkptRd, l, m));
+            if (horizontal) {  // checkpoint (l, m) = the INPUT of layer l (schedule.cpp:186-209)
+              if (t.link == LinkKind::PCIe_D2H) {
+                R(slot_id(kOutY, par, 0));
+                W(slot_id(kCkptImg, l, m));
+              } else if (t.link == LinkKind::PCIe_H2D) {
+                R(slot_id(kCkptImg, l, m));
+                R(slot_id(kCkptRd, l, m));
+                W(slot_id(kInX, par, 0));
+              } else if (t.link == LinkKind::SSD_Write) {
+                R(slot_id(kCkptImg, l, m));
+                W(slot_id(kCkptFile, l, m));
+              } else {
+                W(slot_id(kCkptRd, l, m));
+                R(slot_id(kCkptFile, l, m));
+              }
               break;
             }
             if (t.link == LinkKind::PCIe_D2H) {
@@ -857,18 +875,18 @@ void Executor::Impl::compute_task(const Task& t, int it) {
       lc.n += 1;
       x = ws.x0;
     } else if (horizontal) {
-      x = ck(out_y, 0, m);
+      x = ck(in_g, parm1, 0);  // previous layer's output of the same micro-batch
     } else {
       x = m == first_mb(st) ? ck(out_y, parm1, m) : ck(in_x, par, m);
     }
-    void* y = horizontal ? ws.tmp : ck(out_y, par, m);
     if (horizontal) {
-      // horizontal: the D2H'd checkpoint is this layer's INPUT (schedule.cpp:186-188)
-      if (x != ck(out_y, 0, m))
-        cuda_check(cudaMemcpyAsync(ck(out_y, 0, m), x, cb, cudaMemcpyDeviceToDevice, s_gpu), "ckpt stage");
+      // horizontal checkpoints are layer INPUTS (schedule.cpp:186-188): stage a
+      // copy for the D2H so the carry buffer can move on
+      cuda_check(cudaMemcpyAsync(ck(out_y, par, 0), x, cb, cudaMemcpyDeviceToDevice, s_gpu), "ckpt stage");
+      cuda_check(layer_forward(d, W, x, ck(in_g, par, 0), ws, s_gpu, lc), "layer_forward");
+    } else {
+      cuda_check(layer_forward(d, W, x, ck(out_y, par, m), ws, s_gpu, lc), "layer_forward");
     }
-    cuda_check(layer_forward(d, W, horizontal ? ck(out_y, 0, m) : x, y, ws, s_gpu, lc), "layer_forward");
-    if (horizontal) cuda_check(cudaMemcpyAsync(ck(in_g, 0, m), y, cb, cudaMemcpyDeviceToDevice, s_gpu), "carry");
     launches += lc.n;
     return;
   }
@@ -881,7 +899,7 @@ void Executor::Impl::compute_task(const Task& t, int it) {
     lc.n += 1;
     x = ws.x0;
   } else {
-    x = horizontal ? ck(in_x, 0, m) : ck(in_x, par, m);
+    x = horizontal ? ck(in_x, par, 0) : ck(in_x, par, m);
   }
   HeadArgs head;
   const HeadArgs* hp = nullptr;
@@ -894,16 +912,15 @@ void Executor::Impl::compute_task(const Task& t, int it) {
     head.loss_sum = dev_loss + it;
     hp = &head;
   } else if (horizontal) {
-    dy = ck(out_g, 1, m);
+    dy = ck(out_g, parm1, 0);  // dx of layer l+1, same micro-batch
   } else {
     dy = m == first_mb(st) ? ck(out_g, parm1, m) : ck(in_g, par, m);
   }
-  void* dx = horizontal ? ck(out_g, 0, m) : ck(out_g, par, m);
+  void* dx = horizontal ? ck(out_g, par, 0) : ck(out_g, par, m);
   bool first;
   if (horizontal) first = (m == 0);  // later MBs accumulate onto the fetched partial sum
   else first = (m == first_mb(st));
   cuda_check(layer_backward(d, W, x, dy, dx, gslot, first, hp, ws, s_gpu, lc), "layer_backward");
-  if (horizontal && l > 0) cuda_check(cudaMemcpyAsync(ck(out_g, 1, m), dx, cb, cudaMemcpyDeviceToDevice, s_gpu), "carry");
   if (l == 0) {
     cuda_check(gs::embed_bwd(d.dt, tok, dx, fx_grad, fx_grad + 1LL * d.V * d.h, d.b, d.s, d.h, s_gpu), "embed_bwd");
     lc.n += 1;
@@ -994,8 +1011,8 @@ void Executor::Impl::xfer_task(const Task& t, int it, u64& phys) {
     case DataKind::Ckpt: {
       if (horizontal) {
         Blob& b = ckpt_blob[static_cast<size_t>(l * M + m)];
-        if (t.link == LinkKind::PCIe_D2H) phys = download(b, 0, cb, ck(out_y, 0, m), s_d2h);
-        else if (t.link == LinkKind::PCIe_H2D) phys = upload(b, 0, cb, ck(in_x, 0, m), Src::ReadStaging, s_h2d, ~0ull);
+        if (t.link == LinkKind::PCIe_D2H) phys = download(b, 0, cb, ck(out_y, par, 0), s_d2h);
+        else if (t.link == LinkKind::PCIe_H2D) phys = upload(b, 0, cb, ck(in_x, par, 0), Src::ReadStaging, s_h2d, ~0ull);
         else if (t.link == LinkKind::SSD_Write) phys = ssd_io(b, 0, cb, true);
         else phys = ssd_io(b, 0, cb, false);
         break;
