@@ -17,9 +17,11 @@ implementation is the C oracle port (oracle/gs_oracle.c, fp32, OpenMP) on a
 bounded sample (one layer's forward + recompute + backward at the workload's
 b*s tokens... see `cpu_sample`), extrapolated to the model.
 
-Multi-GPU: one process per GPU (torchrun); each rank runs its own replica of
-the workload (dp sharding with NCCL is not wired into the executor yet, so
-scaling is "weak", replicas only) and rank 0 reports max-over-ranks time.
+Multi-GPU: one process per GPU (torchrun).  ZeRO-3 data parallelism inside
+the executor: each rank runs its own M micro-batches (global batch grows with
+N: scaling "weak"), owns 1/N of every layer's params / grads / optimizer state,
+all-gathers layer shards (NCCL) before each stage and reduce-scatters the fp32
+layer gradient after it; rank 0 reports max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -204,15 +206,15 @@ def config_dict(args):
                         f"M={M} micro-batches/iteration, split(x_ckpt,x_param,x_opt)={split}, alpha={alpha}",
             "schedule": args.schedule,
             "global_batch": M * b * max(args.gpus, 1), "seq_len": s, "microbatches": M, "alpha": alpha,
-            "split": list(split), "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single",
+            "split": list(split), "parallelism": f"zero3-dp{args.gpus}" if args.gpus > 1 else "single",
             "l2": "working set (2.4 GB params/iteration streamed) >> 126 MB L2; no flush needed"}
 
 
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
+    import torch.distributed as dist
     if world > 1:
-        import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     else:
@@ -221,15 +223,23 @@ def run_ours(args):
     import oracle_bindings as ob
     N, h, H, s, b, V, M, split, alpha = CONFIGS[args.config]
     M = args.microbatches or M
-    model = gs.ModelSpec(N, h, H, s, b, 2, 4, 3, 1)
+    model = gs.ModelSpec(N, h, H, s, b, 2, 4, 3, world)  # ZeRO-3 over the ranks
     if args.schedule == "horizontal":
         alpha = 0.0
         plan = gs.build_horizontal(model, M, gs.StorageSplit(*split))
     else:
         plan = gs.build_vertical(model, M, gs.StorageSplit(*split), alpha)
     nvme = os.environ.get("GS_NVME_DIR", "/tmp")
-    eng = gs.Engine(plan, model, V, gs.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0), seed=1234 + rank,
-                    device=torch.cuda.current_device(), nvme_dir=nvme, opt_tier=0, profile=True)
+    nccl_id = None
+    if world > 1:  # rank 0's NCCL unique id, shared through the torch process group
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(gs.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
+    eng = gs.Engine(plan, model, V, gs.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0), seed=1234,
+                    device=torch.cuda.current_device(), nvme_dir=nvme, opt_tier=0, profile=True, rank=rank,
+                    world=world, nccl_id=nccl_id)
     g = ob.Geometry(n_layers=N, hidden=h, heads=H, seq=s, mb_size=b, vocab=V)
     K, W = args.steps, args.warmup
     tokens = ob.make_tokens(g, W + 2 * K, M, seed=7 + rank)

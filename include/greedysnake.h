@@ -107,7 +107,13 @@ typedef struct gs_engine_config {
   int opt_tier;            /* 0 auto, 1 HBM, 2 pinned host */
   int record_trace;
   int profile_kernels;     /* CUDA-event timing per kernel class (gs_engine_kernel_profile) */
+  int rank, world;         /* ZeRO-3 data parallelism: model.data_parallel_degree == world */
+  const uint8_t* nccl_id;  /* 128-byte ncclUniqueId from gs_nccl_unique_id() on rank 0 (world > 1) */
+  int force_collectives;   /* run the sharded / NCCL path even at world == 1 */
 } gs_engine_config;
+
+/* ncclGetUniqueId() for rank 0 of a data-parallel job */
+int gs_nccl_unique_id(uint8_t out[128]);
 
 typedef struct gs_run_report {
   double total_ms;          /* CUDA-event time of the whole run */

@@ -52,7 +52,11 @@ struct ExecConfig {
   OptTier opt_tier = OptTier::Auto;
   bool record_trace = false;   // per-task timestamps (adds event records)
   bool profile_kernels = false;  // CUDA-event timing per kernel class on the compute stream
-  int rank = 0, world = 1;     // data parallel (model.data_parallel_degree == world)
+  // ZeRO-3 data parallelism: one executor per rank, model.data_parallel_degree
+  // == world; rank 0's ncclUniqueId (128 bytes) shared out of band.
+  int rank = 0, world = 1;
+  std::vector<uint8_t> nccl_id;
+  bool force_collectives = false;  // run the sharded code path even at world == 1 (tests)
 };
 
 struct TraceRecord {

@@ -86,7 +86,8 @@ class _EngineConfig(C.Structure):
     _fields_ = [("model", _ModelSpec), ("vocab_size", C.c_int), ("lr", C.c_float), ("beta1", C.c_float),
                 ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float), ("seed", C.c_uint64),
                 ("device", C.c_int), ("nvme_dir", C.c_char_p), ("odirect", C.c_int), ("opt_tier", C.c_int),
-                ("record_trace", C.c_int), ("profile_kernels", C.c_int)]
+                ("record_trace", C.c_int), ("profile_kernels", C.c_int), ("rank", C.c_int), ("world", C.c_int),
+                ("nccl_id", C.c_void_p), ("force_collectives", C.c_int)]
 
 
 class _RunReport(C.Structure):
@@ -289,6 +290,21 @@ def overlap_window(plan: SchedulePlan) -> int:
     return int(lib().gs_plan_overlap_window(plan.handle))
 
 
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId() (rank 0 of a data-parallel job)."""
+    buf = (C.c_uint8 * 128)()
+    check(lib().gs_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def shard_range(params_per_layer: int, world: int, rank: int) -> tuple:
+    """[lo, hi) of a layer's elements owned by `rank` (ZeRO-3 shards of
+    ceil(P / world) elements, the last one short) — the executor's layout."""
+    ps = -(-params_per_layer // world)
+    lo = min(params_per_layer, rank * ps)
+    return lo, min(params_per_layer, lo + ps)
+
+
 def simulate(plan: SchedulePlan, machine: MachineSpec) -> dict:
     """report_to_json(offsim::simulate(plan, machine)) (simulator.hpp:34)."""
     n = C.c_size_t()
@@ -328,14 +344,18 @@ class Engine:
 
     def __init__(self, plan: SchedulePlan, model: ModelSpec, vocab_size: int, adam: AdamConfig = AdamConfig(),
                  seed: int = 42, device: int = 0, nvme_dir: str = "/tmp", odirect: bool = True, opt_tier: int = 0,
-                 record_trace: bool = False, profile: bool = False):
+                 record_trace: bool = False, profile: bool = False, rank: int = 0, world: int = 1,
+                 nccl_id: bytes | None = None, force_collectives: bool = False):
         self.model = model
         self.vocab_size = vocab_size
         self.plan = plan
         self.microbatches = plan.as_dict()["microbatches"] if len(plan) < 20000 else None
         self._nvme = nvme_dir.encode()
+        self._id = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         cfg = _EngineConfig(model._c(), vocab_size, adam.lr, adam.beta1, adam.beta2, adam.eps, adam.weight_decay,
-                            seed, device, self._nvme, int(odirect), opt_tier, int(record_trace), int(profile))
+                            seed, device, self._nvme, int(odirect), opt_tier, int(record_trace), int(profile),
+                            rank, world, C.cast(self._id, C.c_void_p) if self._id is not None else None,
+                            int(force_collectives))
         h = C.c_void_p()
         check(lib().gs_engine_create(plan.handle, C.byref(cfg), C.byref(h)))
         self._h = h

@@ -3,6 +3,7 @@
 // convention, proj/tools/offsim_main.cpp:400-409) and keeps the last error
 // message per thread.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <cstring>
 #include <exception>
@@ -213,6 +214,10 @@ int gs_engine_create(const gs_plan* plan, const gs_engine_config* c, gs_engine**
     cfg.opt_tier = static_cast<offsim::OptTier>(c->opt_tier);
     cfg.record_trace = c->record_trace != 0;
     cfg.profile_kernels = c->profile_kernels != 0;
+    cfg.rank = c->rank;
+    cfg.world = c->world > 0 ? c->world : 1;
+    if (c->nccl_id) cfg.nccl_id.assign(c->nccl_id, c->nccl_id + 128);
+    cfg.force_collectives = c->force_collectives != 0;
     auto e = std::make_unique<gs_engine>();
     e->ex = std::make_unique<offsim::Executor>(plan->plan, cfg);
     *out = e.release();
@@ -349,5 +354,16 @@ int gs_layer_backward(int dtype, int b, int s, int h, int heads, const void* W, 
   return layer_call(dtype, b, s, h, heads, false, W, x, dy, dx, dW, first, stream);
 }
 int64_t gs_launch_count(void) { return gs::launch_counter_ref(); }
+
+int gs_nccl_unique_id(uint8_t out[128]) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) {
+    g_error = "NCCL: ncclGetUniqueId failed";
+    return GS_ERR_RUNTIME;
+  }
+  std::memcpy(out, &id, sizeof(id));
+  return GS_OK;
+}
 
 }  // extern "C"

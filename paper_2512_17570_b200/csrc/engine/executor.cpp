@@ -22,6 +22,7 @@
 #include "offsim/executor.hpp"
 
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -128,6 +129,14 @@ struct Executor::Impl {
   u64 el_now = 0, el_late = 0;
   bool horizontal = false;
   int grad_ring = 3;
+  // ZeRO-3 data parallelism: rank R of W owns elements
+  // [e_lo, e_hi) of every layer (shards of Ps = ceil(P / W), the last one
+  // padded); params are all-gathered per stage, gradients reduce-scattered.
+  int W = 1, R = 0;
+  u64 Ps = 0, e_lo = 0, e_hi = 0, n_my = 0, loc_now = 0, loc_late = 0;
+  bool dp = false;
+  ncclComm_t comm = nullptr;
+  std::vector<float*> grad_shard;  // [ring] reduce-scatter output (aliases grad_slot when !dp)
 
   // streams
   cudaStream_t s_gpu = nullptr, s_h2d = nullptr, s_d2h = nullptr, s_opt = nullptr;
@@ -243,8 +252,12 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
     throw ValidationError("executor: fp32 gradients and three Adam states required");
   if (ms.hidden_dim % ms.num_heads || ms.hidden_dim / ms.num_heads > 128 || ms.hidden_dim > 12288)
     throw ValidationError("executor: head_dim must divide hidden and be <= 128; hidden <= 12288");
-  if (ms.data_parallel_degree != 1 || cfg.world != 1)
-    throw ValidationError("executor: data parallel runs go through the dp driver (one executor per rank, dp=1 plan)");
+  if (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world)
+    throw ValidationError("executor: rank must be in [0, world)");
+  if (ms.data_parallel_degree != cfg.world)
+    throw ValidationError("executor: model.data_parallel_degree must equal the number of ranks (world)");
+  if (cfg.world > 1 && horizontal)
+    throw ValidationError("executor: data-parallel execution covers the vertical schedule");
   if (plan.num_layers != ms.num_layers) throw ValidationError("executor: plan and model disagree on num_layers");
   if (cfg.vocab_size < 2) throw ValidationError("executor: vocab_size must be >= 2");
 
@@ -262,6 +275,23 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   cb = ls.ckpt_bytes_per_mb;
   el_late = horizontal ? 0 : scaled_portion(P, plan.kind.delay_ratio);
   el_now = P - el_late;
+  W = cfg.world;
+  R = cfg.rank;
+  dp = W > 1 || cfg.force_collectives;
+  Ps = (P + static_cast<u64>(W) - 1) / static_cast<u64>(W);
+  e_lo = std::min<u64>(P, static_cast<u64>(R) * Ps);
+  e_hi = std::min<u64>(P, e_lo + Ps);
+  n_my = e_hi - e_lo;
+  loc_now = el_now > e_lo ? std::min<u64>(el_now - e_lo, n_my) : 0;
+  loc_late = n_my - loc_now;
+  if (dp) {
+    if (cfg.nccl_id.size() != sizeof(ncclUniqueId))
+      throw ValidationError("executor: data-parallel run needs the 128-byte NCCL unique id of rank 0");
+    ncclUniqueId id;
+    std::memcpy(&id, cfg.nccl_id.data(), sizeof(id));
+    cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice");
+    if (ncclCommInitRank(&comm, W, id, R) != ncclSuccess) throw std::runtime_error("NCCL: ncclCommInitRank failed");
+  }
 
   cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice");
   (void)cudaGetLastError();  // do not inherit a stale error of an earlier, unrelated call
@@ -271,7 +301,7 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   cuda_check(cudaStreamCreateWithFlags(&s_opt, cudaStreamNonBlocking), "stream");
 
   // ---- optimizer tier placement
-  const u64 opt_bytes = 12 * P;
+  const u64 opt_bytes = 12 * Ps;  // this rank's shard of the layer's [master, m, v]
   const u64 cpu_opt = cpu_portion(opt_bytes, plan.split.x_opt);
   bool opt_hbm = cfg.opt_tier == OptTier::Hbm;
   if (cfg.opt_tier == OptTier::Auto) {
@@ -282,12 +312,17 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   }
 
   // ---- device buffers
-  for (int i = 0; i < 2; ++i) dev_param[i] = dmalloc(pb);
+  const u64 lpb = static_cast<u64>(d.lp());
+  for (int i = 0; i < 2; ++i) dev_param[i] = dmalloc(lpb * Ps * static_cast<u64>(W));  // gathered layer
   grad_ring = horizontal ? 2 : 3;
-  for (int i = 0; i < grad_ring; ++i) grad_slot.push_back(static_cast<float*>(dmalloc(4 * P)));
+  for (int i = 0; i < grad_ring; ++i) {
+    grad_slot.push_back(static_cast<float*>(dmalloc(4 * Ps * static_cast<u64>(W))));
+    cuda_check(cudaMemset(grad_slot.back(), 0, 4 * Ps * static_cast<u64>(W)), "memset");  // shard padding
+    grad_shard.push_back(dp ? static_cast<float*>(dmalloc(4 * Ps)) : grad_slot.back());
+  }
   retain.assign(static_cast<size_t>(N), nullptr);
-  if (el_late > 0)
-    for (int l = 0; l < N; ++l) retain[static_cast<size_t>(l)] = static_cast<float*>(dmalloc(4 * el_late));
+  if (loc_late > 0)
+    for (int l = 0; l < N; ++l) retain[static_cast<size_t>(l)] = static_cast<float*>(dmalloc(4 * loc_late));
   n_fixed = static_cast<long long>(d.V + d.s) * d.h;
   fx_master = static_cast<float*>(dmalloc(4 * n_fixed));
   fx_m = static_cast<float*>(dmalloc(4 * n_fixed));
@@ -318,9 +353,9 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   if (need_nvme) nvme = std::make_unique<NvmeFile>(cfg.nvme_dir, cfg.odirect, 8);
   const u64 lp = static_cast<u64>(d.lp());
   for (int l = 0; l < N; ++l) {
-    param_blob.push_back(make_blob(pb, {lp * el_now}, cpu_portion(pb, plan.split.x_param), false));
-    opt_blob.push_back(make_blob(opt_bytes, {12 * el_now}, cpu_opt, opt_hbm));
-    host_grad.push_back(arena.alloc(4 * P));
+    param_blob.push_back(make_blob(lp * Ps, {lp * loc_now}, cpu_portion(lp * Ps, plan.split.x_param), false));
+    opt_blob.push_back(make_blob(opt_bytes, {12 * loc_now}, cpu_opt, opt_hbm));
+    host_grad.push_back(arena.alloc(4 * Ps));
   }
   for (int l = 0; l < N; ++l)
     for (int m = 0; m < M; ++m) ckpt_blob.push_back(make_blob(cb, {}, cpu_portion(cb, plan.split.x_ckpt), false));
@@ -349,6 +384,7 @@ Executor::Impl::~Impl() {
       if (e) cudaEventDestroy(e);
   if (ev_base) cudaEventDestroy(ev_base);
   free_workspace(ws);
+  if (comm) ncclCommDestroy(comm);
   for (void* p : dev_allocs) cudaFree(p);
   for (cudaStream_t s : {s_gpu, s_h2d, s_d2h, s_opt})
     if (s) cudaStreamDestroy(s);
@@ -402,16 +438,15 @@ Blob Executor::Impl::make_blob(u64 size, std::vector<u64> cuts, u64 cpu_bytes, b
 void Executor::Impl::init_weights() {
   const long long h2 = 1LL * d.h * d.h;
   const double scaled = 0.02 / std::sqrt(2.0 * N);
-  std::vector<float> w(P);
-  std::vector<float> state(12 * P / 4);
-  std::vector<uint8_t> lpbuf(pb);
+  std::vector<float> state(3 * Ps, 0.0f);  // this rank's shard, padding zero
+  std::vector<uint8_t> lpbuf(static_cast<size_t>(d.lp()) * Ps, 0);
   for (int l = 0; l < N; ++l) {
     const uint64_t key = stream_key(cfg.seed, 100 + static_cast<uint64_t>(l));
-    parallel_for(static_cast<long long>(P), [&](long long lo, long long hi) {
+    parallel_for(static_cast<long long>(n_my), [&](long long lo, long long hi) {
       for (long long i = lo; i < hi; ++i) {
-        const bool out_proj = (i >= 3 * h2 && i < 4 * h2) || i >= 8 * h2;
-        const float v = static_cast<float>((out_proj ? scaled : 0.02) * normal_at(key, static_cast<uint64_t>(i)));
-        w[static_cast<size_t>(i)] = v;
+        const long long gi = static_cast<long long>(e_lo) + i;  // element index within the layer
+        const bool out_proj = (gi >= 3 * h2 && gi < 4 * h2) || gi >= 8 * h2;
+        const float v = static_cast<float>((out_proj ? scaled : 0.02) * normal_at(key, static_cast<uint64_t>(gi)));
         state[3 * static_cast<size_t>(i)] = v;
         state[3 * static_cast<size_t>(i) + 1] = 0.0f;
         state[3 * static_cast<size_t>(i) + 2] = 0.0f;
@@ -848,6 +883,9 @@ void Executor::Impl::compute_task(const Task& t, int it) {
                "tokens");
     cuda_check(cudaMemsetAsync(dev_loss + it, 0, sizeof(double), s_gpu), "loss");
     if (fixed_done < git) {  // embedding / head step with the previous iteration's grads
+      if (dp && ncclAllReduce(fx_grad, fx_grad, static_cast<size_t>(n_fixed), ncclFloat, ncclSum, comm, s_gpu) !=
+                    ncclSuccess)
+        throw std::runtime_error("NCCL: all-reduce of the embedding gradient failed");
       gs::AdamHyper hp{cfg.adam.lr, cfg.adam.beta1, cfg.adam.beta2, cfg.adam.eps, cfg.adam.weight_decay};
       cuda_check(gs::adam_step(hp, static_cast<int>(git), 1.0f, fx_master, fx_m, fx_v, fx_grad, fx_lp, d.dt, n_fixed,
                                s_gpu),
@@ -863,7 +901,15 @@ void Executor::Impl::compute_task(const Task& t, int it) {
   const int par = st % 2, parm1 = (st + 1) % 2;
   const long long tok_n = 1LL * d.b * (d.s + 1);
   const int32_t* tok = dev_tok[slot] + m * tok_n;
-  const void* W = dev_param[par];
+  const void* Wt = dev_param[par];
+  if (dp && (horizontal || m == first_mb(st))) {
+    // first compute of the stage: gather the layer from the per-rank shards
+    // (in place: this rank's H2D chunks already sit at offset R * shard)
+    const u64 sb = static_cast<u64>(d.lp()) * Ps;
+    if (ncclAllGather(static_cast<uint8_t*>(dev_param[par]) + sb * R, dev_param[par], sb, ncclUint8, comm, s_gpu) !=
+        ncclSuccess)
+      throw std::runtime_error("NCCL: all-gather of the layer parameters failed");
+  }
   const void* wte = fx_lp;
   const void* wpe = static_cast<const uint8_t*>(fx_lp) + 1LL * d.V * d.h * d.lp();
   auto ck = [&](std::vector<void*>& v, int p, int mb) { return v[static_cast<size_t>(p * M + mb)]; };
@@ -883,9 +929,9 @@ void Executor::Impl::compute_task(const Task& t, int it) {
       // horizontal checkpoints are layer INPUTS (schedule.cpp:186-188): stage a
       // copy for the D2H so the carry buffer can move on
       cuda_check(cudaMemcpyAsync(ck(out_y, par, 0), x, cb, cudaMemcpyDeviceToDevice, s_gpu), "ckpt stage");
-      cuda_check(layer_forward(d, W, x, ck(in_g, par, 0), ws, s_gpu, lc), "layer_forward");
+      cuda_check(layer_forward(d, Wt, x, ck(in_g, par, 0), ws, s_gpu, lc), "layer_forward");
     } else {
-      cuda_check(layer_forward(d, W, x, ck(out_y, par, m), ws, s_gpu, lc), "layer_forward");
+      cuda_check(layer_forward(d, Wt, x, ck(out_y, par, m), ws, s_gpu, lc), "layer_forward");
     }
     launches += lc.n;
     return;
@@ -908,7 +954,7 @@ void Executor::Impl::compute_task(const Task& t, int it) {
     head.wte = wte;
     head.dwte = fx_grad;
     head.tokens = tok;
-    head.scale = 1.0f / (static_cast<float>(d.T()) * static_cast<float>(M));
+    head.scale = 1.0f / (static_cast<float>(d.T()) * static_cast<float>(M) * static_cast<float>(W));
     head.loss_sum = dev_loss + it;
     hp = &head;
   } else if (horizontal) {
@@ -920,15 +966,22 @@ void Executor::Impl::compute_task(const Task& t, int it) {
   bool first;
   if (horizontal) first = (m == 0);  // later MBs accumulate onto the fetched partial sum
   else first = (m == first_mb(st));
-  cuda_check(layer_backward(d, W, x, dy, dx, gslot, first, hp, ws, s_gpu, lc), "layer_backward");
+  cuda_check(layer_backward(d, Wt, x, dy, dx, gslot, first, hp, ws, s_gpu, lc), "layer_backward");
+  if (dp && !horizontal && m == last_mb(st)) {
+    // full-layer fp32 gradient of this rank's micro-batches -> summed shard
+    if (ncclReduceScatter(gslot, grad_shard[static_cast<size_t>(l % grad_ring)], Ps, ncclFloat, ncclSum, comm, s_gpu) !=
+        ncclSuccess)
+      throw std::runtime_error("NCCL: reduce-scatter of the layer gradient failed");
+  }
   if (l == 0) {
     cuda_check(gs::embed_bwd(d.dt, tok, dx, fx_grad, fx_grad + 1LL * d.V * d.h, d.b, d.s, d.h, s_gpu), "embed_bwd");
     lc.n += 1;
   }
   if (!horizontal && m == last_mb(st) && el_late > 0) {
-    cuda_check(cudaMemcpyAsync(retain[static_cast<size_t>(l)], gslot + el_now, 4 * el_late, cudaMemcpyDeviceToDevice,
-                               s_gpu),
-               "retain");
+    if (loc_late > 0)
+      cuda_check(cudaMemcpyAsync(retain[static_cast<size_t>(l)], grad_shard[static_cast<size_t>(l % grad_ring)] + loc_now,
+                                 4 * loc_late, cudaMemcpyDeviceToDevice, s_gpu),
+                 "retain");
     late_ready[static_cast<size_t>(l)].store(git);
   }
   launches += lc.n;
@@ -975,12 +1028,12 @@ void Executor::Impl::step_task(const Task& t, int it) {
     // retained before the first iteration
     const long long ready = late_ready[static_cast<size_t>(l)].load();
     if (el_late == 0 || ready != git - 1 || late_applied[static_cast<size_t>(l)].load() >= ready) return;
-    apply_adam(l, el_now, P, retain[static_cast<size_t>(l)], static_cast<int>(git), s_opt, it);
+    if (loc_late > 0) apply_adam(l, loc_now, n_my, retain[static_cast<size_t>(l)], static_cast<int>(git), s_opt, it);
     late_applied[static_cast<size_t>(l)].store(ready);
     return;
   }
-  if (el_now > 0)
-    apply_adam(l, 0, el_now, grad_slot[static_cast<size_t>(l % grad_ring)], static_cast<int>(git + 1), s_opt, it);
+  if (loc_now > 0)
+    apply_adam(l, 0, loc_now, grad_shard[static_cast<size_t>(l % grad_ring)], static_cast<int>(git + 1), s_opt, it);
 }
 
 void Executor::Impl::xfer_task(const Task& t, int it, u64& phys) {
@@ -995,16 +1048,18 @@ void Executor::Impl::xfer_task(const Task& t, int it, u64& phys) {
       if (t.link == LinkKind::SSD_Read) {
         // forward: only the immediate slice is re-read (the delayed slice was
         // just produced in DRAM by the delayed step); backward: all of it
-        phys = fwd ? ssd_io(b, 0, lp * el_now, false) : ssd_io(b, 0, b.size, false);
+        phys = fwd ? ssd_io(b, 0, lp * loc_now, false) : ssd_io(b, 0, b.size, false);
       } else if (t.link == LinkKind::SSD_Write) {
-        phys = delayed(t) ? ssd_io(b, lp * el_now, b.size, true) : ssd_io(b, 0, lp * el_now, true);
+        phys = delayed(t) ? ssd_io(b, lp * loc_now, b.size, true) : ssd_io(b, 0, lp * loc_now, true);
       } else {
         // chunk j of the layer's params (dp = 1: the shard is the layer),
         // cut by chunk_size(shard, M, j) in emission order
         const u64 lo = chunk_lo[static_cast<size_t>(t.id)];
         const int use_par = (((st + 1) % 2) + 2) % 2;
         const Src src = fwd ? Src::Auto : Src::ReadStaging;
-        phys = upload(b, lo, lo + t.bytes, static_cast<uint8_t*>(dev_param[use_par]) + lo, src, s_h2d, lp * el_now);
+        // this rank's shard lands at its offset of the gathered layer buffer
+        phys = upload(b, lo, lo + t.bytes, static_cast<uint8_t*>(dev_param[use_par]) + lp * Ps * R + lo, src, s_h2d,
+                      lp * loc_now);
       }
       break;
     }
@@ -1030,7 +1085,7 @@ void Executor::Impl::xfer_task(const Task& t, int it, u64& phys) {
       break;
     }
     case DataKind::GradAccum: {
-      float* g = grad_slot[static_cast<size_t>(l % grad_ring)];
+      float* g = grad_shard[static_cast<size_t>(l % grad_ring)];
       if (t.link == LinkKind::PCIe_D2H) {
         cuda_check(cudaMemcpyAsync(host_grad[static_cast<size_t>(l)], g, t.bytes, cudaMemcpyDeviceToHost, s_d2h), "grad");
       } else {
@@ -1055,7 +1110,7 @@ void Executor::Impl::xfer_task(const Task& t, int it, u64& phys) {
     case DataKind::OptState: {
       Blob& b = opt_blob[static_cast<size_t>(l)];
       const bool late = delayed(t) && !horizontal;
-      const u64 lo = late ? 12 * el_now : 0, hi = late ? b.size : 12 * el_now;
+      const u64 lo = late ? 12 * loc_now : 0, hi = late ? b.size : 12 * loc_now;
       phys = ssd_io(b, lo, hi, t.link == LinkKind::SSD_Write);
       break;
     }
@@ -1201,11 +1256,15 @@ void Executor::flush() {
   for (int l = 0; l < I.N; ++l) {
     const long long ready = I.late_ready[static_cast<size_t>(l)].load();
     if (I.el_late == 0 || ready < 0 || I.late_applied[static_cast<size_t>(l)].load() >= ready) continue;
-    I.apply_adam(l, I.el_now, I.P, I.retain[static_cast<size_t>(l)], static_cast<int>(ready + 1), I.s_opt, -2,
-                 Src::Image);
+    if (I.loc_late > 0)
+      I.apply_adam(l, I.loc_now, I.n_my, I.retain[static_cast<size_t>(l)], static_cast<int>(ready + 1), I.s_opt, -2,
+                   Src::Image);
     I.late_applied[static_cast<size_t>(l)].store(ready);
   }
   if (I.fixed_done < I.global_iter) {
+    if (I.dp && ncclAllReduce(I.fx_grad, I.fx_grad, static_cast<size_t>(I.n_fixed), ncclFloat, ncclSum, I.comm, I.s_opt) !=
+                    ncclSuccess)
+      throw std::runtime_error("NCCL: all-reduce of the embedding gradient failed");
     gs::AdamHyper hp{I.cfg.adam.lr, I.cfg.adam.beta1, I.cfg.adam.beta2, I.cfg.adam.eps, I.cfg.adam.weight_decay};
     cuda_check(gs::adam_step(hp, static_cast<int>(I.global_iter), 1.0f, I.fx_master, I.fx_m, I.fx_v, I.fx_grad, I.fx_lp,
                              I.d.dt, I.n_fixed, I.s_opt),
@@ -1249,7 +1308,8 @@ void read_field(Executor::Impl& I, int layer, int f, float* out) {
       std::memcpy(all.data() + s.lo, s.img, s.size());
   }
   const float* st = reinterpret_cast<const float*>(all.data());
-  for (u64 i = 0; i < I.P; ++i) out[i] = st[3 * i + static_cast<u64>(f)];
+  // this rank's shard [e_lo, e_hi) of the layer (the whole layer when W == 1)
+  for (u64 i = 0; i < I.n_my; ++i) out[I.e_lo + i] = st[3 * i + static_cast<u64>(f)];
 }
 }  // namespace
 
