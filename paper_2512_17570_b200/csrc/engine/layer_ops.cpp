@@ -206,8 +206,8 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
   float* dW2 = dW + 8 * h2;
   // MLP
   GS_TRY(mm(d, h, 4 * h, T, dy, false, ws.g, false, dW2, wg, st, lc, nullptr, nullptr, ws.prof));          // dW2 (+)= dy^T g
-  GS_TRY(mm(d, T, 4 * h, h, dy, true, w2, false, ws.big, Epi::Store, st, lc, nullptr, nullptr, ws.prof));    // dg = dy W2
-  GS_PROF(Other, gelu_bwd(d.dt, ws.u, ws.big, ws.big, 4LL * T * h, st));                  // du
+  // du = (dy W2) * gelu'(u): GELU backward fused into the dgrad epilogue
+  GS_TRY(mm(d, T, 4 * h, h, dy, true, w2, false, ws.big, Epi::MulGeluGrad, st, lc, ws.u, nullptr, ws.prof));
   GS_TRY(mm(d, 4 * h, h, T, ws.big, false, ws.c, false, dW1, wg, st, lc, nullptr, nullptr, ws.prof));       // dW1 (+)= du^T c
   GS_TRY(mm(d, T, h, 4 * h, ws.big, true, w1, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));  // dc = du W1
   GS_PROF(Other, cudaMemcpyAsync(ws.dx1, dy, 1LL * T * h * eb, cudaMemcpyDeviceToDevice, st));

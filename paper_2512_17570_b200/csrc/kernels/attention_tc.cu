@@ -32,7 +32,8 @@ constexpr int kD = 128;       // head dim
 constexpr int kBQ = 128;      // queries per CTA
 constexpr int kBK = 128;      // keys per block
 constexpr int kTile = kBQ * kD * 2;  // 32 KB: one 128 x 128 bf16 tile
-constexpr int kThreadsFa = 256;      // warp 0 TMA, 1 MMA, 2 TMEM alloc, 4-7 softmax
+constexpr int kThreadsFa = 256;      // backward: warp 0 TMA, 1 MMA, 2 TMEM alloc, 4-7 compute
+constexpr int kThreadsFwd = 384;     // forward: warps 4-11 softmax, two per TMEM lane quarter
 
 // ---------------------------------------------------------------- PTX
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -127,9 +128,11 @@ struct FaSmem {
   uint8_t tiles[6][kTile];
   uint64_t q_full, k_full[2], v_full[2], kv_empty[2], s_full[2], p_full, o_done;
   uint32_t tmem;
+  float rmax[2][2][kBQ];  // [block parity][column half][row] partial row maxima
+  float rsum[2][kBQ];     // [column half][row] partial row sums (end of kernel)
 };
 
-__global__ void __launch_bounds__(kThreadsFa, 1)
+__global__ void __launch_bounds__(kThreadsFwd, 1)
     fa_fwd_tc_kernel(const __grid_constant__ CUtensorMap map, bf16* __restrict__ o, float* __restrict__ lse, int s,
                      int h, int H, float scale_log2) {
   extern __shared__ uint8_t raw[];
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(kThreadsFa, 1)
       bar_init(&sm.kv_empty[i], 1);
       bar_init(&sm.s_full[i], 1);
     }
-    bar_init(&sm.p_full, 128);
+    bar_init(&sm.p_full, 256);
     bar_init(&sm.o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -213,22 +216,25 @@ __global__ void __launch_bounds__(kThreadsFa, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===== softmax: thread t owns query row r = t (TMEM lane)
-    const int r = (warp - 4) * 32 + lane;
+    // ===== softmax: warps 4-7 and 8-11 cover TMEM lane quarters twice; the
+    // first set owns key columns 0-63 (and O columns 0-63), the second 64-127.
+    const int wq = (warp - 4) & 3, half = (warp - 4) >> 2;
+    const int r = wq * 32 + lane;  // query row = TMEM lane
     const int qrow = q0 + r;
-    const uint32_t lane_base = ((uint32_t)((warp - 4) * 32)) << 16;
+    const uint32_t lane_base = ((uint32_t)(wq * 32)) << 16;
+    const int c0 = half * 64;      // first key column (and O column) of this thread
     float m_run = -INFINITY, l_run = 0.0f;
     const uint32_t swz = (uint32_t)(r & 7);
-    uint8_t* prow = Ps + (r >> 3) * 1024 + (r & 7) * 128;
+    uint8_t* prow = Ps + half * 16384 + (r >> 3) * 1024 + (r & 7) * 128;
     for (int kb = 0; kb < nblk; ++kb) {
       const int buf = kb & 1;
       bar_wait(&sm.s_full[buf], (kb >> 1) & 1);
       fence_after();
-      float sv[kBK];
+      float sv[64];
 #pragma unroll
-      for (int c = 0; c < kBK / 32; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t rr[32];
-        tld32(tmem + lane_base + buf * 128 + c * 32, rr);
+        tld32(tmem + lane_base + buf * 128 + c0 + c * 32, rr);
         tld_wait();
 #pragma unroll
         for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(rr[i]) * scale_log2;
@@ -236,14 +242,18 @@ __global__ void __launch_bounds__(kThreadsFa, 1)
       const bool diag = kb == qb;
       float mx = m_run;
 #pragma unroll
-      for (int i = 0; i < kBK; ++i) {
-        if (diag && kb * kBK + i > qrow) sv[i] = -INFINITY;
+      for (int i = 0; i < 64; ++i) {
+        if (diag && kb * kBK + c0 + i > qrow) sv[i] = -INFINITY;
         mx = fmaxf(mx, sv[i]);
       }
+      // row max across the two column halves (double-buffered exchange)
+      sm.rmax[buf][half][r] = mx;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      mx = fmaxf(mx, sm.rmax[buf][half ^ 1][r]);
       const float corr = exp2f(m_run - mx);
       float rs = 0.0f;
 #pragma unroll
-      for (int i = 0; i < kBK; ++i) {
+      for (int i = 0; i < 64; ++i) {
         sv[i] = exp2f(sv[i] - mx);
         rs += sv[i];
       }
@@ -256,40 +266,41 @@ __global__ void __launch_bounds__(kThreadsFa, 1)
         // tcgen05.ld/st are warp-collective: rescale when any row of the warp moved
         if (__any_sync(0xffffffffu, corr != 1.0f)) {
 #pragma unroll
-          for (int c = 0; c < kD / 32; ++c) {
+          for (int c = 0; c < 2; ++c) {
             uint32_t rr[32];
-            tld32(tmem + lane_base + 256 + c * 32, rr);
+            tld32(tmem + lane_base + 256 + c0 + c * 32, rr);
             tld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * corr);
-            tst32(tmem + lane_base + 256 + c * 32, rr);
+            tst32(tmem + lane_base + 256 + c0 + c * 32, rr);
           }
           tst_wait();
         }
       }
-      // P row -> K-major 128B-swizzled tile: chunk c (keys 64c..), 16-byte
-      // piece p (8 keys) stored at slot p ^ (row % 8)
+      // P row half -> K-major 128B-swizzled chunk `half`: 16-byte piece p
+      // (8 keys) stored at slot p ^ (row % 8)
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int p = 0; p < 8; ++p) {
-          const float* v = sv + c * 64 + p * 8;
-          uint4 w = make_uint4(pack(v[0], v[1]), pack(v[2], v[3]), pack(v[4], v[5]), pack(v[6], v[7]));
-          *reinterpret_cast<uint4*>(prow + c * 16384 + ((p ^ swz) << 4)) = w;
-        }
+      for (int p = 0; p < 8; ++p) {
+        const float* v = sv + p * 8;
+        uint4 w = make_uint4(pack(v[0], v[1]), pack(v[2], v[3]), pack(v[4], v[5]), pack(v[6], v[7]));
+        *reinterpret_cast<uint4*>(prow + ((p ^ swz) << 4)) = w;
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
       fence_before();
       bar_arrive(&sm.p_full);
     }
-    // epilogue: wait for the last PV, normalise, write O and lse
+    // epilogue: combine the row sums, wait for the last PV, normalise, write
+    sm.rsum[half][r] = l_run;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const float l_tot = l_run + sm.rsum[half ^ 1][r];
     bar_wait(&sm.o_done, (nblk - 1) & 1);
     fence_after();
-    const float inv = 1.0f / l_run;
-    bf16* orow = o + (long long)(row0 + qrow) * h + j * kD;
+    const float inv = 1.0f / l_tot;
+    bf16* orow = o + (long long)(row0 + qrow) * h + j * kD + c0;
 #pragma unroll
-    for (int c = 0; c < kD / 32; ++c) {
+    for (int c = 0; c < 2; ++c) {
       uint32_t rr[32];
-      tld32(tmem + lane_base + 256 + c * 32, rr);
+      tld32(tmem + lane_base + 256 + c0 + c * 32, rr);
       tld_wait();
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -301,7 +312,7 @@ __global__ void __launch_bounds__(kThreadsFa, 1)
         *reinterpret_cast<uint4*>(orow + c * 32 + 8 * q) = w;
       }
     }
-    lse[(long long)bh * s + qrow] = (m_run + log2f(l_run)) * 0.6931471805599453f;
+    if (half == 0) lse[(long long)bh * s + qrow] = (m_run + log2f(l_tot)) * 0.6931471805599453f;
   }
   fence_before();
   __syncthreads();
@@ -331,6 +342,7 @@ struct FaBwdSmem {
   uint8_t Q[2][kHalf], dO[2][kHalf];
   uint8_t PT[kPT], dST[kPT];
   float L[2][kBQb], D[2][kBQb];
+  float dq_stage[kBQb][kD];  // dQ tile for the TMA reduce-add into dq_acc
   uint64_t kv_full, q_full[2], q_empty[2], s_full, ps_full, dq_full;
   uint32_t tmem;
 };
@@ -358,7 +370,7 @@ constexpr uint32_t idesc2(int n, bool a_mn, bool b_mn) {
 
 __global__ void __launch_bounds__(kThreadsFa, 1)
     fa_bwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_q,
-                     const __grid_constant__ CUtensorMap map_do,
+                     const __grid_constant__ CUtensorMap map_do, const __grid_constant__ CUtensorMap map_dq,
                      const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv,
                      float* __restrict__ dq_acc, int s, int h, int H, float scale) {
   extern __shared__ uint8_t raw[];
@@ -451,18 +463,29 @@ __global__ void __launch_bounds__(kThreadsFa, 1)
     const int key = k0 + r;
     const uint32_t swz = (uint32_t)(r & 7);
     const int rowoff = (r >> 3) * 1024 + (r & 7) * 128;
-    auto drain_dq = [&](int i) {  // dQ^T of block i -> fp32 red.add
+    auto drain_dq = [&](int i) {  // dQ^T of block i -> smem [q][d] -> TMA reduce-add into dq_acc
       bar_wait(&sm.dq_full, i & 1);
       fence_after();
-      const int q0 = (qb0 + i) * kBQb;
-      float* dst = dq_acc + (long long)(row0 + q0) * h + j * kD + r;
+      if (r == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
+      asm volatile("bar.sync 2, 128;" ::: "memory");
 #pragma unroll
       for (int c = 0; c < kBQb / 32; ++c) {
         uint32_t rr[32];
         tld32(tmem + lb + kDQ + c * 32, rr);
         tld_wait();
 #pragma unroll
-        for (int q = 0; q < 32; ++q) atomicAdd(dst + (long long)(c * 32 + q) * h, __uint_as_float(rr[q]) * scale);
+        for (int q = 0; q < 32; ++q) sm.dq_stage[c * 32 + q][r] = __uint_as_float(rr[q]) * scale;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (r == 0) {
+        const int q0 = (qb0 + i) * kBQb;
+        asm volatile(
+            "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                reinterpret_cast<uint64_t>(&map_dq)),
+            "r"(su32(&sm.dq_stage[0][0])), "r"(j * kD), "r"(row0 + q0)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     };
     for (int i = 0; i < nq; ++i) {
@@ -501,6 +524,7 @@ __global__ void __launch_bounds__(kThreadsFa, 1)
       bar_arrive(&sm.ps_full);
     }
     drain_dq(nq - 1);  // dq_full of the last block also covers dK / dV
+    if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     bf16* krow = dqkv + (long long)(row0 + key) * 3 * h + h + j * kD;
 #pragma unroll
     for (int part = 0; part < 2; ++part) {  // 0: dK (scaled), 1: dV
@@ -576,7 +600,7 @@ cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s,
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)kD);
   count_launch();
-  fa_fwd_tc_kernel<<<dim3(s / kBQ, b * H), kThreadsFa, smem, st>>>(map, (bf16*)o, lse, s, h, H, scale_log2);
+  fa_fwd_tc_kernel<<<dim3(s / kBQ, b * H), kThreadsFwd, smem, st>>>(map, (bf16*)o, lse, s, h, H, scale_log2);
   return cudaGetLastError();
 }
 
@@ -604,6 +628,16 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
+  CUtensorMap mdq;
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)h, (cuuint64_t)b * s};
+    const cuuint64_t strides[1] = {(cuuint64_t)h * 4};
+    const cuuint32_t box[2] = {128, 64};
+    if (encoder()(&mdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq_acc, dims, strides, box, elem,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
   const int smem = (int)sizeof(FaBwdSmem) + 1024;
   static bool init = false;
   if (!init) {
@@ -612,7 +646,7 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
     init = true;
   }
   count_launch();
-  fa_bwd_tc_kernel<<<dim3(s / kBK, b * H), kThreadsFa, smem, st>>>(mq, mq64, md, lse, D, (bf16*)dqkv, dq_acc, s, h, H,
+  fa_bwd_tc_kernel<<<dim3(s / kBK, b * H), kThreadsFa, smem, st>>>(mq, mq64, md, mdq, lse, D, (bf16*)dqkv, dq_acc, s, h, H,
                                                                     1.0f / sqrtf((float)kD));
   return cudaGetLastError();
 }

@@ -201,7 +201,7 @@ __device__ __forceinline__ void epilogue_chunk(const float (&v)[32], int row, in
   float w[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) w[i] = v[i];
-  if (EPI == (int)Epi::AddResidual) {
+  if (EPI == (int)Epi::AddResidual || EPI == (int)Epi::MulGeluGrad) {
     const uint4* r = reinterpret_cast<const uint4*>(R + o);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -210,8 +210,15 @@ __device__ __forceinline__ void epilogue_chunk(const float (&v)[32], int row, in
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const __nv_bfloat162 p = *reinterpret_cast<const __nv_bfloat162*>(&u[j]);
-        w[8 * q + 2 * j] += __bfloat162float(p.x);
-        w[8 * q + 2 * j + 1] += __bfloat162float(p.y);
+        if (EPI == (int)Epi::AddResidual) {
+          w[8 * q + 2 * j] += __bfloat162float(p.x);
+          w[8 * q + 2 * j + 1] += __bfloat162float(p.y);
+        } else {
+          // round dg to bf16 first: identical to storing dg and running gelu_bwd
+          w[8 * q + 2 * j] = __bfloat162float(__float2bfloat16_rn(w[8 * q + 2 * j])) * gelu_grad_f(__bfloat162float(p.x));
+          w[8 * q + 2 * j + 1] =
+              __bfloat162float(__float2bfloat16_rn(w[8 * q + 2 * j + 1])) * gelu_grad_f(__bfloat162float(p.y));
+        }
       }
     }
   }
@@ -471,6 +478,7 @@ cudaError_t launch_epi(const GemmArgs& g, cudaStream_t s) {
     case Epi::AccumF32: return launch<BN, A_MN, B_MN, 2, CG>(g, s);
     case Epi::StoreGelu: return launch<BN, A_MN, B_MN, 3, CG>(g, s);
     case Epi::StoreF32: return launch<BN, A_MN, B_MN, 4, CG>(g, s);
+    case Epi::MulGeluGrad: return launch<BN, A_MN, B_MN, 5, CG>(g, s);
   }
   return cudaErrorInvalidValue;
 }

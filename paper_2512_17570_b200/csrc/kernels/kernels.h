@@ -21,6 +21,7 @@ enum class Epi {
   AccumF32 = 2,     // Cf32 += acc
   StoreGelu = 3,    // C(dt) = acc, G(dt) = gelu(acc)
   StoreF32 = 4,     // Cf32 = acc
+  MulGeluGrad = 5,  // C(dt) = acc * gelu'(R(dt))   (dgrad of FC2 fused with GELU backward)
 };
 struct GemmArgs {
   int M = 0, N = 0, K = 0;

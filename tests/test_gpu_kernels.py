@@ -84,6 +84,12 @@ def test_tcgen05_fused_epilogues():
     gemm(BF16, A, True, B, True, M, N, K, 3, u, G=g)
     assert rel(u.float(), ref) < 5e-3
     assert rel(g.float(), torch.nn.functional.gelu(u.float(), approximate="tanh")) < 5e-3
+    # GELU backward fused into the dgrad epilogue: (A B^T) * gelu'(R)
+    du = torch.empty(M, N, device=d, dtype=torch.bfloat16)
+    gemm(BF16, A, True, B, True, M, N, K, 5, du, R=R)
+    x = R.float().clone().requires_grad_(True)
+    torch.nn.functional.gelu(x, approximate="tanh").backward(ref.bfloat16().float())
+    assert rel(du.float(), x.grad) < 5e-3
 
 
 @pytest.mark.parametrize("M,N,K", [(64, 64, 64), (100, 70, 33), (256, 192, 128)])
