@@ -210,6 +210,50 @@ def config_dict(args):
             "l2": "working set (2.4 GB params/iteration streamed) >> 126 MB L2; no flush needed"}
 
 
+def calibrate_and_simulate(gs, eng, plan, model, tokens, K, dev_ms):
+    """§8(f): feed the executor's measured per-task times into the
+    reference's MachineSpec and compare simulate()'s predicted iteration time
+    (proj/src/simulator.cpp:77) with the measured one."""
+    import numpy as np
+    eng.set_trace(True)
+    rep = eng.run(tokens, iterations=2)
+    eng.set_trace(False)
+    tasks = [plan.task(i) for i in range(len(plan))]
+    last = [r for r in rep.trace if r["iteration"] == 1]
+    def mean_ms(kind):
+        d = [r["t_end_ms"] - r["t_start_ms"] for r in last if tasks[r["task"]]["kind"] == kind]
+        return float(np.mean(d)) if d else 0.0
+    steps = [(r, tasks[r["task"]]) for r in last if tasks[r["task"]]["kind"] == "cpu_step"]
+    el = sum(t["elements"] for _, t in steps)
+    step_ms = sum(r["t_end_ms"] - r["t_start_ms"] for r, _ in steps)
+    xfer = {}
+    for r in last:
+        t = tasks[r["task"]]
+        if t["kind"] == "xfer":
+            a = xfer.setdefault(t["link"], [0, 0.0])
+            a[0] += t["bytes"]
+            a[1] += r["t_end_ms"] - r["t_start_ms"]
+    bw = {k: (v[0] / (v[1] / 1e3) if v[1] > 0 else 1e12) for k, v in xfer.items()}
+    machine = gs.MachineSpec(gpu_mem_bytes=180 << 30, cpu_usable_dram_bytes=190 << 30,
+                             pcie_h2d_bw=bw.get("H2D", 55e9), pcie_d2h_bw=bw.get("D2H", 55e9),
+                             ssd_read_bw=bw.get("SSD_read", 1e12), ssd_write_bw=bw.get("SSD_write", 1e12),
+                             fwd_compute_time_per_layer_per_mb=mean_ms("fwd") / 1e3,
+                             bwd_compute_time_per_layer_per_mb=mean_ms("bwd") / 1e3,
+                             cpu_step_throughput=el / (step_ms / 1e3) if step_ms > 0 else 1e12,
+                             fixed_overhead_time=mean_ms("fixed_ops") / 1e3, num_gpus=1,
+                             gpu_working_set_bytes=1 << 30, ssd_duplex=True)
+    sim = gs.simulate(plan, machine)
+    measured = dev_ms / K
+    return {"method": "MachineSpec from this run's executor trace (mean task times, per-link achieved "
+                      "bandwidth, Adam elements/s) -> offsim::simulate (proj/src/simulator.cpp:77)",
+            "predicted_iteration_ms": sim["iteration_time"] * 1e3, "measured_iteration_ms": measured,
+            "gap": sim["iteration_time"] * 1e3 / measured - 1.0, "bound_class": sim["bound_class"],
+            "utilization": sim["utilization"],
+            "machine": {"fwd_ms": mean_ms("fwd"), "bwd_ms": mean_ms("bwd"), "fixed_ms": mean_ms("fixed_ops"),
+                        "h2d_gbs": bw.get("H2D", 0) / 1e9, "d2h_gbs": bw.get("D2H", 0) / 1e9,
+                        "adam_gelem_s": (el / (step_ms / 1e3) / 1e9) if step_ms > 0 else None}}
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
@@ -260,6 +304,9 @@ def run_ours(args):
     dev_ms = max_over_ranks(rep.total_ms, world)
     prof = eng.kernel_profile()
     eng.set_profiling(0)
+    calib = None
+    if args.calibrate and world == 1:
+        calib = calibrate_and_simulate(gs, eng, plan, model, tokens[W:W + 2], K, dev_ms)
     # end-to-end through the public call: host tokens, losses read back
     barrier(world)
     t0 = time.perf_counter()
@@ -317,6 +364,7 @@ def run_ours(args):
             "ledger_equals_plan": bool(np.array_equal(led, gs.plan_traffic(plan))),
             "kernel_ms_per_step": {k: v[1] * v[3] / max(v[2], 1) / K for k, v in prof.items()},
             "losses": rep.losses,
+            "model_vs_measured": calib,
             "clocks": clk.summary()}
     if not args.no_cpu_baseline:
         dt, toks, threads, desc = cpu_sample(args.config)
@@ -336,6 +384,7 @@ def main():
     ap.add_argument("--schedule", default="vertical", choices=["vertical", "horizontal"],
                     help="horizontal = the micro-batch-major ablation baseline (BASELINE configs[1])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--calibrate", type=int, default=1, help="calibrate offsim::simulate from the trace")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

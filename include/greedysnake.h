@@ -154,6 +154,8 @@ int gs_engine_kernel_profile(gs_engine* engine, double flops[5], double ms[5], i
                              int64_t total_launches[5]);
 /* time one launch in `stride` per kernel class during later runs (0 = off) */
 int gs_engine_set_profiling(gs_engine* engine, int stride);
+/* record the per-task trace during later runs */
+int gs_engine_set_trace(gs_engine* engine, int on);
 /* trace of the last run (last <= 3 iterations when record_trace was set) */
 int gs_engine_trace(gs_engine* engine, gs_trace_record* out, int cap, int* n);
 

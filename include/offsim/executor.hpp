@@ -113,6 +113,9 @@ class Executor {
   KernelTotals kernel_profile() const;
   // 0 disables per-kernel timing; n times one launch in n per class.
   void set_profiling(int stride);
+  // Per-task trace for the following runs (timing events are created on
+  // first use).
+  void set_trace(bool on);
 
   const SchedulePlan& plan() const;
   const ExecConfig& config() const;

@@ -404,6 +404,9 @@ class Engine:
     def set_profiling(self, stride: int) -> None:
         check(lib().gs_engine_set_profiling(self._h, int(stride)))
 
+    def set_trace(self, on: bool) -> None:
+        check(lib().gs_engine_set_trace(self._h, int(bool(on))))
+
     def flush(self) -> None:
         check(lib().gs_engine_flush(self._h))
 

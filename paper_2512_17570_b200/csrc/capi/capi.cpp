@@ -267,6 +267,9 @@ int gs_engine_kernel_profile(gs_engine* engine, double flops[5], double ms[5], i
 int gs_engine_set_profiling(gs_engine* engine, int stride) {
   return guarded([&] { engine->ex->set_profiling(stride); });
 }
+int gs_engine_set_trace(gs_engine* engine, int on) {
+  return guarded([&] { engine->ex->set_trace(on != 0); });
+}
 int gs_engine_trace(gs_engine* engine, gs_trace_record* out, int cap, int* n) {
   return guarded([&] {
     *n = static_cast<int>(engine->trace.size());

@@ -1319,6 +1319,24 @@ Executor::KernelTotals Executor::kernel_profile() const {
   return t;
 }
 
+void Executor::set_trace(bool on) {
+  Impl& I = *impl_;
+  cuda_check(cudaDeviceSynchronize(), "sync");
+  if (on && I.ev_start.empty()) {
+    const size_t n = I.plan.tasks.size();
+    I.ev_start.resize(n);
+    for (size_t i = 0; i < n; ++i)
+      for (int k = 0; k < 3; ++k) {
+        I.ev_start[i][static_cast<size_t>(k)] = nullptr;
+        if (!I.is_stream[i]) continue;
+        cudaEventDestroy(I.ev_done[i][static_cast<size_t>(k)]);  // timing-enabled replacements
+        cuda_check(cudaEventCreate(&I.ev_done[i][static_cast<size_t>(k)]), "event");
+        cuda_check(cudaEventCreate(&I.ev_start[i][static_cast<size_t>(k)]), "event");
+      }
+  }
+  I.cfg.record_trace = on;
+}
+
 void Executor::set_profiling(int stride) {
   impl_->prof.stride = stride > 0 ? stride : 1;
   impl_->ws.prof = stride > 0 ? &impl_->prof : nullptr;

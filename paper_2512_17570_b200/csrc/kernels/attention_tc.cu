@@ -322,6 +322,193 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
   }
 }
 
+// ------------------------------------------------------------ forward v2
+// 64-key blocks: 112 KB of shared memory and 256 TMEM columns per CTA, so two
+// CTAs share an SM and one CTA's softmax overlaps the other's MMAs.
+constexpr int kBK2 = 64;
+constexpr int kKV2 = kBK2 * kD * 2;  // 16 KB
+struct FaSmem2 {
+  uint8_t Q[kTile];          // [2 d-chunks][128 rows][128 B]
+  uint8_t K[2][kKV2];        // [2 d-chunks][64 rows][128 B]
+  uint8_t V[2][kKV2];
+  uint8_t P[kBQ * kBK2 * 2]; // [128 rows][128 B] (64 keys)
+  uint64_t q_full, k_full[2], v_full[2], kv_empty[2], s_full[2], p_full, o_done;
+  uint32_t tmem;
+};
+
+__global__ void __launch_bounds__(256, 2)
+    fa_fwd_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
+                      bf16* __restrict__ o, float* __restrict__ lse, int s, int h, int H, float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t raw2[];
+  FaSmem2& sm = *reinterpret_cast<FaSmem2*>(raw2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qb = gridDim.x - 1 - blockIdx.x;
+  const int bh = blockIdx.y, bi = bh / H, j = bh % H;
+  const int row0 = bi * s, q0 = qb * kBQ;
+  const int nblk = (q0 + kBQ) / kBK2;  // causal: keys < q0 + 128
+
+  if (threadIdx.x == 0) {
+    bar_init(&sm.q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&sm.k_full[i], 1);
+      bar_init(&sm.v_full[i], 1);
+      bar_init(&sm.kv_empty[i], 1);
+      bar_init(&sm.s_full[i], 1);
+    }
+    bar_init(&sm.p_full, 128);
+    bar_init(&sm.o_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&sm.tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = sm.tmem;  // S0: 0-63, S1: 64-127, O: 128-255
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_q)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_kv)) : "memory");
+      bar_expect(&sm.q_full, kTile);
+      for (int c = 0; c < 2; ++c) tma2d(sm.Q + c * 16384, &map_q, &sm.q_full, j * kD + 64 * c, row0 + q0);
+      for (int kb = 0; kb < nblk; ++kb) {
+        const int buf = kb & 1;
+        bar_wait(&sm.kv_empty[buf], ((kb >> 1) & 1) ^ 1);
+        bar_expect(&sm.k_full[buf], kKV2);
+        for (int c = 0; c < 2; ++c)
+          tma2d(sm.K[buf] + c * 8192, &map_kv, &sm.k_full[buf], h + j * kD + 64 * c, row0 + kb * kBK2);
+        bar_expect(&sm.v_full[buf], kKV2);
+        for (int c = 0; c < 2; ++c)
+          tma2d(sm.V[buf] + c * 8192, &map_kv, &sm.v_full[buf], 2 * h + j * kD + 64 * c, row0 + kb * kBK2);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t qa = su32(sm.Q), pa = su32(sm.P);
+      bar_wait(&sm.q_full, 0);
+      auto issue_s = [&](int kb) {
+        const int buf = kb & 1;
+        bar_wait(&sm.k_full[buf], (kb >> 1) & 1);
+        fence_after();
+        const uint32_t ka = su32(sm.K[buf]);
+#pragma unroll
+        for (int ks = 0; ks < kD / 16; ++ks)
+          mma(tmem + buf * 64, sdesc(qa + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024),
+              sdesc(ka + (ks >> 2) * 8192 + (ks & 3) * 32, 16, 1024),
+              (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24),
+              ks != 0);
+        commit(&sm.s_full[buf]);
+      };
+      issue_s(0);
+      for (int kb = 0; kb < nblk; ++kb) {
+        const int buf = kb & 1;
+        if (kb + 1 < nblk) issue_s(kb + 1);
+        bar_wait(&sm.p_full, kb & 1);
+        bar_wait(&sm.v_full[buf], (kb >> 1) & 1);
+        fence_after();
+        const uint32_t va = su32(sm.V[buf]);
+#pragma unroll
+        for (int ks = 0; ks < kBK2 / 16; ++ks)
+          mma(tmem + 128, sdesc(pa + ks * 32, 16, 1024), sdesc(va + ks * 2048, 8192, 1024), idesc(true),
+              (kb | ks) != 0);
+        commit(&sm.o_done);
+        commit(&sm.kv_empty[buf]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane;
+    const int qrow = q0 + r;
+    const uint32_t lane_base = ((uint32_t)((warp - 4) * 32)) << 16;
+    float m_run = -INFINITY, l_run = 0.0f;
+    const uint32_t swz = (uint32_t)(r & 7);
+    uint8_t* prow = sm.P + (r >> 3) * 1024 + (r & 7) * 128;
+    for (int kb = 0; kb < nblk; ++kb) {
+      const int buf = kb & 1;
+      bar_wait(&sm.s_full[buf], (kb >> 1) & 1);
+      fence_after();
+      float sv[kBK2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t rr[32];
+        tld32(tmem + lane_base + buf * 64 + c * 32, rr);
+        tld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(rr[i]) * scale_log2;
+      }
+      const bool mask = (kb + 1) * kBK2 > q0;  // blocks crossing the diagonal
+      float mx = m_run;
+#pragma unroll
+      for (int i = 0; i < kBK2; ++i) {
+        if (mask && kb * kBK2 + i > qrow) sv[i] = -INFINITY;
+        mx = fmaxf(mx, sv[i]);
+      }
+      const float corr = exp2f(m_run - mx);
+      float rs = 0.0f;
+#pragma unroll
+      for (int i = 0; i < kBK2; ++i) {
+        sv[i] = exp2f(sv[i] - mx);
+        rs += sv[i];
+      }
+      l_run = l_run * corr + rs;
+      m_run = mx;
+      if (kb > 0) {  // PV(kb-1) done: P free, O final for the rescale
+        bar_wait(&sm.o_done, (kb - 1) & 1);
+        fence_after();
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const float* v = sv + p * 8;
+        *reinterpret_cast<uint4*>(prow + ((p ^ swz) << 4)) =
+            make_uint4(pack(v[0], v[1]), pack(v[2], v[3]), pack(v[4], v[5]), pack(v[6], v[7]));
+      }
+      if (kb > 0 && __any_sync(0xffffffffu, corr != 1.0f)) {
+#pragma unroll
+        for (int c = 0; c < kD / 32; ++c) {
+          uint32_t rr[32];
+          tld32(tmem + lane_base + 128 + c * 32, rr);
+          tld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * corr);
+          tst32(tmem + lane_base + 128 + c * 32, rr);
+        }
+        tst_wait();
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      fence_before();
+      bar_arrive(&sm.p_full);
+    }
+    bar_wait(&sm.o_done, (nblk - 1) & 1);
+    fence_after();
+    const float inv = 1.0f / l_run;
+    bf16* orow = o + (long long)(row0 + qrow) * h + j * kD;
+#pragma unroll
+    for (int c = 0; c < kD / 32; ++c) {
+      uint32_t rr[32];
+      tld32(tmem + lane_base + 128 + c * 32, rr);
+      tld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack(__uint_as_float(rr[8 * q]) * inv, __uint_as_float(rr[8 * q + 1]) * inv);
+        w.y = pack(__uint_as_float(rr[8 * q + 2]) * inv, __uint_as_float(rr[8 * q + 3]) * inv);
+        w.z = pack(__uint_as_float(rr[8 * q + 4]) * inv, __uint_as_float(rr[8 * q + 5]) * inv);
+        w.w = pack(__uint_as_float(rr[8 * q + 6]) * inv, __uint_as_float(rr[8 * q + 7]) * inv);
+        *reinterpret_cast<uint4*>(orow + c * 32 + 8 * q) = w;
+      }
+    }
+    lse[(long long)bh * s + qrow] = (m_run + log2f(l_run)) * 0.6931471805599453f;
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
 // ============================================================== backward
 // One CTA per (128-key block, batch x head); loop over 64-query blocks from
 // the diagonal down.  Per block (TMEM columns in brackets):
@@ -581,7 +768,39 @@ bool attention_tc_supported(DType dt, int s, int h, int H) {
   return !off && dt == DType::BF16 && h / H == kD && h % H == 0 && s % kBQ == 0 && encoder() != nullptr;
 }
 
+static int fwd_variant() {  // GS_ATTN_FWD=1: 128-key single-CTA kernel; default 2: 64-key, 2 CTAs/SM
+  static int v = [] {
+    const char* e = getenv("GS_ATTN_FWD");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
+
 cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s, int h, int H, cudaStream_t st) {
+  if (fwd_variant() == 2) {
+    CUtensorMap mq, mkv;
+    const cuuint64_t dims[2] = {(cuuint64_t)3 * h, (cuuint64_t)b * s};
+    const cuuint64_t strides[1] = {(cuuint64_t)3 * h * 2};
+    const cuuint32_t elem[2] = {1, 1};
+    for (int rows : {128, 64}) {
+      const cuuint32_t box[2] = {64, (cuuint32_t)rows};
+      if (encoder()(rows == 128 ? &mq : &mkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims,
+                    strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
+    const int smem = (int)sizeof(FaSmem2);
+    static bool init2 = false;
+    if (!init2) {
+      cudaError_t e = cudaFuncSetAttribute(fa_fwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      init2 = true;
+    }
+    count_launch();
+    fa_fwd_tc2_kernel<<<dim3(s / kBQ, b * H), 256, smem, st>>>(mq, mkv, (bf16*)o, lse, s, h, H,
+                                                               1.4426950408889634f / sqrtf((float)kD));
+    return cudaGetLastError();
+  }
   CUtensorMap map;
   const cuuint64_t dims[2] = {(cuuint64_t)3 * h, (cuuint64_t)b * s};
   const cuuint64_t strides[1] = {(cuuint64_t)3 * h * 2};
