@@ -321,7 +321,7 @@ int gs_layernorm_fwd(int dtype, const void* x, void* y, float* mean, float* rstd
 }
 int gs_layernorm_bwd(int dtype, const void* x, const float* mean, const float* rstd, const void* dy, void* dx,
                      int rows, int h, int accumulate, void* stream) {
-  return cuda_status(gs::layernorm_bwd(dt_of(dtype), x, mean, rstd, dy, dx, rows, h, accumulate != 0,
+  return cuda_status(gs::layernorm_bwd(dt_of(dtype), x, mean, rstd, dy, accumulate ? dx : nullptr, dx, rows, h,
                                        static_cast<cudaStream_t>(stream)));
 }
 int gs_adam_step_packed(float lr, float beta1, float beta2, float eps, float wd, int step, float grad_scale,

@@ -196,7 +196,7 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
     GS_TRY(mm(d, d.V, h, T, ws.dlogits, false, ws.z, false, head->dwte, Epi::AccumF32, st, lc, nullptr, nullptr, ws.prof));
     // dz = dlogits . wte   (M=T, N=h, K=V)
     GS_TRY(mm(d, T, h, d.V, ws.dlogits, true, head->wte, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));
-    GS_PROF(Norm, layernorm_bwd(d.dt, ws.y, ws.mz, ws.rz, ws.tmp, ws.dy, T, h, false, st));
+    GS_PROF(Norm, layernorm_bwd(d.dt, ws.y, ws.mz, ws.rz, ws.tmp, nullptr, ws.dy, T, h, st));
     dy = ws.dy;
     lc.n += 3;
   }
@@ -210,8 +210,7 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
   GS_TRY(mm(d, T, 4 * h, h, dy, true, w2, false, ws.big, Epi::MulGeluGrad, st, lc, ws.u, nullptr, ws.prof));
   GS_TRY(mm(d, 4 * h, h, T, ws.big, false, ws.c, false, dW1, wg, st, lc, nullptr, nullptr, ws.prof));       // dW1 (+)= du^T c
   GS_TRY(mm(d, T, h, 4 * h, ws.big, true, w1, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));  // dc = du W1
-  GS_PROF(Other, cudaMemcpyAsync(ws.dx1, dy, 1LL * T * h * eb, cudaMemcpyDeviceToDevice, st));
-  GS_PROF(Norm, layernorm_bwd(d.dt, ws.x1, ws.m2, ws.r2, ws.tmp, ws.dx1, T, h, true, st));  // dx1 = dy + LN2'
+  GS_PROF(Norm, layernorm_bwd(d.dt, ws.x1, ws.m2, ws.r2, ws.tmp, dy, ws.dx1, T, h, st));  // dx1 = dy + LN2'
   // attention
   GS_TRY(mm(d, h, h, T, ws.dx1, false, ws.o, false, dWo, wg, st, lc, nullptr, nullptr, ws.prof));           // dWo (+)= dx1^T o
   GS_TRY(mm(d, T, h, h, ws.dx1, true, wo, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));    // do = dx1 Wo
@@ -221,8 +220,7 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
   }
   GS_TRY(mm(d, 3 * h, h, T, ws.dqkv, false, ws.a, false, dWqkv, wg, st, lc, nullptr, nullptr, ws.prof));    // dWqkv (+)= dqkv^T a
   GS_TRY(mm(d, T, h, 3 * h, ws.dqkv, true, wqkv, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));  // da = dqkv Wqkv
-  GS_PROF(Other, cudaMemcpyAsync(dx, ws.dx1, 1LL * T * h * eb, cudaMemcpyDeviceToDevice, st));
-  GS_PROF(Norm, layernorm_bwd(d.dt, x, ws.m1, ws.r1, ws.tmp, dx, T, h, true, st));      // dx = dx1 + LN1'
+  GS_PROF(Norm, layernorm_bwd(d.dt, x, ws.m1, ws.r1, ws.tmp, ws.dx1, dx, T, h, st));  // dx = dx1 + LN1'
   lc.n += 6;
   return cudaSuccess;
 }

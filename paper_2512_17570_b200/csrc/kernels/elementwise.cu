@@ -5,6 +5,7 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <algorithm>
 #include <cmath>
 
 namespace gs {
@@ -107,6 +108,180 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(const T* __restrict
     }
   }
 }
+
+// Vectorised row kernels (h % (16 / sizeof(T)) == 0, the engine's case): a
+// row is owned by a group of nw warps (nw = 1 for h <= 2048 bf16, so the
+// reductions are warp shuffles only), each lane holds C 16-byte vectors of the
+// row as packed storage-type registers, and blocks carry 8 / nw rows.
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+  static constexpr int N = 4;
+  __device__ __forceinline__ static void unpack(const uint4& r, float* f) {
+    f[0] = __uint_as_float(r.x); f[1] = __uint_as_float(r.y);
+    f[2] = __uint_as_float(r.z); f[3] = __uint_as_float(r.w);
+  }
+  __device__ __forceinline__ static uint4 pack(const float* f) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+  }
+};
+template <> struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ __forceinline__ static float lo(uint32_t w) { return __uint_as_float(w << 16); }
+  __device__ __forceinline__ static float hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+  __device__ __forceinline__ static void unpack(const uint4& r, float* f) {
+    f[0] = lo(r.x); f[1] = hi(r.x); f[2] = lo(r.y); f[3] = hi(r.y);
+    f[4] = lo(r.z); f[5] = hi(r.z); f[6] = lo(r.w); f[7] = hi(r.w);
+  }
+  __device__ __forceinline__ static uint32_t p2(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+  }
+  __device__ __forceinline__ static uint4 pack(const float* f) {
+    return make_uint4(p2(f[0], f[1]), p2(f[2], f[3]), p2(f[4], f[5]), p2(f[6], f[7]));
+  }
+};
+
+// Sum over the nw warps of this thread's row group (uniform nw per launch).
+__device__ __forceinline__ float group_sum(float v, float* red, int nw) {
+  v = warp_sum(v);
+  if (nw == 1) return v;
+  const int w = threadIdx.x >> 5, base = (w / nw) * nw;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  float r = 0.0f;
+  for (int i = 0; i < nw; ++i) r += red[base + i];
+  return r;
+}
+
+template <typename T, int C>
+__global__ void __launch_bounds__(256) ln_fwd_vec_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                         float* __restrict__ mean, float* __restrict__ rstd,
+                                                         int rows, int h, int nw) {
+  using VT = Vec<T>;
+  constexpr int N = VT::N;
+  __shared__ float red[8];
+  const int gt = 32 * nw, t = threadIdx.x % gt;
+  const long long row = (long long)blockIdx.x * (blockDim.x / gt) + threadIdx.x / gt;
+  const bool live = row < rows;
+  const int nv = h / N;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * h);
+  uint4 raw[C];
+  float s = 0.0f;
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    const int v = t + k * gt;
+    raw[k] = (live && v < nv) ? __ldg(xr + v) : make_uint4(0, 0, 0, 0);
+    float f[N];
+    VT::unpack(raw[k], f);
+#pragma unroll
+    for (int e = 0; e < N; ++e) s += f[e];
+  }
+  const float mu = group_sum(s, red, nw) / h;
+  float ss = 0.0f;
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    if (t + k * gt < nv) {
+      float f[N];
+      VT::unpack(raw[k], f);
+#pragma unroll
+      for (int e = 0; e < N; ++e) ss += (f[e] - mu) * (f[e] - mu);
+    }
+  }
+  const float rs = rsqrtf(group_sum(ss, red, nw) / h + kLnEps);
+  if (!live) return;
+  uint4* yr = reinterpret_cast<uint4*>(y + row * h);
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    const int v = t + k * gt;
+    if (v < nv) {
+      float f[N];
+      VT::unpack(raw[k], f);
+#pragma unroll
+      for (int e = 0; e < N; ++e) f[e] = (f[e] - mu) * rs;
+      yr[v] = VT::pack(f);
+    }
+  }
+  if (t == 0) {
+    if (mean) mean[row] = mu;
+    if (rstd) rstd[row] = rs;
+  }
+}
+
+// dx = res + rs * (g - mean(g) - xh * mean(g * xh)); res may alias dx or be null.
+template <typename T, int C>
+__global__ void __launch_bounds__(256) ln_bwd_vec_kernel(const T* __restrict__ x, const float* __restrict__ mean,
+                                                         const float* __restrict__ rstd, const T* __restrict__ dy,
+                                                         const T* res, T* dx, int rows, int h, int nw) {
+  using VT = Vec<T>;
+  constexpr int N = VT::N;
+  __shared__ float red[8];
+  const int gt = 32 * nw, t = threadIdx.x % gt;
+  const long long row = (long long)blockIdx.x * (blockDim.x / gt) + threadIdx.x / gt;
+  const bool live = row < rows;
+  const int nv = h / N;
+  const float mu = live ? mean[row] : 0.0f, rs = live ? rstd[row] : 0.0f;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * h);
+  const uint4* gr = reinterpret_cast<const uint4*>(dy + row * h);
+  uint4 rx[C], rg[C];
+  float sg = 0.0f, sgx = 0.0f;
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    const int v = t + k * gt;
+    const bool ok = live && v < nv;
+    rx[k] = ok ? __ldg(xr + v) : make_uint4(0, 0, 0, 0);
+    rg[k] = ok ? __ldg(gr + v) : make_uint4(0, 0, 0, 0);
+    float fx[N], fg[N];
+    VT::unpack(rx[k], fx);
+    VT::unpack(rg[k], fg);
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+      sg += fg[e];
+      sgx += fg[e] * ((fx[e] - mu) * rs);
+    }
+  }
+  const float mg = group_sum(sg, red, nw) / h;
+  const float mgx = group_sum(sgx, red, nw) / h;
+  if (!live) return;
+  uint4* dr = reinterpret_cast<uint4*>(dx + row * h);
+  const uint4* rr = reinterpret_cast<const uint4*>(res + row * h);
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    const int v = t + k * gt;
+    if (v < nv) {
+      float fx[N], fg[N], fr[N];
+      VT::unpack(rx[k], fx);
+      VT::unpack(rg[k], fg);
+      if (res) VT::unpack(rr[v], fr);
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        const float d = rs * (fg[e] - mg - ((fx[e] - mu) * rs) * mgx);
+        fx[e] = res ? fr[e] + d : d;
+      }
+      dr[v] = VT::pack(fx);
+    }
+  }
+}
+
+struct RowShape {
+  int nw, rpb, c;  // warps per row (<= 8), rows per block, 16-byte vectors per lane (<= 16)
+};
+inline RowShape row_shape(int h, int n) {
+  const int nv = h / n;
+  RowShape r;
+  r.nw = std::min(8, (nv + 255) / 256);
+  r.rpb = 8 / r.nw;
+  r.c = (nv + 32 * r.nw - 1) / (32 * r.nw);
+  return r;
+}
+#define GS_ROW_C(c, ...)                                       \
+  do {                                                         \
+    if ((c) <= 1) { constexpr int C = 1; __VA_ARGS__; }        \
+    else if ((c) <= 2) { constexpr int C = 2; __VA_ARGS__; }   \
+    else if ((c) <= 4) { constexpr int C = 4; __VA_ARGS__; }   \
+    else if ((c) <= 8) { constexpr int C = 8; __VA_ARGS__; }   \
+    else { constexpr int C = 16; __VA_ARGS__; }                \
+  } while (0)
 
 // E in {1,2,4,8,16,24,32,48}: smallest covering h
 #define GS_ROW_E(h, ...)                                  \
@@ -278,17 +453,37 @@ cudaError_t layernorm_fwd(DType dt, const void* x, void* y, float* mean, float* 
                           cudaStream_t s) {
   if (h > kRowThreads * kMaxPerThread) return cudaErrorInvalidValue;
   if (rows == 0) return cudaSuccess;
-  GS_DISPATCH(dt, GS_ROW_E(h, ln_fwd_kernel<T, E><<<rows, kRowThreads, 0, s>>>((const T*)x, (T*)y, mean, rstd, h)));
+  GS_DISPATCH(dt, {
+    if (h % Vec<T>::N == 0) {
+      const RowShape r = row_shape(h, Vec<T>::N);
+      GS_ROW_C(r.c, ln_fwd_vec_kernel<T, C><<<(rows + r.rpb - 1) / r.rpb, 32 * r.nw * r.rpb, 0, s>>>(
+                        (const T*)x, (T*)y, mean, rstd, rows, h, r.nw));
+    } else {
+      GS_ROW_E(h, ln_fwd_kernel<T, E><<<rows, kRowThreads, 0, s>>>((const T*)x, (T*)y, mean, rstd, h));
+    }
+  });
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t layernorm_bwd(DType dt, const void* x, const float* mean, const float* rstd, const void* dy,
-                          void* dx, int rows, int h, bool accumulate, cudaStream_t s) {
+                          const void* res, void* dx, int rows, int h, cudaStream_t s) {
   if (h > kRowThreads * kMaxPerThread) return cudaErrorInvalidValue;
   if (rows == 0) return cudaSuccess;
-  GS_DISPATCH(dt, GS_ROW_E(h, ln_bwd_kernel<T, E><<<rows, kRowThreads, 0, s>>>((const T*)x, mean, rstd,
-                                                                            (const T*)dy, (T*)dx, h, accumulate)));
+  GS_DISPATCH(dt, {
+    if (h % Vec<T>::N == 0) {
+      const RowShape r = row_shape(h, Vec<T>::N);
+      GS_ROW_C(r.c, ln_bwd_vec_kernel<T, C><<<(rows + r.rpb - 1) / r.rpb, 32 * r.nw * r.rpb, 0, s>>>(
+                        (const T*)x, mean, rstd, (const T*)dy, (const T*)res, (T*)dx, rows, h, r.nw));
+    } else {
+      if (res && res != dx) {
+        cudaError_t e = cudaMemcpyAsync(dx, res, (size_t)rows * h * sizeof(T), cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return e;
+      }
+      GS_ROW_E(h, ln_bwd_kernel<T, E><<<rows, kRowThreads, 0, s>>>((const T*)x, mean, rstd, (const T*)dy, (T*)dx,
+                                                                   h, res != nullptr));
+    }
+  });
   count_launch();
   return cudaGetLastError();
 }

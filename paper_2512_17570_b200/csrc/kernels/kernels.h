@@ -61,9 +61,9 @@ cudaError_t attention_bwd(DType dt, const void* qkv, const void* o, const float*
 // non-affine LayerNorm over rows of width h, eps = 1e-5
 cudaError_t layernorm_fwd(DType dt, const void* x, void* y, float* mean, float* rstd, int rows, int h,
                           cudaStream_t s);
-// dx = (accumulate ? dx : 0) + LN_backward(dy); dx may alias nothing else
+// dx = (res ? res : 0) + LN_backward(dy); res may alias dx (res = dx accumulates)
 cudaError_t layernorm_bwd(DType dt, const void* x, const float* mean, const float* rstd, const void* dy,
-                          void* dx, int rows, int h, bool accumulate, cudaStream_t s);
+                          const void* res, void* dx, int rows, int h, cudaStream_t s);
 
 // ---------------------------------------------------------- elementwise
 cudaError_t gelu_fwd(DType dt, const void* u, void* g, long long n, cudaStream_t s);

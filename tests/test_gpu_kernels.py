@@ -145,11 +145,12 @@ def test_attention_fwd_bwd(dtype, b, s, h, H):
         assert rel(dqkv[:, sl].float(), g[:, sl]) < (2e-2 if dtype == BF16 else 1e-5), part
 
 
-@pytest.mark.parametrize("dtype,h", [(F32, 64), (F32, 2048), (BF16, 2048), (F32, 12288)])
+@pytest.mark.parametrize("dtype,h", [(F32, 64), (F32, 2048), (BF16, 2048), (F32, 12288), (BF16, 5120),
+                                     (BF16, 12288), (BF16, 8), (F32, 100), (BF16, 1000), (BF16, 36)])
 def test_layernorm(dtype, h):
     d = dev()
     tdt = torch.bfloat16 if dtype == BF16 else torch.float32
-    rows = 64
+    rows = 61  # not a multiple of the rows per block
     x = (torch.randn(rows, h, device=d) * 2 + 0.5).to(tdt)
     y = torch.empty_like(x)
     mean = torch.empty(rows, device=d)
@@ -167,6 +168,12 @@ def test_layernorm(dtype, h):
     gs.check(lib.gs_layernorm_bwd(dtype, ptr(x), ptr(mean), ptr(rstd), ptr(dy), ptr(dx), rows, h, 0, None))
     torch.cuda.synchronize()
     assert rel(dx.float(), xr.grad) < tol
+    # accumulate: dx = res + LN'(dy)
+    res = torch.randn_like(x)
+    acc = res.clone()
+    gs.check(lib.gs_layernorm_bwd(dtype, ptr(x), ptr(mean), ptr(rstd), ptr(dy), ptr(acc), rows, h, 1, None))
+    torch.cuda.synchronize()
+    assert rel(acc.float(), res.float() + xr.grad) < tol
 
 
 @pytest.mark.parametrize("n", [1, 7, 1024, 1 << 20])

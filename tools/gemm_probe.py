@@ -57,6 +57,17 @@ dqkv = torch.empty_like(qkv)
 work = torch.empty(lib.gs_attention_bwd_workspace(b, s, h, H), dtype=torch.uint8, device=d)
 ms = timed(lambda: gs.check(lib.gs_attention_bwd(1, p(qkv), p(o), p(lse), p(dout), p(dqkv), p(work), b, s, h, H, None)))
 rows.append(dict(kernel="attn_bwd", ms=ms, tflops=2.5 * fl / ms / 1e9))
+# LayerNorm fwd / bwd(+residual): the step's shape (L2-resident) and 16x rows (HBM)
+for rows_ln in (T, 16 * T):
+    x = torch.randn(rows_ln, h, device=d).bfloat16()
+    y = torch.empty_like(x)
+    mean = torch.empty(rows_ln, device=d)
+    rstd = torch.empty(rows_ln, device=d)
+    ms = timed(lambda: gs.check(lib.gs_layernorm_fwd(1, p(x), p(y), p(mean), p(rstd), rows_ln, h, None)))
+    rows.append(dict(kernel="ln_fwd", rows=rows_ln, ms=ms, gbs=2 * x.numel() * 2 / ms / 1e6))
+    ms = timed(lambda: gs.check(lib.gs_layernorm_bwd(1, p(x), p(mean), p(rstd), p(y), p(y), rows_ln, h, 1, None)))
+    rows.append(dict(kernel="ln_bwd_acc", rows=rows_ln, ms=ms, gbs=4 * x.numel() * 2 / ms / 1e6))
+    del x, y
 # torch reference matmul for context
 A = torch.randn(8192, 8192, device=d).bfloat16()
 B = torch.randn(8192, 8192, device=d).bfloat16()
