@@ -342,8 +342,10 @@ __global__ void __launch_bounds__(256, 2)
   extern __shared__ __align__(1024) uint8_t raw2[];
   FaSmem2& sm = *reinterpret_cast<FaSmem2*>(raw2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qb = gridDim.x - 1 - blockIdx.x;
-  const int bh = blockIdx.y, bi = bh / H, j = bh % H;
+  // grid (b*H, s/128): every head's heaviest query tile is launched before
+  // any lighter one (longest-processing-time-first over the whole grid)
+  const int qb = gridDim.y - 1 - blockIdx.y;
+  const int bh = blockIdx.x, bi = bh / H, j = bh % H;
   const int row0 = bi * s, q0 = qb * kBQ;
   const int nblk = (q0 + kBQ) / kBK2;  // causal: keys < q0 + 128
 
@@ -445,15 +447,22 @@ __global__ void __launch_bounds__(256, 2)
         if (mask && kb * kBK2 + i > qrow) sv[i] = -INFINITY;
         mx = fmaxf(mx, sv[i]);
       }
-      const float corr = exp2f(m_run - mx);
+      // Lazy rescaling: the running max only moves when the block max exceeds
+      // it by more than 2^8 (P <= 256 stays exact in bf16 / fp32); O and l
+      // are then consistent with the stale max and the final O / l, lse are
+      // unchanged.  With a moving max every block would pay a full TMEM
+      // read + write of O.
+      const bool bump = mx > m_run + 8.0f;
+      const float m_new = bump ? mx : m_run;
+      const float corr = bump ? exp2f(m_run - mx) : 1.0f;
       float rs = 0.0f;
 #pragma unroll
       for (int i = 0; i < kBK2; ++i) {
-        sv[i] = exp2f(sv[i] - mx);
+        sv[i] = exp2f(sv[i] - m_new);
         rs += sv[i];
       }
       l_run = l_run * corr + rs;
-      m_run = mx;
+      m_run = m_new;
       if (kb > 0) {  // PV(kb-1) done: P free, O final for the rescale
         bar_wait(&sm.o_done, (kb - 1) & 1);
         fence_after();
@@ -464,7 +473,7 @@ __global__ void __launch_bounds__(256, 2)
         *reinterpret_cast<uint4*>(prow + ((p ^ swz) << 4)) =
             make_uint4(pack(v[0], v[1]), pack(v[2], v[3]), pack(v[4], v[5]), pack(v[6], v[7]));
       }
-      if (kb > 0 && __any_sync(0xffffffffu, corr != 1.0f)) {
+      if (kb > 0 && __any_sync(0xffffffffu, bump)) {
 #pragma unroll
         for (int c = 0; c < kD / 32; ++c) {
           uint32_t rr[32];
@@ -771,8 +780,10 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
   extern __shared__ __align__(1024) uint8_t rawb[];
   FaBwdSmem2& sm = *reinterpret_cast<FaBwdSmem2*>(rawb);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = gridDim.x - 1 - blockIdx.x;  // long key blocks (few queries) last
-  const int bh = blockIdx.y, bi = bh / H, j = bh % H;
+  // grid (b*H, s/128): key block 0 (the most query blocks) of every head is
+  // launched first, the short diagonal-only blocks last (LPT order)
+  const int kb = blockIdx.y;
+  const int bh = blockIdx.x, bi = bh / H, j = bh % H;
   const int row0 = bi * s;
   const int k0 = kb * kBK;
   const int qb0 = k0 / kBQb, nq = s / kBQb - qb0;
@@ -929,20 +940,19 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
       const int buf = i & 1;
       bar_wait(&sm.dq_full[buf], (i >> 1) & 1);
       fence_after();
+      // TMEM -> registers first and release the buffer at once (the MMA warp
+      // waits on it before S/dP(i+2)); only then wait for the previous TMA
+      // reduce to finish reading the staging tile.
+      uint32_t rr[kBQb];
+      tld32(tmem + lb + buf * 128, *reinterpret_cast<uint32_t(*)[32]>(rr));
+      tld32(tmem + lb + buf * 128 + 32, *reinterpret_cast<uint32_t(*)[32]>(rr + 32));
+      tld_wait();
+      fence_before();
+      bar_arrive(&sm.dq_empty[buf]);
       if (r == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
       asm volatile("bar.sync 3, 128;" ::: "memory");
 #pragma unroll
-      for (int c = 0; c < kBQb / 32; ++c) {
-        uint32_t rr[32];
-        tld32(tmem + lb + buf * 128 + c * 32, rr);
-        tld_wait();
-        if (c == kBQb / 32 - 1) {  // TMEM buffer free for S/dP(i+2)
-          fence_before();
-          bar_arrive(&sm.dq_empty[buf]);
-        }
-#pragma unroll
-        for (int q = 0; q < 32; ++q) sm.dq_stage[c * 32 + q][r] = __uint_as_float(rr[q]) * scale;
-      }
+      for (int q = 0; q < kBQb; ++q) sm.dq_stage[q][r] = __uint_as_float(rr[q]) * scale;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("bar.sync 3, 128;" ::: "memory");
       if (r == 0) {
@@ -1037,7 +1047,7 @@ cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s,
       init2 = true;
     }
     count_launch();
-    fa_fwd_tc2_kernel<<<dim3(s / kBQ, b * H), 256, smem, st>>>(mq, mkv, (bf16*)o, lse, s, h, H,
+    fa_fwd_tc2_kernel<<<dim3(b * H, s / kBQ), 256, smem, st>>>(mq, mkv, (bf16*)o, lse, s, h, H,
                                                                1.4426950408889634f / sqrtf((float)kD));
     return cudaGetLastError();
   }
@@ -1110,7 +1120,7 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
       init2 = true;
     }
     count_launch();
-    fa_bwd_tc2_kernel<<<dim3(s / kBK, b * H), kThreadsBwd2, smem2, st>>>(mq, mq64, md, mdq, lse, D, (bf16*)dqkv, s,
+    fa_bwd_tc2_kernel<<<dim3(b * H, s / kBK), kThreadsBwd2, smem2, st>>>(mq, mq64, md, mdq, lse, D, (bf16*)dqkv, s,
                                                                           h, H, 1.0f / sqrtf((float)kD));
     return cudaGetLastError();
   }

@@ -115,13 +115,23 @@ def attn_reference(qkv, b, s, h, H):
     return o.transpose(1, 2).reshape(b * s, h), lse
 
 
-@pytest.mark.parametrize("dtype,b,s,h,H", [(BF16, 2, 256, 512, 4), (BF16, 1, 512, 512, 8), (BF16, 2, 2048, 2048, 16),
-                                           (F32, 2, 32, 64, 4), (BF16, 2, 32, 64, 4)])
-def test_attention_fwd_bwd(dtype, b, s, h, H):
+@pytest.mark.parametrize("dtype,b,s,h,H,amp", [(BF16, 2, 256, 512, 4, 0.5), (BF16, 1, 512, 512, 8, 0.5),
+                                               (BF16, 2, 2048, 2048, 16, 0.5), (F32, 2, 32, 64, 4, 0.5),
+                                               (BF16, 2, 32, 64, 4, 0.5),
+                                               # large scores: the running max jumps by >2^8 (lazy O rescale path)
+                                               (BF16, 1, 1024, 512, 4, 2.5), (BF16, 2, 512, 256, 2, "ramp")])
+def test_attention_fwd_bwd(dtype, b, s, h, H, amp):
     d = dev()
     tdt = torch.bfloat16 if dtype == BF16 else torch.float32
     torch.manual_seed(0)
-    qkv = (torch.randn(b * s, 3 * h, device=d) * 0.5).to(tdt)
+    if amp == "ramp":
+        # scores grow with the key position: the row max moves in every key block
+        qkv = torch.randn(b * s, 3 * h, device=d) * 0.3
+        qkv[:, :h] = qkv[:, :h].abs() + 1.0
+        qkv[:, h:2 * h] = qkv[:, h:2 * h].abs() * (torch.arange(b * s, device=d) % s).float()[:, None] / 64.0
+        qkv = qkv.to(tdt)
+    else:
+        qkv = (torch.randn(b * s, 3 * h, device=d) * amp).to(tdt)
     o = torch.empty(b * s, h, device=d, dtype=tdt)
     lse = torch.empty(b * H * s, device=d)
     lib = gs.lib()
