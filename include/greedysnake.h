@@ -110,6 +110,7 @@ typedef struct gs_engine_config {
   int rank, world;         /* ZeRO-3 data parallelism: model.data_parallel_degree == world */
   const uint8_t* nccl_id;  /* 128-byte ncclUniqueId from gs_nccl_unique_id() on rank 0 (world > 1) */
   int force_collectives;   /* run the sharded / NCCL path even at world == 1 */
+  int ssd_ring_layers;     /* pinned staging slots per SSD-resident data kind (0 -> 8) */
 } gs_engine_config;
 
 /* ncclGetUniqueId() for rank 0 of a data-parallel job */
@@ -184,6 +185,10 @@ int gs_adam_step_packed(float lr, float beta1, float beta2, float eps, float wei
 int gs_layer_forward(int dtype, int b, int s, int h, int heads, const void* W, const void* x, void* y, void* stream);
 int gs_layer_backward(int dtype, int b, int s, int h, int heads, const void* W, const void* x, const void* dy,
                       void* dx, float* dW, int first, void* stream);
+/* diagnostics: `iters` back-to-back layer forwards, then recompute+backwards,
+ * on one stream with preallocated buffers; out = {fwd GPU ms, fwd host enqueue
+ * ms, bwd GPU ms, bwd host enqueue ms} per call */
+int gs_layer_bench(int dtype, int b, int s, int h, int heads, int iters, double out[4]);
 /* number of device kernels launched through this library so far */
 int64_t gs_launch_count(void);
 

@@ -57,6 +57,10 @@ struct ExecConfig {
   int rank = 0, world = 1;
   std::vector<uint8_t> nccl_id;
   bool force_collectives = false;  // run the sharded code path even at world == 1 (tests)
+  // SSD-resident bytes have no permanent DRAM copy: each data kind stages
+  // them through a ring of this many per-layer pinned slots (slot = layer %
+  // ring); reuse of a slot is ordered by the executor's hazard edges.
+  int ssd_ring_layers = 8;
 };
 
 struct TraceRecord {

@@ -87,7 +87,7 @@ class _EngineConfig(C.Structure):
                 ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float), ("seed", C.c_uint64),
                 ("device", C.c_int), ("nvme_dir", C.c_char_p), ("odirect", C.c_int), ("opt_tier", C.c_int),
                 ("record_trace", C.c_int), ("profile_kernels", C.c_int), ("rank", C.c_int), ("world", C.c_int),
-                ("nccl_id", C.c_void_p), ("force_collectives", C.c_int)]
+                ("nccl_id", C.c_void_p), ("force_collectives", C.c_int), ("ssd_ring_layers", C.c_int)]
 
 
 class _RunReport(C.Structure):
@@ -345,7 +345,7 @@ class Engine:
     def __init__(self, plan: SchedulePlan, model: ModelSpec, vocab_size: int, adam: AdamConfig = AdamConfig(),
                  seed: int = 42, device: int = 0, nvme_dir: str = "/tmp", odirect: bool = True, opt_tier: int = 0,
                  record_trace: bool = False, profile: bool = False, rank: int = 0, world: int = 1,
-                 nccl_id: bytes | None = None, force_collectives: bool = False):
+                 nccl_id: bytes | None = None, force_collectives: bool = False, ssd_ring_layers: int = 0):
         self.model = model
         self.vocab_size = vocab_size
         self.plan = plan
@@ -355,7 +355,7 @@ class Engine:
         cfg = _EngineConfig(model._c(), vocab_size, adam.lr, adam.beta1, adam.beta2, adam.eps, adam.weight_decay,
                             seed, device, self._nvme, int(odirect), opt_tier, int(record_trace), int(profile),
                             rank, world, C.cast(self._id, C.c_void_p) if self._id is not None else None,
-                            int(force_collectives))
+                            int(force_collectives), int(ssd_ring_layers))
         h = C.c_void_p()
         check(lib().gs_engine_create(plan.handle, C.byref(cfg), C.byref(h)))
         self._h = h

@@ -5,11 +5,13 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cstring>
 #include <exception>
 #include <memory>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "greedysnake.h"
 #include "kernels.h"
@@ -218,6 +220,7 @@ int gs_engine_create(const gs_plan* plan, const gs_engine_config* c, gs_engine**
     cfg.world = c->world > 0 ? c->world : 1;
     if (c->nccl_id) cfg.nccl_id.assign(c->nccl_id, c->nccl_id + 128);
     cfg.force_collectives = c->force_collectives != 0;
+    if (c->ssd_ring_layers > 0) cfg.ssd_ring_layers = c->ssd_ring_layers;
     auto e = std::make_unique<gs_engine>();
     e->ex = std::make_unique<offsim::Executor>(plan->plan, cfg);
     *out = e.release();
@@ -357,6 +360,80 @@ int gs_layer_backward(int dtype, int b, int s, int h, int heads, const void* W, 
   return layer_call(dtype, b, s, h, heads, false, W, x, dy, dx, dW, first, stream);
 }
 int64_t gs_launch_count(void) { return gs::launch_counter_ref(); }
+
+int gs_layer_bench(int dtype, int b, int s, int h, int heads, int iters, double out[4]) {
+  return guarded([&] {
+    if (iters < 1 || !out) throw offsim::ValidationError("layer_bench: iters >= 1 and out required");
+    gs::engine::Dims d;
+    d.b = b;
+    d.s = s;
+    d.h = h;
+    d.H = heads;
+    d.V = 128;
+    d.dt = dt_of(dtype);
+    gs::engine::Workspace ws;
+    if (!gs::engine::alloc_workspace(d, ws)) throw offsim::InfeasibleError("layer_bench: workspace");
+    const size_t eb = static_cast<size_t>(d.lp()), T = static_cast<size_t>(d.T());
+    void *W = nullptr, *x = nullptr, *y = nullptr, *dy = nullptr, *dx = nullptr;
+    float* dW = nullptr;
+    auto ok = [](cudaError_t e) {
+      if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    };
+    ok(cudaMalloc(&W, 12ull * h * h * eb));
+    ok(cudaMalloc(&dW, 12ull * h * h * 4));
+    for (void** p : {&x, &y, &dy, &dx}) ok(cudaMalloc(p, T * h * eb));
+    // realistic operands (all-zero GEMMs draw less power and clock higher):
+    // W ~ U(-0.02, 0.02), activations / gradients ~ U(-1, 1)
+    auto fill = [&](void* p, size_t n, float amp) {
+      std::vector<uint8_t> hbuf(n * eb);
+      uint64_t st = 0x9E3779B97F4A7C15ull ^ n;
+      for (size_t i = 0; i < n; ++i) {
+        st = st * 6364136223846793005ull + 1442695040888963407ull;
+        const float v = amp * (static_cast<float>(st >> 40) / 8388608.0f - 1.0f);
+        if (eb == 2) {
+          uint32_t u;
+          std::memcpy(&u, &v, 4);
+          const uint16_t b16 = static_cast<uint16_t>(u >> 16);
+          std::memcpy(&hbuf[2 * i], &b16, 2);
+        } else {
+          std::memcpy(&hbuf[4 * i], &v, 4);
+        }
+      }
+      ok(cudaMemcpy(p, hbuf.data(), n * eb, cudaMemcpyHostToDevice));
+    };
+    fill(W, 12ull * h * h, 0.02f);
+    for (void* p : {x, y, dy, dx}) fill(p, T * h, 1.0f);
+    cudaStream_t st;
+    ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1;
+    ok(cudaEventCreate(&e0));
+    ok(cudaEventCreate(&e1));
+    gs::engine::LaunchCounter lc;
+    for (int pass = 0; pass < 2; ++pass) {  // 0: forward, 1: recompute + backward
+      for (int w = 0; w < 2; ++w)
+        ok(pass == 0 ? gs::engine::layer_forward(d, W, x, y, ws, st, lc)
+                     : gs::engine::layer_backward(d, W, x, dy, dx, dW, w == 0, nullptr, ws, st, lc));
+      ok(cudaStreamSynchronize(st));
+      ok(cudaEventRecord(e0, st));
+      const auto h0 = std::chrono::steady_clock::now();
+      for (int i = 0; i < iters; ++i)
+        ok(pass == 0 ? gs::engine::layer_forward(d, W, x, y, ws, st, lc)
+                     : gs::engine::layer_backward(d, W, x, dy, dx, dW, false, nullptr, ws, st, lc));
+      const auto h1 = std::chrono::steady_clock::now();
+      ok(cudaEventRecord(e1, st));
+      ok(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      ok(cudaEventElapsedTime(&ms, e0, e1));
+      out[2 * pass] = ms / iters;                                                            // GPU ms per call
+      out[2 * pass + 1] = std::chrono::duration<double, std::milli>(h1 - h0).count() / iters;  // host enqueue ms
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+    for (void* p : {W, x, y, dy, dx, static_cast<void*>(dW)}) cudaFree(p);
+    gs::engine::free_workspace(ws);
+  });
+}
 
 int gs_nccl_unique_id(uint8_t out[128]) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");

@@ -15,10 +15,13 @@
 //    possible.
 //  * Each data kind lives in a "blob" cut into segments by the split's byte
 //    boundaries (types.hpp:35-53 rounding) and by the immediate/delayed
-//    element boundary; SSD segments have a pinned image (authoritative copy /
-//    CPU double buffer), a pinned read-staging buffer and a 4 KiB-aligned
-//    region of the NVMe file.  Reads that the plan routes through the SSD
-//    are served from the read staging, so every SSD byte really round-trips.
+//    element boundary.  DRAM segments are pinned images.  SSD segments live
+//    only in a 4 KiB-aligned region of the NVMe file (the authoritative
+//    copy); they pass through a pinned staging slot drawn from a per-kind
+//    ring of cfg.ssd_ring_layers layers (slot = layer % ring), which the
+//    plan's SSD reads fill and its SSD writes drain.  DRAM use is therefore
+//    independent of the SSD-resident bytes, and every SSD byte the plan
+//    names really round-trips through the file.
 #include "offsim/executor.hpp"
 
 #include <cuda_runtime.h>
@@ -29,6 +32,8 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -97,8 +102,8 @@ enum class Tier { Dram, Ssd, Hbm };
 struct Segment {
   u64 lo = 0, hi = 0;  // logical byte range within the blob
   Tier tier = Tier::Dram;
-  uint8_t* img = nullptr;  // pinned image (Dram / Ssd)
-  uint8_t* rd = nullptr;   // pinned NVMe read staging (Ssd)
+  uint8_t* img = nullptr;  // Dram: pinned image; Ssd: the layer's staging-ring slot
+  uint8_t* rd = nullptr;   // Ssd: same staging slot (NVMe reads land here)
   uint8_t* dev = nullptr;  // HBM (Hbm)
   u64 file_off = 0;        // NVMe region (Ssd)
   u64 size() const { return hi - lo; }
@@ -163,6 +168,9 @@ struct Executor::Impl {
   // host state
   PinnedArena arena;
   std::unique_ptr<NvmeFile> nvme;
+  int ring_k = 1;                                     // staging slots per kind
+  std::vector<uint8_t*> ring_param, ring_opt, ring_ckpt;  // [ring_k] ([ring_k * M] for ckpt)
+  bool ssd_param = false, ssd_opt = false, ssd_ckpt = false;
   std::vector<Blob> param_blob, opt_blob;  // [N]
   std::vector<Blob> ckpt_blob;             // [N*M]
   std::vector<uint8_t*> host_grad;         // [N]
@@ -200,6 +208,10 @@ struct Executor::Impl {
   int last_iter = -1;
   std::vector<TraceRecord> trace;
   std::mutex trace_mu;
+  // GS_HOST_PROF=1: host seconds the GPU dispatcher spends waiting on
+  // dependencies vs enqueueing kernels (printed to stderr after each run)
+  bool host_prof = false;
+  double host_wait_s = 0.0, host_enqueue_s = 0.0;
   std::chrono::steady_clock::time_point host_base;
   cudaEvent_t ev_base = nullptr;
 
@@ -207,7 +219,8 @@ struct Executor::Impl {
   Impl(const SchedulePlan& p, const ExecConfig& c);
   ~Impl();
   void* dmalloc(u64 bytes);
-  Blob make_blob(u64 size, std::vector<u64> cuts, u64 cpu_bytes, bool hbm_for_cpu);
+  Blob make_blob(u64 size, std::vector<u64> cuts, u64 cpu_bytes, bool hbm_for_cpu, std::vector<uint8_t*>& ring,
+                 int slot);
   void init_weights();
   void build_tasks();
   void hazards();
@@ -352,13 +365,28 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   const bool need_nvme = plan.split.x_param < 1.0 || plan.split.x_ckpt < 1.0 || plan.split.x_opt < 1.0;
   if (need_nvme) nvme = std::make_unique<NvmeFile>(cfg.nvme_dir, cfg.odirect, 8);
   const u64 lp = static_cast<u64>(d.lp());
+  ring_k = std::max(1, std::min(cfg.ssd_ring_layers, N));
+  ring_param.assign(static_cast<size_t>(ring_k), nullptr);
+  ring_opt.assign(static_cast<size_t>(ring_k), nullptr);
+  ring_ckpt.assign(static_cast<size_t>(ring_k) * M, nullptr);
   for (int l = 0; l < N; ++l) {
-    param_blob.push_back(make_blob(lp * Ps, {lp * loc_now}, cpu_portion(lp * Ps, plan.split.x_param), false));
-    opt_blob.push_back(make_blob(opt_bytes, {12 * loc_now}, cpu_opt, opt_hbm));
+    param_blob.push_back(
+        make_blob(lp * Ps, {lp * loc_now}, cpu_portion(lp * Ps, plan.split.x_param), false, ring_param, l % ring_k));
+    opt_blob.push_back(make_blob(opt_bytes, {12 * loc_now}, cpu_opt, opt_hbm, ring_opt, l % ring_k));
     host_grad.push_back(arena.alloc(4 * Ps));
   }
   for (int l = 0; l < N; ++l)
-    for (int m = 0; m < M; ++m) ckpt_blob.push_back(make_blob(cb, {}, cpu_portion(cb, plan.split.x_ckpt), false));
+    for (int m = 0; m < M; ++m)
+      ckpt_blob.push_back(
+          make_blob(cb, {}, cpu_portion(cb, plan.split.x_ckpt), false, ring_ckpt, (l % ring_k) * M + m));
+  auto has_ssd = [](const Blob& b) {
+    for (const Segment& sg : b.segs)
+      if (sg.tier == Tier::Ssd) return true;
+    return false;
+  };
+  ssd_param = has_ssd(param_blob[0]);
+  ssd_opt = has_ssd(opt_blob[0]);
+  ssd_ckpt = has_ssd(ckpt_blob[0]);
   for (int i = 0; i < 2 * M; ++i) host_ilg.push_back(arena.alloc(cb));
   if (nvme) nvme->finalize_size();
 
@@ -400,9 +428,11 @@ void* Executor::Impl::dmalloc(u64 bytes) {
 }
 
 // Cut [0,size) at the CPU/SSD boundary and the extra cut points; CPU-resident
-// segments live in pinned DRAM (or HBM), SSD segments get image + read
-// staging + an NVMe region.
-Blob Executor::Impl::make_blob(u64 size, std::vector<u64> cuts, u64 cpu_bytes, bool hbm_for_cpu) {
+// segments live in pinned DRAM (or HBM), SSD segments get an NVMe region and
+// a 4 KiB-aligned place in staging slot ring[slot] (allocated by the first
+// blob that uses the slot; blobs of one kind have identical segments).
+Blob Executor::Impl::make_blob(u64 size, std::vector<u64> cuts, u64 cpu_bytes, bool hbm_for_cpu,
+                               std::vector<uint8_t*>& ring, int slot) {
   cuts.push_back(0);
   cuts.push_back(size);
   cuts.push_back(cpu_bytes);
@@ -424,11 +454,22 @@ Blob Executor::Impl::make_blob(u64 size, std::vector<u64> cuts, u64 cpu_bytes, b
       }
     } else {
       s.tier = Tier::Ssd;
-      s.img = arena.alloc(s.size());
-      s.rd = arena.alloc(s.size());
       s.file_off = nvme->reserve(s.size());
     }
     b.segs.push_back(s);
+  }
+  u64 staged = 0;
+  for (const Segment& s : b.segs)
+    if (s.tier == Tier::Ssd) staged += align_up(s.size(), kNvmeAlign);
+  if (staged > 0) {
+    uint8_t*& base = ring[static_cast<size_t>(slot)];
+    if (!base) base = arena.alloc(staged);
+    u64 off = 0;
+    for (Segment& s : b.segs) {
+      if (s.tier != Tier::Ssd) continue;
+      s.img = s.rd = base + off;
+      off += align_up(s.size(), kNvmeAlign);
+    }
   }
   return b;
 }
@@ -546,7 +587,8 @@ void Executor::Impl::build_tasks() {
 namespace {
 enum SlotKind {
   kDevParam, kInX, kOutY, kInG, kOutG, kGrad, kRetain, kHostIlg, kParamImg, kParamRd, kOptImg, kOptRd, kCkptImg,
-  kCkptRd, kHostGrad, kOptDev, kParamFile, kOptFile, kCkptFile
+  kCkptRd, kHostGrad, kOptDev, kParamFile, kOptFile, kCkptFile,
+  kParamStage, kOptStage, kCkptStage  // SSD staging-ring slots (layer % ring)
 };
 struct Access {
   long long slot;
@@ -567,6 +609,14 @@ void Executor::Impl::hazards() {
     const int parm1 = (((st - 1) % 2) + 2) % 2;
     const bool late = delayed(t);
     const int imm_late = late ? 1 : 0;
+    const int rl = ((l % ring_k) + ring_k) % ring_k, rlm1 = (((l - 1) % ring_k) + ring_k) % ring_k;
+    // staging-ring accesses, only for kinds that have SSD-resident bytes
+    auto RS = [&](bool on, int kind, long long a, long long b2) {
+      if (on) R(slot_id(kind, a, b2));
+    };
+    auto WS = [&](bool on, int kind, long long a, long long b2) {
+      if (on) W(slot_id(kind, a, b2));
+    };
     switch (t.kind) {
       case TaskKind::FixedOps: break;
       case TaskKind::FwdCompute:
@@ -604,6 +654,11 @@ void Executor::Impl::hazards() {
         W(slot_id(kOptImg, l, imm_late));
         W(slot_id(kOptDev, l, imm_late));
         W(slot_id(kParamImg, l));
+        RS(ssd_opt, kOptStage, rl, imm_late);
+        WS(ssd_opt, kOptStage, rl, imm_late);
+        WS(ssd_param, kParamStage, rl, imm_late);
+        // a skipped delayed step refills the slice from the file
+        if (late) RS(ssd_param, kParamFile, l, 1);
         break;
       case TaskKind::Xfer: {
         const bool fwd = fwd_phase[i] != 0;
@@ -612,13 +667,20 @@ void Executor::Impl::hazards() {
             if (t.link == LinkKind::SSD_Read) {
               W(slot_id(kParamRd, l));
               R(slot_id(kParamFile, l, 0));
-              if (!fwd) R(slot_id(kParamFile, l, 1));
+              WS(ssd_param, kParamStage, rl, 0);
+              if (!fwd) {
+                R(slot_id(kParamFile, l, 1));
+                WS(ssd_param, kParamStage, rl, 1);
+              }
             } else if (t.link == LinkKind::SSD_Write) {
               R(slot_id(kParamImg, l));
               W(slot_id(kParamFile, l, imm_late));
+              RS(ssd_param, kParamStage, rl, imm_late);
             } else {
               R(slot_id(kParamImg, l));
               R(slot_id(kParamRd, l));
+              RS(ssd_param, kParamStage, rl, 0);
+              RS(ssd_param, kParamStage, rl, 1);
               W(slot_id(kDevParam, (((st + 1) % 2) + 2) % 2));
             }
             break;
@@ -627,35 +689,43 @@ void Executor::Impl::hazards() {
               if (t.link == LinkKind::PCIe_D2H) {
                 R(slot_id(kOutY, par, 0));
                 W(slot_id(kCkptImg, l, m));
+                WS(ssd_ckpt, kCkptStage, rl, m);
               } else if (t.link == LinkKind::PCIe_H2D) {
                 R(slot_id(kCkptImg, l, m));
                 R(slot_id(kCkptRd, l, m));
+                RS(ssd_ckpt, kCkptStage, rl, m);
                 W(slot_id(kInX, par, 0));
               } else if (t.link == LinkKind::SSD_Write) {
                 R(slot_id(kCkptImg, l, m));
                 W(slot_id(kCkptFile, l, m));
+                RS(ssd_ckpt, kCkptStage, rl, m);
               } else {
                 W(slot_id(kCkptRd, l, m));
                 R(slot_id(kCkptFile, l, m));
+                WS(ssd_ckpt, kCkptStage, rl, m);
               }
               break;
             }
             if (t.link == LinkKind::PCIe_D2H) {
               R(slot_id(kOutY, par, m));
               W(slot_id(kCkptImg, l, m));
+              WS(ssd_ckpt, kCkptStage, rl, m);
             } else if (t.link == LinkKind::PCIe_H2D) {
               R(slot_id(kCkptImg, l - 1, m));
               if (!fwd) R(slot_id(kCkptRd, l - 1, m));
+              RS(ssd_ckpt, kCkptStage, rlm1, m);
               W(slot_id(kInX, par, m));
             } else if (t.link == LinkKind::SSD_Write) {
               for (int k = 0; k < M; ++k) {
                 R(slot_id(kCkptImg, l, k));
                 W(slot_id(kCkptFile, l, k));
+                RS(ssd_ckpt, kCkptStage, rl, k);
               }
             } else {
               for (int k = 0; k < M; ++k) {
                 W(slot_id(kCkptRd, l - 1, k));
                 R(slot_id(kCkptFile, l - 1, k));
+                WS(ssd_ckpt, kCkptStage, rlm1, k);
               }
             }
             break;
@@ -681,9 +751,11 @@ void Executor::Impl::hazards() {
             if (t.link == LinkKind::SSD_Read) {
               W(slot_id(kOptRd, l, imm_late));
               R(slot_id(kOptFile, l, imm_late));
+              WS(ssd_opt, kOptStage, rl, imm_late);
             } else {
               R(slot_id(kOptImg, l, imm_late));
               W(slot_id(kOptFile, l, imm_late));
+              RS(ssd_opt, kOptStage, rl, imm_late);
             }
             break;
         }
@@ -836,6 +908,7 @@ void Executor::Impl::run_task(int id, int it) {
   const Resource r = res_of[static_cast<size_t>(id)];
   const bool stream = is_stream[static_cast<size_t>(id)];
   cudaStream_t st = stream_of(r);
+  const auto w0 = std::chrono::steady_clock::now();
   for (int dep : t.deps) wait_dep(dep, it, stream, st);
   if (t.cross_iter_dep >= 0) wait_dep(t.cross_iter_dep, it - 1, stream, st);
   for (const ExtraDep& x : extra[static_cast<size_t>(id)]) wait_dep(x.task, it + x.offset, stream, st);
@@ -853,6 +926,11 @@ void Executor::Impl::run_task(int id, int it) {
   }
   if (stream) {
     cuda_check(cudaEventRecord(ev_done[static_cast<size_t>(id)][static_cast<size_t>(it % 3)], st), "record");
+  }
+  if (host_prof && r == Resource::GPU) {
+    const auto h1 = std::chrono::steady_clock::now();
+    host_wait_s += std::chrono::duration<double>(h0 - w0).count();
+    host_enqueue_s += std::chrono::duration<double>(h1 - h0).count();
   }
   if (t.kind == TaskKind::Xfer) note_ledger(it, t, phys);
   if (cfg.record_trace) {
@@ -1027,7 +1105,19 @@ void Executor::Impl::step_task(const Task& t, int it) {
     // alpha slice of the previous iteration (step count git); nothing is
     // retained before the first iteration
     const long long ready = late_ready[static_cast<size_t>(l)].load();
-    if (el_late == 0 || ready != git - 1 || late_applied[static_cast<size_t>(l)].load() >= ready) return;
+    if (el_late == 0 || ready != git - 1 || late_applied[static_cast<size_t>(l)].load() >= ready) {
+      // nothing to apply (first iteration, or flushed): the slice's SSD bytes
+      // still have to be in the staging slot for the plan's parameter write-
+      // back and upload that follow
+      if (loc_late > 0 && ssd_param) {
+        // the dependencies were enqueued on s_opt as stream waits; this host
+        // write into the (shared) staging slot must follow them too
+        cuda_check(cudaStreamSynchronize(s_opt), "refill sync");
+        const u64 lp = static_cast<u64>(d.lp());
+        ssd_io(param_blob[static_cast<size_t>(l)], lp * loc_now, lp * n_my, false);
+      }
+      return;
+    }
     if (loc_late > 0) apply_adam(l, loc_now, n_my, retain[static_cast<size_t>(l)], static_cast<int>(git), s_opt, it);
     late_applied[static_cast<size_t>(l)].store(ready);
     return;
@@ -1186,6 +1276,11 @@ ExecReport Executor::run(int iterations, const int32_t* tokens, bool tokens_on_d
   I.last_iter = iterations - 1;
   I.trace.clear();
   I.launches.store(0);
+  {
+    const char* e = getenv("GS_HOST_PROF");
+    I.host_prof = e && atoi(e) != 0;
+    I.host_wait_s = I.host_enqueue_s = 0.0;
+  }
   I.prof.reset();
 
   cuda_check(cudaDeviceSynchronize(), "pre-run sync");
@@ -1220,6 +1315,9 @@ ExecReport Executor::run(int iterations, const int32_t* tokens, bool tokens_on_d
   float ms = 0.0f;
   cuda_check(cudaEventElapsedTime(&ms, I.ev_base, ev_end), "elapsed");
   rep.total_ms = ms;
+  if (I.host_prof)
+    fprintf(stderr, "[gs host] %d iterations: GPU %.1f ms, compute dispatcher enqueue %.1f ms, dep waits %.1f ms\n",
+            iterations, ms, 1e3 * I.host_enqueue_s, 1e3 * I.host_wait_s);
   cuda_check(cudaMemcpy(loss.data(), I.dev_loss, sizeof(double) * loss.size(), cudaMemcpyDeviceToHost), "loss");
   cudaEventDestroy(ev_end);
   const double denom = static_cast<double>(I.d.T()) * I.M;
@@ -1253,12 +1351,21 @@ ExecReport Executor::run(int iterations, const int32_t* tokens, bool tokens_on_d
 void Executor::flush() {
   Impl& I = *impl_;
   cuda_check(cudaDeviceSynchronize(), "flush sync");
+  const u64 lp = static_cast<u64>(I.d.lp());
   for (int l = 0; l < I.N; ++l) {
     const long long ready = I.late_ready[static_cast<size_t>(l)].load();
     if (I.el_late == 0 || ready < 0 || I.late_applied[static_cast<size_t>(l)].load() >= ready) continue;
-    if (I.loc_late > 0)
+    if (I.loc_late > 0) {
+      Blob& ob = I.opt_blob[static_cast<size_t>(l)];
+      Blob& pb = I.param_blob[static_cast<size_t>(l)];
+      // SSD-resident state: file -> staging slot, step, staging -> file
+      if (I.ssd_opt) I.ssd_io(ob, 12 * I.loc_now, ob.size, false);
       I.apply_adam(l, I.loc_now, I.n_my, I.retain[static_cast<size_t>(l)], static_cast<int>(ready + 1), I.s_opt, -2,
                    Src::Image);
+      cuda_check(cudaStreamSynchronize(I.s_opt), "flush step");
+      if (I.ssd_opt) I.ssd_io(ob, 12 * I.loc_now, ob.size, true);
+      if (I.ssd_param) I.ssd_io(pb, lp * I.loc_now, pb.size, true);
+    }
     I.late_applied[static_cast<size_t>(l)].store(ready);
   }
   if (I.fixed_done < I.global_iter) {
@@ -1302,10 +1409,18 @@ void read_field(Executor::Impl& I, int layer, int f, float* out) {
   const Blob& b = I.opt_blob[static_cast<size_t>(layer)];
   std::vector<uint8_t> all(b.size);
   for (const Segment& s : b.segs) {
-    if (s.tier == Tier::Hbm)
+    if (s.tier == Tier::Hbm) {
       cuda_check(cudaMemcpy(all.data() + s.lo, s.dev, s.size(), cudaMemcpyDeviceToHost), "read opt");
-    else
+    } else if (s.tier == Tier::Dram) {
       std::memcpy(all.data() + s.lo, s.img, s.size());
+    } else {  // the NVMe file holds the only copy
+      const u64 n = align_up(s.size(), kNvmeAlign);
+      void* tmp = nullptr;
+      if (posix_memalign(&tmp, kNvmeAlign, n) != 0) throw std::bad_alloc();
+      I.nvme->read(s.file_off, tmp, s.size());
+      std::memcpy(all.data() + s.lo, tmp, s.size());
+      std::free(tmp);
+    }
   }
   const float* st = reinterpret_cast<const float*>(all.data());
   // this rank's shard [e_lo, e_hi) of the layer (the whole layer when W == 1)

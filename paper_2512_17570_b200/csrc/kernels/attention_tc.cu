@@ -332,7 +332,9 @@ struct FaSmem2 {
   uint8_t K[2][kKV2];        // [2 d-chunks][64 rows][128 B]
   uint8_t V[2][kKV2];
   uint8_t P[kBQ * kBK2 * 2]; // [128 rows][128 B] (64 keys)
-  uint64_t q_full, k_full[2], v_full[2], kv_empty[2], s_full[2], p_full, o_done;
+  // K and V slots are released separately: K(kb) right after S(kb), so the
+  // load of K(kb+2) overlaps softmax(kb) instead of waiting for PV(kb)
+  uint64_t q_full, k_full[2], v_full[2], k_empty[2], v_empty[2], s_full[2], p_full, o_done;
   uint32_t tmem;
 };
 
@@ -354,7 +356,8 @@ __global__ void __launch_bounds__(256, 2)
     for (int i = 0; i < 2; ++i) {
       bar_init(&sm.k_full[i], 1);
       bar_init(&sm.v_full[i], 1);
-      bar_init(&sm.kv_empty[i], 1);
+      bar_init(&sm.k_empty[i], 1);
+      bar_init(&sm.v_empty[i], 1);
       bar_init(&sm.s_full[i], 1);
     }
     bar_init(&sm.p_full, 128);
@@ -378,10 +381,11 @@ __global__ void __launch_bounds__(256, 2)
       for (int c = 0; c < 2; ++c) tma2d(sm.Q + c * 16384, &map_q, &sm.q_full, j * kD + 64 * c, row0 + q0);
       for (int kb = 0; kb < nblk; ++kb) {
         const int buf = kb & 1;
-        bar_wait(&sm.kv_empty[buf], ((kb >> 1) & 1) ^ 1);
+        bar_wait(&sm.k_empty[buf], ((kb >> 1) & 1) ^ 1);
         bar_expect(&sm.k_full[buf], kKV2);
         for (int c = 0; c < 2; ++c)
           tma2d(sm.K[buf] + c * 8192, &map_kv, &sm.k_full[buf], h + j * kD + 64 * c, row0 + kb * kBK2);
+        bar_wait(&sm.v_empty[buf], ((kb >> 1) & 1) ^ 1);
         bar_expect(&sm.v_full[buf], kKV2);
         for (int c = 0; c < 2; ++c)
           tma2d(sm.V[buf] + c * 8192, &map_kv, &sm.v_full[buf], 2 * h + j * kD + 64 * c, row0 + kb * kBK2);
@@ -403,6 +407,7 @@ __global__ void __launch_bounds__(256, 2)
               (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24),
               ks != 0);
         commit(&sm.s_full[buf]);
+        commit(&sm.k_empty[buf]);
       };
       issue_s(0);
       for (int kb = 0; kb < nblk; ++kb) {
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(256, 2)
           mma(tmem + 128, sdesc(pa + ks * 32, 16, 1024), sdesc(va + ks * 2048, 8192, 1024), idesc(true),
               (kb | ks) != 0);
         commit(&sm.o_done);
-        commit(&sm.kv_empty[buf]);
+        commit(&sm.v_empty[buf]);
       }
     }
   } else if (warp >= 4) {
@@ -992,6 +997,251 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
   }
 }
 
+// ---------------------------------------------------------- backward v3
+// Same math; the MMA issue order and buffering are arranged so that neither
+// the Q/dO loads nor the dQ drain sit on the tensor pipe's critical path:
+//   per block i the MMA warp issues dQ^T(i) first (commit dq_full), then
+//   dV(i), dK(i) (commit q_empty / pds_empty), then S^T/dP^T(i+2).  The drain
+//   of dQ^T(i) overlaps dV/dK(i); the softmax of block i+1 overlaps
+//   dQ/dV/dK(i); the single P^T/dS^T buffer is rewritten while S/dP(i+2)
+//   run; Q/dO/L/D use a 3-slot ring so block i+2's loads start one block
+//   earlier than in v2.  dQ^T leaves through a 32-query fp32 staging half.
+//   TMEM: [0,128)/[128,256) S^T|dP^T of block i&1 (dQ^T(i) overwrites the
+//   S^T half after the softmax read it), [256,384) dV, [384,512) dK.
+constexpr int kQS = 3;  // Q / dO ring depth
+struct FaBwdSmem3 {
+  uint8_t K[kTile], V[kTile];
+  uint8_t Q[kQS][kHalf], dO[kQS][kHalf];
+  uint8_t PT[kPT], dST[kPT];
+  float dq_stage[kBQb / 2][kD];
+  float L[kQS][kBQb], D[kQS][kBQb];
+  uint64_t kv_full, q_full[kQS], q_empty[kQS], s_full[2], ps_full, pds_empty, dq_full[2], dq_empty[2], mma_done;
+  uint32_t tmem;
+};
+
+__global__ void __launch_bounds__(kThreadsBwd2, 1)
+    fa_bwd_tc3_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_q,
+                      const __grid_constant__ CUtensorMap map_do, const __grid_constant__ CUtensorMap map_dq,
+                      const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv, int s,
+                      int h, int H, float scale) {
+  extern __shared__ __align__(1024) uint8_t rawb3[];
+  FaBwdSmem3& sm = *reinterpret_cast<FaBwdSmem3*>(rawb3);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.y;  // grid (b*H, s/128): key block 0 (most query blocks) first
+  const int bh = blockIdx.x, bi = bh / H, j = bh % H;
+  const int row0 = bi * s;
+  const int k0 = kb * kBK;
+  const int qb0 = k0 / kBQb, nq = s / kBQb - qb0;
+  const float scale_log2 = scale * 1.4426950408889634f;
+
+  if (threadIdx.x == 0) {
+    bar_init(&sm.kv_full, 1);
+    for (int i = 0; i < kQS; ++i) {
+      bar_init(&sm.q_full[i], 1);
+      bar_init(&sm.q_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&sm.s_full[i], 1);
+      bar_init(&sm.dq_full[i], 1);
+      bar_init(&sm.dq_empty[i], 128);
+    }
+    bar_init(&sm.ps_full, 128);
+    bar_init(&sm.pds_empty, 1);
+    bar_init(&sm.mma_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = sm.tmem;
+  constexpr uint32_t kDV = 256, kDK = 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_do)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_q)) : "memory");
+      bar_expect(&sm.kv_full, 2 * kTile);
+      for (int c = 0; c < 2; ++c) {
+        tma2d(sm.K + c * 16384, &map_qkv, &sm.kv_full, h + j * kD + 64 * c, row0 + k0);
+        tma2d(sm.V + c * 16384, &map_qkv, &sm.kv_full, 2 * h + j * kD + 64 * c, row0 + k0);
+      }
+      for (int i = 0; i < nq; ++i) {
+        const int sl = i % kQS, q0 = (qb0 + i) * kBQb;
+        bar_wait(&sm.q_empty[sl], ((i / kQS) & 1) ^ 1);
+        bar_expect(&sm.q_full[sl], 2 * kHalf + 2 * kBQb * 4);
+        for (int c = 0; c < 2; ++c) {
+          tma2d(sm.Q[sl] + c * 8192, &map_q, &sm.q_full[sl], j * kD + 64 * c, row0 + q0);
+          tma2d(sm.dO[sl] + c * 8192, &map_do, &sm.q_full[sl], j * kD + 64 * c, row0 + q0);
+        }
+        bulk_g2s(sm.L[sl], lse + (long long)bh * s + q0, kBQb * 4, &sm.q_full[sl]);
+        bulk_g2s(sm.D[sl], Dg + (long long)bh * s + q0, kBQb * 4, &sm.q_full[sl]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t ka = su32(sm.K), va = su32(sm.V), pa = su32(sm.PT), da = su32(sm.dST);
+      bar_wait(&sm.kv_full, 0);
+      auto issue_s = [&](int i) {  // S^T, dP^T of block i into TMEM buffer i&1
+        const int buf = i & 1, sl = i % kQS;
+        bar_wait(&sm.q_full[sl], (i / kQS) & 1);
+        bar_wait(&sm.dq_empty[buf], ((i >> 1) & 1) ^ 1);  // dQ^T of block i-2 drained
+        fence_after();
+        const uint32_t qa = su32(sm.Q[sl]), oa = su32(sm.dO[sl]);
+        const uint32_t t0 = tmem + buf * 128;
+#pragma unroll
+        for (int ks = 0; ks < kD / 16; ++ks) {
+          mma(t0, desc_k(ka, ks, 128), desc_k(qa, ks, 64), idesc2(64, false, false), ks != 0);
+          mma(t0 + 64, desc_k(va, ks, 128), desc_k(oa, ks, 64), idesc2(64, false, false), ks != 0);
+        }
+        commit(&sm.s_full[buf]);
+      };
+      issue_s(0);
+      if (nq > 1) issue_s(1);
+      for (int i = 0; i < nq; ++i) {
+        const int buf = i & 1, sl = i % kQS;
+        bar_wait(&sm.ps_full, i & 1);
+        fence_after();
+        // dQ^T(i) = K^T dS^T into the (already read) S^T half of buffer i&1
+#pragma unroll
+        for (int ks = 0; ks < kBK / 16; ++ks)
+          mma(tmem + buf * 128, desc_mn(ka, ks, 16384), desc_mn(da, ks, 8192), idesc2(64, true, true), ks != 0);
+        commit(&sm.dq_full[buf]);
+        const uint32_t qa = su32(sm.Q[sl]), oa = su32(sm.dO[sl]);
+#pragma unroll
+        for (int ks = 0; ks < kBQb / 16; ++ks) {
+          mma(tmem + kDV, desc_k(pa, ks, 128), desc_mn(oa, ks, 8192), idesc2(128, false, true), (i | ks) != 0);
+          mma(tmem + kDK, desc_k(da, ks, 128), desc_mn(qa, ks, 8192), idesc2(128, false, true), (i | ks) != 0);
+        }
+        commit(&sm.q_empty[sl]);
+        commit(&sm.pds_empty);
+        if (i + 2 < nq) issue_s(i + 2);
+      }
+      commit(&sm.mma_done);
+    }
+  } else if (warp >= 4 && warp < 8) {
+    const int r = (warp - 4) * 32 + lane;  // key row
+    const uint32_t lb = ((uint32_t)((warp & 3) * 32)) << 16;
+    const int key = k0 + r;
+    const uint32_t swz = (uint32_t)(r & 7);
+    const int rowoff = (r >> 3) * 1024 + (r & 7) * 128;
+    for (int i = 0; i < nq; ++i) {
+      const int buf = i & 1, sl = i % kQS, q0 = (qb0 + i) * kBQb;
+      bar_wait(&sm.q_full[sl], (i / kQS) & 1);  // L, D of this block
+      bar_wait(&sm.s_full[buf], (i >> 1) & 1);
+      fence_after();
+      float p[kBQb], ds[kBQb];
+#pragma unroll
+      for (int c = 0; c < kBQb / 32; ++c) {
+        uint32_t a[32], b[32];
+        tld32(tmem + lb + buf * 128 + c * 32, a);
+        tld32(tmem + lb + buf * 128 + 64 + c * 32, b);
+        tld_wait();
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int qi = c * 32 + q;
+          float pv = exp2f(__uint_as_float(a[q]) * scale_log2 - sm.L[sl][qi] * 1.4426950408889634f);
+          if (q0 + qi < key) pv = 0.0f;  // causal
+          p[qi] = pv;
+          ds[qi] = pv * (__uint_as_float(b[q]) - sm.D[sl][qi]);
+        }
+      }
+      bar_wait(&sm.pds_empty, (i & 1) ^ 1);  // MMAs of block i-1 done with P^T / dS^T
+#pragma unroll
+      for (int pc = 0; pc < 8; ++pc) {
+        const float* v = p + pc * 8;
+        const float* w = ds + pc * 8;
+        *reinterpret_cast<uint4*>(sm.PT + rowoff + ((pc ^ swz) << 4)) =
+            make_uint4(pack(v[0], v[1]), pack(v[2], v[3]), pack(v[4], v[5]), pack(v[6], v[7]));
+        *reinterpret_cast<uint4*>(sm.dST + rowoff + ((pc ^ swz) << 4)) =
+            make_uint4(pack(w[0], w[1]), pack(w[2], w[3]), pack(w[4], w[5]), pack(w[6], w[7]));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      fence_before();
+      bar_arrive(&sm.ps_full);
+    }
+    bar_wait(&sm.mma_done, 0);
+    fence_after();
+    bf16* out = dqkv + (long long)(row0 + key) * 3 * h + h + j * kD;
+#pragma unroll
+    for (int c = 0; c < kD / 32; ++c) {
+      uint32_t rr[32];
+      tld32(tmem + lb + kDK + c * 32, rr);
+      tld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack(__uint_as_float(rr[8 * q]) * scale, __uint_as_float(rr[8 * q + 1]) * scale);
+        w.y = pack(__uint_as_float(rr[8 * q + 2]) * scale, __uint_as_float(rr[8 * q + 3]) * scale);
+        w.z = pack(__uint_as_float(rr[8 * q + 4]) * scale, __uint_as_float(rr[8 * q + 5]) * scale);
+        w.w = pack(__uint_as_float(rr[8 * q + 6]) * scale, __uint_as_float(rr[8 * q + 7]) * scale);
+        *reinterpret_cast<uint4*>(out + c * 32 + 8 * q) = w;
+      }
+    }
+  } else if (warp >= 8) {
+    const int r = (warp - 8) * 32 + lane;  // d row of dQ^T; key row for dV
+    const uint32_t lb = ((uint32_t)((warp & 3) * 32)) << 16;
+    for (int i = 0; i < nq; ++i) {
+      const int buf = i & 1;
+      bar_wait(&sm.dq_full[buf], (i >> 1) & 1);
+      fence_after();
+      uint32_t rr[kBQb];
+      tld32(tmem + lb + buf * 128, *reinterpret_cast<uint32_t(*)[32]>(rr));
+      tld32(tmem + lb + buf * 128 + 32, *reinterpret_cast<uint32_t(*)[32]>(rr + 32));
+      tld_wait();
+      fence_before();
+      bar_arrive(&sm.dq_empty[buf]);  // TMEM buffer free for S/dP(i+2)
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        if (r == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < kBQb / 2; ++q) sm.dq_stage[q][r] = __uint_as_float(rr[half * (kBQb / 2) + q]) * scale;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+        if (r == 0) {
+          const int q0 = (qb0 + i) * kBQb + half * (kBQb / 2);
+          asm volatile(
+              "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                  reinterpret_cast<uint64_t>(&map_dq)),
+              "r"(su32(&sm.dq_stage[0][0])), "r"(j * kD), "r"(row0 + q0)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    }
+    if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    bar_wait(&sm.mma_done, 0);
+    fence_after();
+    bf16* out = dqkv + (long long)(row0 + k0 + r) * 3 * h + 2 * h + j * kD;
+#pragma unroll
+    for (int c = 0; c < kD / 32; ++c) {
+      uint32_t rr2[32];
+      tld32(tmem + lb + kDV + c * 32, rr2);
+      tld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack(__uint_as_float(rr2[8 * q]), __uint_as_float(rr2[8 * q + 1]));
+        w.y = pack(__uint_as_float(rr2[8 * q + 2]), __uint_as_float(rr2[8 * q + 3]));
+        w.z = pack(__uint_as_float(rr2[8 * q + 4]), __uint_as_float(rr2[8 * q + 5]));
+        w.w = pack(__uint_as_float(rr2[8 * q + 6]), __uint_as_float(rr2[8 * q + 7]));
+        *reinterpret_cast<uint4*>(out + c * 32 + 8 * q) = w;
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1097,20 +1347,33 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
+  static const int variant = [] {  // GS_ATTN_BWD=1: unpipelined kernel, 2: v2; default 3
+    const char* e = getenv("GS_ATTN_BWD");
+    return e ? atoi(e) : 3;
+  }();
   CUtensorMap mdq;
   {
     const cuuint64_t dims[2] = {(cuuint64_t)h, (cuuint64_t)b * s};
     const cuuint64_t strides[1] = {(cuuint64_t)h * 4};
-    const cuuint32_t box[2] = {128, 64};
+    const cuuint32_t box[2] = {128, (cuuint32_t)(variant == 3 ? kBQb / 2 : kBQb)};
     if (encoder()(&mdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq_acc, dims, strides, box, elem,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  static const int variant = [] {  // GS_ATTN_BWD=1: unpipelined kernel; default 2
-    const char* e = getenv("GS_ATTN_BWD");
-    return e ? atoi(e) : 2;
-  }();
+  if (variant == 3) {
+    const int smem3 = (int)sizeof(FaBwdSmem3);
+    static bool init3 = false;
+    if (!init3) {
+      cudaError_t e = cudaFuncSetAttribute(fa_bwd_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+      if (e != cudaSuccess) return e;
+      init3 = true;
+    }
+    count_launch();
+    fa_bwd_tc3_kernel<<<dim3(b * H, s / kBK), kThreadsBwd2, smem3, st>>>(mq, mq64, md, mdq, lse, D, (bf16*)dqkv, s,
+                                                                          h, H, 1.0f / sqrtf((float)kD));
+    return cudaGetLastError();
+  }
   if (variant == 2) {
     const int smem2 = (int)sizeof(FaBwdSmem2);
     static bool init2 = false;

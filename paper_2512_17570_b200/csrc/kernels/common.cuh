@@ -43,6 +43,22 @@ __device__ __forceinline__ float gelu_grad_f(float u) {
   return 0.5f * (1.0f + t) + 0.5f * u * (1.0f - t * t) * kGeluK * (1.0f + 3.0f * kGeluC * u * u);
 }
 
+// bf16-path variants on the SFU tanh (tanh.approx.f32, |rel err| < 2^-10.9):
+// the result is rounded to bf16 (2^-8) right after, so the accurate libm
+// tanhf (~20 FP32 instructions) only costs GEMM-epilogue issue slots.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float gelu_fast(float u) {
+  return 0.5f * u * (1.0f + tanh_fast(kGeluK * (u + kGeluC * u * u * u)));
+}
+__device__ __forceinline__ float gelu_grad_fast(float u) {
+  const float t = tanh_fast(kGeluK * (u + kGeluC * u * u * u));
+  return 0.5f * (1.0f + t) + 0.5f * u * (1.0f - t * t) * kGeluK * (1.0f + 3.0f * kGeluC * u * u);
+}
+
 // Kernels launched through this library (host-side count, all threads).
 long long& launch_counter_ref();
 inline void count_launch(int n = 1) { __atomic_fetch_add(&launch_counter_ref(), (long long)n, __ATOMIC_RELAXED); }

@@ -9,8 +9,11 @@
 // and weight-gradient (dY^T X) all run without transpose copies.
 #include <cuda.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -181,6 +184,56 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Work list of one persistent unit (a CTA, or a CTA pair for CG = 2).
+// Tiles [0, dp) are data-parallel (whole tiles, round-robin over units).  The
+// last `rem` tiles are stream-K: their rem * kt k-blocks are cut into `units`
+// contiguous, equal ranges, so the tail wave is spread over every SM instead
+// of leaving (1 - rem / units) of them idle.  A range covers at most two
+// tiles (rem < units); the unit whose range holds a tile's last k-block owns
+// the tile: it adds the fp32 partials of the earlier pieces (workspace slot =
+// the writer's CTA, readiness flag = launch epoch) before the fused epilogue.
+// Every unit has at most one non-owner piece, always its last item, and an
+// owner only waits on lower units, so the waits form no cycle.
+struct Sched {
+  int unit, units, kt, rem, dp;
+  __device__ __forceinline__ int n_dp() const { return unit < dp ? (dp - 1 - unit) / units + 1 : 0; }
+  __device__ __forceinline__ long long sk_bound(int u) const { return (long long)u * rem * kt / units; }
+  // item i of this unit: tile t, k-blocks [ka, kb)
+  __device__ __forceinline__ bool item(int i, int& t, int& ka, int& kb) const {
+    const int nd = n_dp();
+    if (i < nd) {
+      t = unit + i * units;
+      ka = 0;
+      kb = kt;
+      return true;
+    }
+    if (rem == 0) return false;
+    const long long l1 = sk_bound(unit + 1);
+    long long l = sk_bound(unit);
+    for (int j = nd; l < l1; ++j) {
+      const int ts = (int)(l / kt), a = (int)(l % kt);
+      const int b = (int)((long long)a + (l1 - l) < kt ? (long long)a + (l1 - l) : kt);
+      if (j == i) {
+        t = dp + ts;
+        ka = a;
+        kb = b;
+        return true;
+      }
+      l += b - a;
+    }
+    return false;
+  }
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const float (&v)[32], int row, int col, int M, int N, int ldc,
                                                void* C, const bf16* R, bf16* G) {
@@ -215,9 +268,9 @@ __device__ __forceinline__ void epilogue_chunk(const float (&v)[32], int row, in
           w[8 * q + 2 * j + 1] += __bfloat162float(p.y);
         } else {
           // round dg to bf16 first: identical to storing dg and running gelu_bwd
-          w[8 * q + 2 * j] = __bfloat162float(__float2bfloat16_rn(w[8 * q + 2 * j])) * gelu_grad_f(__bfloat162float(p.x));
+          w[8 * q + 2 * j] = __bfloat162float(__float2bfloat16_rn(w[8 * q + 2 * j])) * gelu_grad_fast(__bfloat162float(p.x));
           w[8 * q + 2 * j + 1] =
-              __bfloat162float(__float2bfloat16_rn(w[8 * q + 2 * j + 1])) * gelu_grad_f(__bfloat162float(p.y));
+              __bfloat162float(__float2bfloat16_rn(w[8 * q + 2 * j + 1])) * gelu_grad_fast(__bfloat162float(p.y));
         }
       }
     }
@@ -233,7 +286,7 @@ __device__ __forceinline__ void epilogue_chunk(const float (&v)[32], int row, in
     for (int q = 0; q < 4; ++q) {
       float r[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = gelu_f(__bfloat162float(__float2bfloat16_rn(w[8 * q + j])));
+      for (int j = 0; j < 8; ++j) r[j] = gelu_fast(__bfloat162float(__float2bfloat16_rn(w[8 * q + j])));
       g[q] = make_uint4(pack_bf16(r[0], r[1]), pack_bf16(r[2], r[3]), pack_bf16(r[4], r[5]), pack_bf16(r[6], r[7]));
     }
   }
@@ -243,7 +296,8 @@ __device__ __forceinline__ void epilogue_chunk(const float (&v)[32], int row, in
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
-                   int N, int K, void* C, const bf16* R, bf16* G, int ldc) {
+                   int N, int K, void* C, const bf16* R, bf16* G, int ldc, int sk_rem, float4* __restrict__ sk_ws,
+                   int* __restrict__ sk_flags, int sk_epoch) {
   using Cfg = TileCfg<BN, CG>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -263,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int unit = CG == 2 ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
   const int units = CG == 2 ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
   constexpr int kBN_local = BN / CG;  // B rows staged by this CTA
+  const Sched sch{unit, units, kt, sk_rem, tiles - sk_rem};
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
@@ -302,10 +357,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (CG == 2) tma_load_2d_2sm(dst, map, bar, c0, c1);
         else tma_load_2d(dst, map, bar, c0, c1);
       };
-      for (int t = unit; t < tiles; t += units) {
+      int t, ka, kb_end;
+      for (int it = 0; sch.item(it, t, ka, kb_end); ++it) {
         const int m0 = (t % mt) * BM * CG + static_cast<int>(rank) * BM;
         const int n0 = (t / mt) * BN + static_cast<int>(rank) * kBN_local;
-        for (int kb = 0; kb < kt; ++kb) {
+        for (int kb = ka; kb < kb_end; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           // CTA 0's barrier collects the bytes of both CTAs of a pair
           if (rank == 0) mbar_expect_tx(&full[stage], Cfg::kStageBytes * CG);
@@ -335,11 +391,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = unit; t < tiles; t += units) {
+    int t, ka, kb_end;
+    for (int it = 0; sch.item(it, t, ka, kb_end); ++it) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < kt; ++kb) {
+      for (int kb = ka; kb < kb_end; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
@@ -348,9 +405,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int ks = 0; ks < BK / 16; ++ks) {
             if constexpr (CG == 2)
-              tc_mma_pair(d_tmem, operand_desc<A_MN>(a0, ks), operand_desc<B_MN>(b0, ks), idesc, (kb | ks) != 0);
+              tc_mma_pair(d_tmem, operand_desc<A_MN>(a0, ks), operand_desc<B_MN>(b0, ks), idesc,
+                          (kb > ka || ks != 0) ? 1u : 0u);
             else
-              tc_mma(d_tmem, operand_desc<A_MN>(a0, ks), operand_desc<B_MN>(b0, ks), idesc, (kb | ks) != 0);
+              tc_mma(d_tmem, operand_desc<A_MN>(a0, ks), operand_desc<B_MN>(b0, ks), idesc,
+                     (kb > ka || ks != 0) ? 1u : 0u);
           }
           // frees the smem slot (of both CTAs) when these MMAs retire
           if constexpr (CG == 2) tc_commit_pair(&empty[stage]); else tc_commit(&empty[stage]);
@@ -372,21 +431,80 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int c_begin = ((warp - 4) / 4) * (BN / 2);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = unit; t < tiles; t += units) {
+    const int ep = threadIdx.x - 128;  // 0..255
+    const int my_cta = unit * CG + static_cast<int>(rank);
+    int t, ka, kb_end;
+    int n_items = 0;
+    while (sch.item(n_items, t, ka, kb_end)) ++n_items;
+    // A unit's last item may be its non-owner stream-K piece, right after an
+    // owner piece that waits on the next-lower unit's non-owner piece.  Drain
+    // the non-owner piece first (it sits in the other TMEM buffer) so every
+    // partial is published without waiting: otherwise the waits chain through
+    // all units and serialise their epilogues.
+    bool swap_last = false;
+    if (n_items >= 2) {
+      sch.item(n_items - 1, t, ka, kb_end);
+      swap_last = kb_end < kt;
+    }
+    for (int k = 0; k < n_items; ++k) {
+      const int it = (swap_last && k >= n_items - 2) ? (2 * n_items - 3 - k) : k;
+      sch.item(it, t, ka, kb_end);
+      acc = it & 1;
+      acc_phase = static_cast<uint32_t>((it >> 1) & 1);
       const int m0 = (t % mt) * BM * CG + static_cast<int>(rank) * BM, n0 = (t / mt) * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
+      // workspace float4 index of (warp, chunk, q4, lane): coalesced per warp
+      auto ws_at = [&](int cta, int ci, int q4) {
+        return sk_ws + (((size_t)cta * kEpiWarps + (warp - 4)) * (BN / 64) + ci) * 256 + q4 * 32 + lane;
+      };
+      if (kb_end < kt) {
+        // non-owner stream-K piece: park the fp32 partial, publish it
 #pragma unroll 1
-      for (int c = c_begin; c < c_begin + BN / 2; c += 32) {
-        float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
-        epilogue_chunk<EPI>(v, row, n0 + c, M, N, ldc, C, R, G);
+        for (int c = c_begin, ci = 0; c < c_begin + BN / 2; c += 32, ++ci) {
+          float v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4)
+            __stcg(ws_at(my_cta, ci, q4), make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]));
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        if (ep == 0) st_release(sk_flags + my_cta, sk_epoch);
+      } else {
+        int first_c = unit, n_c = 0;  // contributing units [first_c, unit)
+        if (ka > 0) {
+          const long long S = (long long)(t - sch.dp) * kt;
+          while (first_c > 0 && sch.sk_bound(first_c) > S) --first_c;
+          n_c = unit - first_c;
+          if (ep < n_c) {
+            const int* f = sk_flags + (first_c + ep) * CG + static_cast<int>(rank);
+            while (ld_acquire(f) != sk_epoch) {
+            }
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        }
+#pragma unroll 1
+        for (int c = c_begin, ci = 0; c < c_begin + BN / 2; c += 32, ++ci) {
+          float v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+          for (int u = 0; u < n_c; ++u) {  // fixed order: deterministic sums
+            const int cta = (first_c + u) * CG + static_cast<int>(rank);
+#pragma unroll
+            for (int q4 = 0; q4 < 8; ++q4) {
+              const float4 p = __ldcg(ws_at(cta, ci, q4));
+              v[4 * q4] += p.x;
+              v[4 * q4 + 1] += p.y;
+              v[4 * q4 + 2] += p.z;
+              v[4 * q4 + 3] += p.w;
+            }
+          }
+          epilogue_chunk<EPI>(v, row, n0 + c, M, N, ldc, C, R, G);
+        }
       }
       tc_fence_before();
       if constexpr (CG == 2) mbar_arrive_cluster(&tempty[acc], 0); else mbar_arrive(&tempty[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
     }
   }
   tc_fence_before();
@@ -431,6 +549,54 @@ bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Stream-K workspace of one stream: a 128 x BN fp32 partial slot and a
+// readiness flag per CTA; flags carry the launch epoch, so they never need
+// resetting.  One per stream, because launches on one stream are ordered.
+struct SkSlot {
+  float4* ws = nullptr;
+  int* flags = nullptr;
+  int epoch = 0;
+};
+SkSlot* sk_slot(cudaStream_t s) {
+  static std::mutex mu;
+  static std::vector<std::pair<cudaStream_t, SkSlot*>> slots;
+  std::lock_guard<std::mutex> g(mu);
+  for (auto& p : slots)
+    if (p.first == s) return p.second;
+  SkSlot* k = new SkSlot;  // lives for the process (device buffers freed at exit)
+  const size_t ws_bytes = (size_t)num_sms() * BM * 256 * sizeof(float);
+  if (cudaMalloc(&k->ws, ws_bytes) != cudaSuccess || cudaMalloc(&k->flags, num_sms() * sizeof(int)) != cudaSuccess ||
+      cudaMemset(k->flags, 0, num_sms() * sizeof(int)) != cudaSuccess) {
+    delete k;
+    return nullptr;
+  }
+  slots.emplace_back(s, k);
+  return k;
+}
+
+// GS_GEMM_SK=1 enables stream-K tail balancing (read per launch so tests can
+// toggle it).  Off by default: measured at GPT-1.3B shapes it loses 7-12%
+// (partial-tile traffic and owner fix-up outweigh the recovered tail wave).
+int sk_mode() {
+  const char* e = getenv("GS_GEMM_SK");
+  return e ? atoi(e) : 0;
+}
+
+// Number of stream-K tiles for `tiles` output tiles on `units` persistent
+// units with kt k-blocks each: the partial last wave (or a grid with fewer
+// tiles than units) is spread over all units when that recovers > 4% and
+// every unit gets >= 4 k-blocks.
+int sk_tiles(int tiles, int units, int kt) {
+  if (!sk_mode() || units <= 1) return 0;
+  const int rem = tiles % units;
+  if (rem == 0) return 0;
+  const double waves = (double)tiles / units;
+  const double eff = waves / std::ceil(waves);
+  if (eff > 0.96) return 0;
+  if ((long long)rem * kt < 4LL * units) return 0;
+  return rem;
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 cudaError_t launch(const GemmArgs& g, cudaStream_t s) {
   using Cfg = TileCfg<BN, CG>;
@@ -451,8 +617,17 @@ cudaError_t launch(const GemmArgs& g, cudaStream_t s) {
     attr_set = true;
   }
   const int tiles = (g.M / (BM * CG)) * (g.N / BN);
-  int grid = tiles * CG < num_sms() ? tiles * CG : num_sms();
+  const int full_grid = num_sms() / CG * CG;
+  int rem = sk_tiles(tiles, full_grid / CG, g.K / BK);
+  SkSlot* sk = rem ? sk_slot(s) : nullptr;
+  if (!sk) rem = 0;
+  int grid = rem ? full_grid : (tiles * CG < num_sms() ? tiles * CG : num_sms());
   grid = grid / CG * CG;
+  int epoch = 0;
+  if (sk) {
+    if (++sk->epoch <= 0) sk->epoch = 1;
+    epoch = sk->epoch;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -467,7 +642,7 @@ cudaError_t launch(const GemmArgs& g, cudaStream_t s) {
   cfg.numAttrs = 1;
   count_launch();
   return cudaLaunchKernelEx(&cfg, kern, ma, mb, g.M, g.N, g.K, g.C, (const bf16*)g.R, (bf16*)g.G,
-                            g.ldc ? g.ldc : g.N);
+                            g.ldc ? g.ldc : g.N, rem, sk ? sk->ws : nullptr, sk ? sk->flags : nullptr, epoch);
 }
 
 template <int BN, bool A_MN, bool B_MN, int CG>

@@ -68,6 +68,20 @@ for rows_ln in (T, 16 * T):
     ms = timed(lambda: gs.check(lib.gs_layernorm_bwd(1, p(x), p(mean), p(rstd), p(y), p(y), rows_ln, h, 1, None)))
     rows.append(dict(kernel="ln_bwd_acc", rows=rows_ln, ms=ms, gbs=4 * x.numel() * 2 / ms / 1e6))
     del x, y
+# one layer's FwdCompute / RecomputeAndBwd back to back (no executor): GPU ms
+# per call and the host's enqueue ms per call
+out = (C.c_double * 4)()
+gs.check(lib.gs_layer_bench(1, 2, 2048, 2048, 16, 20, out))
+rows.append(dict(kernel="layer_fwd", gpu_ms=out[0], host_enqueue_ms=out[1]))
+rows.append(dict(kernel="layer_recompute_bwd", gpu_ms=out[2], host_enqueue_ms=out[3]))
+# cuBLAS (torch.matmul) on the same GEMM shapes / operand majors, for context
+for name, M, N, K, ak, bk in [("cublas_fwd_qkv", T, 3 * h, h, 1, 1), ("cublas_fwd_fc1", T, 4 * h, h, 1, 1),
+                              ("cublas_fwd_fc2", T, h, 4 * h, 1, 1), ("cublas_dgrad_fc2", T, 4 * h, h, 1, 0),
+                              ("cublas_wgrad_fc1", 4 * h, h, T, 0, 0)]:
+    A = torch.randn(M, K, device=d).bfloat16() if ak else torch.randn(K, M, device=d).bfloat16().t()
+    B = torch.randn(N, K, device=d).bfloat16().t() if bk else torch.randn(K, N, device=d).bfloat16()
+    ms = timed(lambda: A @ B)
+    rows.append(dict(kernel=name, M=M, N=N, K=K, ms=ms, tflops=2 * M * N * K / ms / 1e9))
 # torch reference matmul for context
 A = torch.randn(8192, 8192, device=d).bfloat16()
 B = torch.randn(8192, 8192, device=d).bfloat16()
