@@ -27,6 +27,7 @@ using bf16 = __nv_bfloat16;
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, one per column half
+constexpr int kEpiWarpsCfg = kEpiWarps;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
 
 // CG = 1: one CTA computes a 128 x BN tile.  CG = 2: a CTA pair (cluster of
@@ -39,7 +40,9 @@ template <int BN, int CG = 1> struct TileCfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   // double-buffered accumulator; allocations are powers of two >= 32 columns
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  // epilogue staging for TMA stores: 4 KB per epilogue warp (32 rows x 128 B)
+  static constexpr int kEpiStage = 4096;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiWarpsCfg * kEpiStage + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -234,68 +237,100 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Epilogue of one 32-row x 32-column accumulator chunk of an epilogue warp
+// (thread = row, v = its 32 fp32 columns): fused math in registers, then the
+// warp stages the chunk in shared memory (TMA swizzle layout: 64 B rows with
+// SWIZZLE_64B for bf16, 128 B rows with SWIZZLE_128B for fp32, which makes
+// the row-per-thread 16-byte stores bank-conflict free) and lane 0 issues a
+// TMA store (fp32 accumulate: a TMA reduce-add, no read-back) of full lines.
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const float (&v)[32], int row, int col, int M, int N, int ldc,
-                                               void* C, const bf16* R, bf16* G) {
-  if (row >= M) return;
-  const long long o = (long long)row * ldc + col;
+__device__ __forceinline__ void epilogue_store(const float (&v)[32], int lane, int row, int col, int row0, int ldc,
+                                               const bf16* R, uint8_t* stg, const CUtensorMap* map_c,
+                                               const CUtensorMap* map_g) {
+  const uint32_t sa = smem_u32(stg);
+  // the previous chunk's bulk store must have finished reading the staging
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  __syncwarp();
   if constexpr (EPI == (int)Epi::AccumF32 || EPI == (int)Epi::StoreF32) {
-    float4* c = reinterpret_cast<float4*>((float*)C + o);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-      if (EPI == (int)Epi::AccumF32) {
-        const float4 y = c[q];
-        x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
-      }
-      c[q] = x;
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t a = sa + lane * 128 + ((j ^ (lane & 7)) << 4);
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v[4 * j]), "f"(v[4 * j + 1]),
+                   "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                   : "memory");
     }
   } else {
-  float w[32];
+    float w[32];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) w[i] = v[i];
-  if (EPI == (int)Epi::AddResidual || EPI == (int)Epi::MulGeluGrad) {
-    const uint4* r = reinterpret_cast<const uint4*>(R + o);
+    for (int i = 0; i < 32; ++i) w[i] = v[i];
+    if constexpr (EPI == (int)Epi::AddResidual || EPI == (int)Epi::MulGeluGrad) {
+      const uint4* r = reinterpret_cast<const uint4*>(R + (long long)row * ldc + col);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint4 x = r[q];
-      const uint32_t u[4] = {x.x, x.y, x.z, x.w};
+      for (int q = 0; q < 4; ++q) {
+        const uint4 x = r[q];
+        const uint32_t u[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const __nv_bfloat162 p = *reinterpret_cast<const __nv_bfloat162*>(&u[j]);
-        if (EPI == (int)Epi::AddResidual) {
-          w[8 * q + 2 * j] += __bfloat162float(p.x);
-          w[8 * q + 2 * j + 1] += __bfloat162float(p.y);
-        } else {
-          // round dg to bf16 first: identical to storing dg and running gelu_bwd
-          w[8 * q + 2 * j] = __bfloat162float(__float2bfloat16_rn(w[8 * q + 2 * j])) * gelu_grad_fast(__bfloat162float(p.x));
-          w[8 * q + 2 * j + 1] =
-              __bfloat162float(__float2bfloat16_rn(w[8 * q + 2 * j + 1])) * gelu_grad_fast(__bfloat162float(p.y));
+        for (int k = 0; k < 4; ++k) {
+          const __nv_bfloat162 p = *reinterpret_cast<const __nv_bfloat162*>(&u[k]);
+          if (EPI == (int)Epi::AddResidual) {
+            w[8 * q + 2 * k] += __bfloat162float(p.x);
+            w[8 * q + 2 * k + 1] += __bfloat162float(p.y);
+          } else {
+            // round dg to bf16 first: identical to storing dg and running gelu_bwd
+            w[8 * q + 2 * k] = __bfloat162float(__float2bfloat16_rn(w[8 * q + 2 * k])) * gelu_grad_fast(__bfloat162float(p.x));
+            w[8 * q + 2 * k + 1] =
+                __bfloat162float(__float2bfloat16_rn(w[8 * q + 2 * k + 1])) * gelu_grad_fast(__bfloat162float(p.y));
+          }
         }
       }
     }
-  }
-  uint4* c = reinterpret_cast<uint4*>((bf16*)C + o);
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-    c[q] = make_uint4(pack_bf16(w[8 * q], w[8 * q + 1]), pack_bf16(w[8 * q + 2], w[8 * q + 3]),
-                      pack_bf16(w[8 * q + 4], w[8 * q + 5]), pack_bf16(w[8 * q + 6], w[8 * q + 7]));
-  if (EPI == (int)Epi::StoreGelu) {
-    uint4* g = reinterpret_cast<uint4*>(G + o);
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t a = sa + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pack_bf16(w[8 * j], w[8 * j + 1])),
+                   "r"(pack_bf16(w[8 * j + 2], w[8 * j + 3])), "r"(pack_bf16(w[8 * j + 4], w[8 * j + 5])),
+                   "r"(pack_bf16(w[8 * j + 6], w[8 * j + 7]))
+                   : "memory");
+    }
+    if constexpr (EPI == (int)Epi::StoreGelu) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float r[8];
+      for (int j = 0; j < 4; ++j) {
+        float r[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = gelu_fast(__bfloat162float(__float2bfloat16_rn(w[8 * q + j])));
-      g[q] = make_uint4(pack_bf16(r[0], r[1]), pack_bf16(r[2], r[3]), pack_bf16(r[4], r[5]), pack_bf16(r[6], r[7]));
+        for (int k = 0; k < 8; ++k) r[k] = gelu_fast(__bfloat162float(__float2bfloat16_rn(w[8 * j + k])));
+        const uint32_t a = sa + 2048 + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pack_bf16(r[0], r[1])),
+                     "r"(pack_bf16(r[2], r[3])), "r"(pack_bf16(r[4], r[5])), "r"(pack_bf16(r[6], r[7]))
+                     : "memory");
+      }
     }
   }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
+  __syncwarp();
+  if (lane == 0) {
+    if constexpr (EPI == (int)Epi::AccumF32)
+      asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                       reinterpret_cast<uint64_t>(map_c)),
+                   "r"(sa), "r"(col), "r"(row0)
+                   : "memory");
+    else
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                       reinterpret_cast<uint64_t>(map_c)),
+                   "r"(sa), "r"(col), "r"(row0)
+                   : "memory");
+    if constexpr (EPI == (int)Epi::StoreGelu)
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                       reinterpret_cast<uint64_t>(map_g)),
+                   "r"(sa + 2048), "r"(col), "r"(row0)
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_g, int M,
                    int N, int K, void* C, const bf16* R, bf16* G, int ldc, int sk_rem, float4* __restrict__ sk_ws,
                    int* __restrict__ sk_flags, int sk_epoch) {
   using Cfg = TileCfg<BN, CG>;
@@ -304,7 +339,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + S * Cfg::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint8_t* smem_epi = smem + S * Cfg::kStageBytes;  // 1024-aligned: stage bytes are multiples of 1 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_epi + kEpiWarps * Cfg::kEpiStage);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -433,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     const int ep = threadIdx.x - 128;  // 0..255
     const int my_cta = unit * CG + static_cast<int>(rank);
+    uint8_t* stg = smem_epi + (warp - 4) * Cfg::kEpiStage;
     int t, ka, kb_end;
     int n_items = 0;
     while (sch.item(n_items, t, ka, kb_end)) ++n_items;
@@ -500,12 +537,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               v[4 * q4 + 3] += p.w;
             }
           }
-          epilogue_chunk<EPI>(v, row, n0 + c, M, N, ldc, C, R, G);
+          epilogue_store<EPI>(v, lane, row, n0 + c, m0 + q * 32, ldc, R, stg, &map_c, &map_g);
         }
       }
       tc_fence_before();
       if constexpr (CG == 2) mbar_arrive_cluster(&tempty[acc], 0); else mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // staged stores done
   }
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
@@ -597,14 +635,35 @@ int sk_tiles(int tiles, int units, int kt) {
   return rem;
 }
 
+// Output tensor [M][ldc] (N columns used) for the epilogue's 32 x 32 TMA
+// stores: bf16 with 64-byte rows (SWIZZLE_64B) or fp32 with 128-byte rows
+// (SWIZZLE_128B), matching epilogue_store's staging layout.
+bool make_out_map(CUtensorMap* map, const void* base, bool f32, uint64_t N, uint64_t M, uint64_t ldc) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {N, M};
+  const cuuint64_t strides[1] = {ldc * (f32 ? 4 : 2)};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t elem[2] = {1, 1};
+  return fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+            dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 cudaError_t launch(const GemmArgs& g, cudaStream_t s) {
   using Cfg = TileCfg<BN, CG>;
   constexpr int kBNl = BN / CG;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc, mg;
   const bool ok_a = A_MN ? make_map(&ma, g.A, g.M, g.K, BK) : make_map(&ma, g.A, g.K, g.M, BM);
   const bool ok_b = B_MN ? make_map(&mb, g.B, g.N, g.K, BK) : make_map(&mb, g.B, g.K, g.N, kBNl);
   if (!ok_a || !ok_b) return cudaErrorInvalidValue;
+  constexpr bool kF32 = EPI == (int)Epi::AccumF32 || EPI == (int)Epi::StoreF32;
+  const uint64_t ldc = g.ldc ? g.ldc : g.N;
+  if (!make_out_map(&mc, g.C, kF32, g.N, g.M, ldc)) return cudaErrorInvalidValue;
+  mg = mc;
+  if (EPI == (int)Epi::StoreGelu && !make_out_map(&mg, g.G, false, g.N, g.M, ldc)) return cudaErrorInvalidValue;
   auto kern = tc_gemm_kernel<BN, A_MN, B_MN, EPI, CG>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -641,7 +700,7 @@ cudaError_t launch(const GemmArgs& g, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   count_launch();
-  return cudaLaunchKernelEx(&cfg, kern, ma, mb, g.M, g.N, g.K, g.C, (const bf16*)g.R, (bf16*)g.G,
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mg, g.M, g.N, g.K, g.C, (const bf16*)g.R, (bf16*)g.G,
                             g.ldc ? g.ldc : g.N, rem, sk ? sk->ws : nullptr, sk ? sk->flags : nullptr, epoch);
 }
 
