@@ -542,6 +542,54 @@ __global__ void dq_store_kernel(const float* __restrict__ dq, bf16* __restrict__
   }
 }
 
+// Vectorised backward prologue / epilogue of the tcgen05 path (h % 8 == 0,
+// head_dim 128): D = rowsum(dO * O) per (bh, query) with 16 lanes per row
+// (8 bf16 each, 16-byte loads) and L2 = lse * log2(e); the same pass zeroes
+// the fp32 dQ accumulator the kernel reduce-adds into (no separate memset).
+__global__ void fa_prep_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout, const float* __restrict__ lse,
+                               float* __restrict__ D, float* __restrict__ L2, float* __restrict__ dq, int b, int s,
+                               int h, int H) {
+  const long long rows = (long long)b * H * s;
+  const int sub = threadIdx.x & 15;
+  for (long long gr = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 4; gr < rows;
+       gr += ((long long)gridDim.x * blockDim.x) >> 4) {
+    const int bh = (int)(gr / s), t = (int)(gr % s), bi = bh / H, j = bh % H;
+    const long long off = ((long long)bi * s + t) * h + j * 128 + sub * 8;
+    const uint4 a = *reinterpret_cast<const uint4*>(o + off);
+    const uint4 g = *reinterpret_cast<const uint4*>(dout + off);
+    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* pg = reinterpret_cast<const __nv_bfloat162*>(&g);
+    float acc = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 fa = __bfloat1622float2(pa[k]), fg = __bfloat1622float2(pg[k]);
+      acc += fa.x * fg.x + fa.y * fg.y;
+    }
+#pragma unroll
+    for (int m = 8; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if (sub == 0) {
+      D[gr] = acc;
+      L2[gr] = lse[gr] * 1.4426950408889634f;  // log2-domain lse for the SFU exp2
+    }
+    float4* z = reinterpret_cast<float4*>(dq + off);
+    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// dQ fp32 [b*s][h] -> bf16 q-columns of dqkv [b*s][3h], 8 columns per thread.
+__global__ void dq_store_vec_kernel(const float* __restrict__ dq, bf16* __restrict__ dqkv, long long rows, int h) {
+  const long long n8 = rows * h / 8;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i * 8, r = e / h, c = e % h;
+    const float4 x = *reinterpret_cast<const float4*>(dq + e);
+    const float4 y = *reinterpret_cast<const float4*>(dq + e + 4);
+    __nv_bfloat162 v[4] = {__floats2bfloat162_rn(x.x, x.y), __floats2bfloat162_rn(x.z, x.w),
+                           __floats2bfloat162_rn(y.x, y.y), __floats2bfloat162_rn(y.z, y.w)};
+    *reinterpret_cast<uint4*>(dqkv + r * 3LL * h + c) = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
 bool fa_ok(DType dt, int s, int h, int H) {
   if (dt != DType::BF16) return false;
   const int d = h / H;
@@ -576,14 +624,22 @@ cudaError_t fa_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16*
   }
   float* dq = static_cast<float*>(work);
   float* D = dq + (size_t)b * s * h;
-  cudaError_t e = cudaMemsetAsync(dq, 0, sizeof(float) * (size_t)b * s * h, st);
-  if (e != cudaSuccess) return e;
+  float* L2 = D + (size_t)b * H * s;
   const long long rows = (long long)b * H * s;
-  count_launch(); fa_dot_kernel<HD><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(o, dout, D, b, s, h, H);
+  cudaError_t e = cudaSuccess;
   if (HD == 128 && attention_tc_supported(DType::BF16, s, h, H)) {
-    e = attention_bwd_tc(qkv, dout, lse, D, dqkv, dq, b, s, h, H, st);
+    count_launch();
+    fa_prep_kernel<<<grid_for(rows * 16, 256), 256, 0, st>>>(o, dout, lse, D, L2, dq, b, s, h, H);
+    e = attention_bwd_tc(qkv, dout, lse, L2, D, dqkv, dq, b, s, h, H, st);
     if (e != cudaSuccess) return e;
-  } else {
+    count_launch();
+    dq_store_vec_kernel<<<grid_for((long long)b * s * h / 8, 256), 256, 0, st>>>(dq, dqkv, (long long)b * s, h);
+    return cudaGetLastError();
+  }
+  e = cudaMemsetAsync(dq, 0, sizeof(float) * (size_t)b * s * h, st);
+  if (e != cudaSuccess) return e;
+  count_launch(); fa_dot_kernel<HD><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(o, dout, D, b, s, h, H);
+  {
     const dim3 grid(s / kFaBN, b * H);
     count_launch();
     fa_bwd_kernel<HD><<<grid, 128, bwd_smem<HD>(), st>>>(qkv, dout, lse, D, dqkv, dq, s, h, H, 1.0f / sqrtf((float)HD));
@@ -595,8 +651,8 @@ cudaError_t fa_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16*
 }  // namespace
 
 size_t attention_bwd_workspace(int b, int s, int h, int H) {
-  // fa path: dq fp32 [b*s][h] + D [b*H*s];  simt path: dk|dv fp32 [b*s][2h]
-  const size_t fa = sizeof(float) * ((size_t)b * s * h + (size_t)b * H * s);
+  // fa path: dq fp32 [b*s][h] + D, L2 [b*H*s];  simt path: dk|dv fp32 [b*s][2h]
+  const size_t fa = sizeof(float) * ((size_t)b * s * h + 2 * (size_t)b * H * s);
   const size_t simt = sizeof(float) * (size_t)b * s * 2 * h;
   return fa > simt ? fa : simt;
 }

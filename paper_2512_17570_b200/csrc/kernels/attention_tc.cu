@@ -16,6 +16,7 @@
 // o [b*s][h], lse [b][H][s] natural log of the 1/sqrt(d)-scaled scores.
 #include <cuda.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -116,6 +117,14 @@ __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int ks) {
 constexpr uint32_t idesc(bool b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(128 >> 3) << 17) |
          ((uint32_t)(128 >> 4) << 24);
+}
+
+// SFU 2^x (ex2.approx.ftz: flushes denormal results; libm exp2f adds four
+// range-fix instructions per element around the same MUFU op)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 __device__ __forceinline__ uint32_t pack(float a, float b) {
@@ -459,11 +468,11 @@ __global__ void __launch_bounds__(256, 2)
       // read + write of O.
       const bool bump = mx > m_run + 8.0f;
       const float m_new = bump ? mx : m_run;
-      const float corr = bump ? exp2f(m_run - mx) : 1.0f;
+      const float corr = bump ? ex2(m_run - mx) : 1.0f;
       float rs = 0.0f;
 #pragma unroll
       for (int i = 0; i < kBK2; ++i) {
-        sv[i] = exp2f(sv[i] - m_new);
+        sv[i] = ex2(sv[i] - m_new);
         rs += sv[i];
       }
       l_run = l_run * corr + rs;
@@ -1023,7 +1032,7 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
     fa_bwd_tc3_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_q,
                       const __grid_constant__ CUtensorMap map_do, const __grid_constant__ CUtensorMap map_dq,
                       const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv, int s,
-                      int h, int H, float scale) {
+                      int h, int H, float scale, int dq_mode, long long* __restrict__ tr) {
   extern __shared__ __align__(1024) uint8_t rawb3[];
   FaBwdSmem3& sm = *reinterpret_cast<FaBwdSmem3*>(rawb3);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1033,6 +1042,15 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
   const int k0 = kb * kBK;
   const int qb0 = k0 / kBQb, nq = s / kBQb - qb0;
   const float scale_log2 = scale * 1.4426950408889634f;
+  // GS_ATTN_TRACE diagnostics: clock64 stamps of CTA (0, 0)'s pipeline events
+  // tr[ev * 64 + i]: 0 mma ps_full(i) seen, 1 mma S(i) issued, 2 softmax
+  // s_full(i) seen, 3 softmax math done, 4 softmax P/dS written, 5 drain
+  // dq_full(i) seen, 6 drain dq_empty(i) arrived, 7 producer Q(i) issued
+  long long* trc = (tr && blockIdx.x == 0 && blockIdx.y == 0) ? tr : nullptr;
+#define GS_TR(ev, i)                                             \
+  do {                                                           \
+    if (trc && (i) < 64) trc[(ev) * 64 + (i)] = clock64();       \
+  } while (0)
 
   if (threadIdx.x == 0) {
     bar_init(&sm.kv_full, 1);
@@ -1080,6 +1098,7 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
         }
         bulk_g2s(sm.L[sl], lse + (long long)bh * s + q0, kBQb * 4, &sm.q_full[sl]);
         bulk_g2s(sm.D[sl], Dg + (long long)bh * s + q0, kBQb * 4, &sm.q_full[sl]);
+        GS_TR(7, i);
       }
     }
   } else if (warp == 1) {
@@ -1090,6 +1109,7 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
         const int buf = i & 1, sl = i % kQS;
         bar_wait(&sm.q_full[sl], (i / kQS) & 1);
         bar_wait(&sm.dq_empty[buf], ((i >> 1) & 1) ^ 1);  // dQ^T of block i-2 drained
+        GS_TR(1, i);
         fence_after();
         const uint32_t qa = su32(sm.Q[sl]), oa = su32(sm.dO[sl]);
         const uint32_t t0 = tmem + buf * 128;
@@ -1105,6 +1125,7 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
       for (int i = 0; i < nq; ++i) {
         const int buf = i & 1, sl = i % kQS;
         bar_wait(&sm.ps_full, i & 1);
+        GS_TR(0, i);
         fence_after();
         // dQ^T(i) = K^T dS^T into the (already read) S^T half of buffer i&1
 #pragma unroll
@@ -1133,23 +1154,37 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
       const int buf = i & 1, sl = i % kQS, q0 = (qb0 + i) * kBQb;
       bar_wait(&sm.q_full[sl], (i / kQS) & 1);  // L, D of this block
       bar_wait(&sm.s_full[buf], (i >> 1) & 1);
+      if (r == 0) GS_TR(2, i);
       fence_after();
       float p[kBQb], ds[kBQb];
+      // only the two query blocks on the diagonal (i < 2) hold masked pairs
+      const bool diag = q0 < k0 + kBK;
 #pragma unroll
       for (int c = 0; c < kBQb / 32; ++c) {
         uint32_t a[32], b[32];
         tld32(tmem + lb + buf * 128 + c * 32, a);
         tld32(tmem + lb + buf * 128 + 64 + c * 32, b);
         tld_wait();
+        if (diag) {
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const int qi = c * 32 + q;
-          float pv = exp2f(__uint_as_float(a[q]) * scale_log2 - sm.L[sl][qi] * 1.4426950408889634f);
-          if (q0 + qi < key) pv = 0.0f;  // causal
-          p[qi] = pv;
-          ds[qi] = pv * (__uint_as_float(b[q]) - sm.D[sl][qi]);
+          for (int q = 0; q < 32; ++q) {
+            const int qi = c * 32 + q;
+            float pv = ex2(fmaf(__uint_as_float(a[q]), scale_log2, -sm.L[sl][qi]));
+            if (q0 + qi < key) pv = 0.0f;  // causal
+            p[qi] = pv;
+            ds[qi] = pv * (__uint_as_float(b[q]) - sm.D[sl][qi]);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const int qi = c * 32 + q;
+            const float pv = ex2(fmaf(__uint_as_float(a[q]), scale_log2, -sm.L[sl][qi]));
+            p[qi] = pv;
+            ds[qi] = pv * (__uint_as_float(b[q]) - sm.D[sl][qi]);
+          }
         }
       }
+      if (r == 0) GS_TR(3, i);
       bar_wait(&sm.pds_empty, (i & 1) ^ 1);  // MMAs of block i-1 done with P^T / dS^T
 #pragma unroll
       for (int pc = 0; pc < 8; ++pc) {
@@ -1163,6 +1198,7 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       fence_before();
       bar_arrive(&sm.ps_full);
+      if (r == 0) GS_TR(4, i);
     }
     bar_wait(&sm.mma_done, 0);
     fence_after();
@@ -1188,6 +1224,7 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
     for (int i = 0; i < nq; ++i) {
       const int buf = i & 1;
       bar_wait(&sm.dq_full[buf], (i >> 1) & 1);
+      if (r == 0) GS_TR(5, i);
       fence_after();
       uint32_t rr[kBQb];
       tld32(tmem + lb + buf * 128, *reinterpret_cast<uint32_t(*)[32]>(rr));
@@ -1195,6 +1232,7 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
       tld_wait();
       fence_before();
       bar_arrive(&sm.dq_empty[buf]);  // TMEM buffer free for S/dP(i+2)
+      if (r == 0) GS_TR(6, i);
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         if (r == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
@@ -1203,7 +1241,7 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
         for (int q = 0; q < kBQb / 2; ++q) sm.dq_stage[q][r] = __uint_as_float(rr[half * (kBQb / 2) + q]) * scale;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync 3, 128;" ::: "memory");
-        if (r == 0) {
+        if (r == 0 && dq_mode == 0) {
           const int q0 = (qb0 + i) * kBQb + half * (kBQb / 2);
           asm volatile(
               "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -1325,7 +1363,8 @@ cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s,
 
 // dqkv: writes the dK / dV columns; dq_acc (fp32 [b*s][h], zeroed by the
 // caller) receives dQ; D = rowsum(dO * O) per (bh, q).
-cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* D, void* dqkv,
+cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* lse2, const float* D,
+                             void* dqkv,
                              float* dq_acc, int b, int s, int h, int H, cudaStream_t st) {
   CUtensorMap mq, mq64, md;
   const cuuint32_t elem[2] = {1, 1};
@@ -1370,8 +1409,32 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
       init3 = true;
     }
     count_launch();
-    fa_bwd_tc3_kernel<<<dim3(b * H, s / kBK), kThreadsBwd2, smem3, st>>>(mq, mq64, md, mdq, lse, D, (bf16*)dqkv, s,
-                                                                          h, H, 1.0f / sqrtf((float)kD));
+    static const int dq_mode = [] {  // GS_ATTN_DQ_EXPERIMENT=1 skips the dQ reduce (timing only, wrong dQ)
+      const char* e = getenv("GS_ATTN_DQ_EXPERIMENT");
+      return e ? atoi(e) : 0;
+    }();
+    static const bool trace = getenv("GS_ATTN_TRACE") != nullptr;
+    long long* tr = nullptr;
+    if (trace) {
+      cudaMalloc(&tr, 8 * 64 * sizeof(long long));
+      cudaMemsetAsync(tr, 0, 8 * 64 * sizeof(long long), st);
+    }
+    // v3 takes the log2-domain lse (lse2 = lse * log2 e, from fa_prep)
+    fa_bwd_tc3_kernel<<<dim3(b * H, s / kBK), kThreadsBwd2, smem3, st>>>(mq, mq64, md, mdq, lse2, D, (bf16*)dqkv, s,
+                                                                          h, H, 1.0f / sqrtf((float)kD), dq_mode, tr);
+    if (trace) {
+      long long hbuf[8 * 64];
+      cudaMemcpyAsync(hbuf, tr, sizeof(hbuf), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      cudaFree(tr);
+      long long t0 = hbuf[7 * 64];
+      fprintf(stderr, "[attn trace] ev: 0 mma_ps_full 1 mma_S_issue 2 sm_s_full 3 sm_math 4 sm_written 5 dq_full 6 dq_empty 7 prod_Q\n");
+      for (int i = 0; i < 32; ++i) {
+        fprintf(stderr, "[attn trace] %2d", i);
+        for (int ev = 0; ev < 8; ++ev) fprintf(stderr, " %7lld", hbuf[ev * 64 + i] ? hbuf[ev * 64 + i] - t0 : -1);
+        fprintf(stderr, "\n");
+      }
+    }
     return cudaGetLastError();
   }
   if (variant == 2) {

@@ -336,6 +336,22 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const T* __res
 }
 
 template <typename T>
+__device__ __forceinline__ void st4(T* p, float a, float b, float c, float d);
+template <>
+__device__ __forceinline__ void st4<float>(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+template <>
+__device__ __forceinline__ void st4<__nv_bfloat16>(__nv_bfloat16* p, float a, float b, float c, float d) {
+  __nv_bfloat162 v[2] = {__floats2bfloat162_rn(a, b), __floats2bfloat162_rn(c, d)};
+  *reinterpret_cast<uint2*>(p) = *reinterpret_cast<const uint2*>(v);
+}
+
+// One row (token) per block: max, sum of exp, then d(CE)/dlogits = (softmax
+// - onehot) * scale.  fp32 logits are read with 16-byte loads when V % 4 == 0
+// (the row stays in L2 between the three passes); SFU exponentials (__expf,
+// relative error ~2^-21) for the sum and the gradient, libm log for the loss.
+template <typename T>
 __global__ void __launch_bounds__(kRowThreads) xent_kernel(const float* __restrict__ logits, T* dlogits,
                                                            const int32_t* __restrict__ tok, int s, int V,
                                                            float scale, double* loss_sum) {
@@ -344,18 +360,35 @@ __global__ void __launch_bounds__(kRowThreads) xent_kernel(const float* __restri
   const int bi = (int)(row / s), t = (int)(row % s);
   const int target = tok[bi * (s + 1) + t + 1];
   const float* lr = logits + row * V;
+  T* dr = dlogits + row * V;
+  const bool vec = (V & 3) == 0;
+  const int V4 = vec ? V / 4 : 0;
+  const float4* l4 = reinterpret_cast<const float4*>(lr);
   float mx = -INFINITY;
-  for (int v = threadIdx.x; v < V; v += kRowThreads) mx = fmaxf(mx, lr[v]);
+  for (int v = threadIdx.x; v < V4; v += kRowThreads) {
+    const float4 x = l4[v];
+    mx = fmaxf(mx, fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
+  }
+  for (int v = 4 * V4 + threadIdx.x; v < V; v += kRowThreads) mx = fmaxf(mx, lr[v]);
   mx = block_max256(mx, red);
   float z = 0.0f;
-  for (int v = threadIdx.x; v < V; v += kRowThreads) z += expf(lr[v] - mx);
+  for (int v = threadIdx.x; v < V4; v += kRowThreads) {
+    const float4 x = l4[v];
+    z += __expf(x.x - mx) + __expf(x.y - mx) + __expf(x.z - mx) + __expf(x.w - mx);
+  }
+  for (int v = 4 * V4 + threadIdx.x; v < V; v += kRowThreads) z += __expf(lr[v] - mx);
   z = block_sum256(z, red);
   const float lse = mx + logf(z);
-  T* dr = dlogits + row * V;
-  for (int v = threadIdx.x; v < V; v += kRowThreads) {
-    const float p = expf(lr[v] - lse);
-    st(dr + v, (p - (v == target ? 1.0f : 0.0f)) * scale);
+  for (int v = threadIdx.x; v < V4; v += kRowThreads) {
+    const float4 x = l4[v];
+    const int e = 4 * v;
+    st4<T>(dr + e, (__expf(x.x - lse) - (e == target ? 1.0f : 0.0f)) * scale,
+           (__expf(x.y - lse) - (e + 1 == target ? 1.0f : 0.0f)) * scale,
+           (__expf(x.z - lse) - (e + 2 == target ? 1.0f : 0.0f)) * scale,
+           (__expf(x.w - lse) - (e + 3 == target ? 1.0f : 0.0f)) * scale);
   }
+  for (int v = 4 * V4 + threadIdx.x; v < V; v += kRowThreads)
+    st(dr + v, (__expf(lr[v] - lse) - (v == target ? 1.0f : 0.0f)) * scale);
   if (threadIdx.x == 0) atomicAdd(loss_sum, (double)(lse - lr[target]));
 }
 

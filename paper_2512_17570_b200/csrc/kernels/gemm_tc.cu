@@ -244,7 +244,7 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // the row-per-thread 16-byte stores bank-conflict free) and lane 0 issues a
 // TMA store (fp32 accumulate: a TMA reduce-add, no read-back) of full lines.
 template <int EPI>
-__device__ __forceinline__ void epilogue_store(const float (&v)[32], int lane, int row, int col, int row0, int ldc,
+__device__ __forceinline__ void epilogue_store(const float (&v)[32], int lane, int row, int col, int row0, int M, int ldc,
                                                const bf16* R, uint8_t* stg, const CUtensorMap* map_c,
                                                const CUtensorMap* map_g) {
   const uint32_t sa = smem_u32(stg);
@@ -264,7 +264,8 @@ __device__ __forceinline__ void epilogue_store(const float (&v)[32], int lane, i
 #pragma unroll
     for (int i = 0; i < 32; ++i) w[i] = v[i];
     if constexpr (EPI == (int)Epi::AddResidual || EPI == (int)Epi::MulGeluGrad) {
-      const uint4* r = reinterpret_cast<const uint4*>(R + (long long)row * ldc + col);
+      // rows past M (half-empty last pair tile) read row 0; the store clips them
+      const uint4* r = reinterpret_cast<const uint4*>(R + (long long)(row < M ? row : 0) * ldc + col);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const uint4 x = r[q];
@@ -347,7 +348,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = M / (BM * CG), nt = N / BN, kt = K / BK;
+  // M % 128 == 0; a CTA pair's last M tile may be half outside M (TMA loads
+  // fill zeros, TMA stores clip, residual loads are guarded)
+  const int mt = (M + BM * CG - 1) / (BM * CG), nt = N / BN, kt = K / BK;
   const int tiles = mt * nt;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;  // CTA within the pair
   const int unit = CG == 2 ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
@@ -537,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               v[4 * q4 + 3] += p.w;
             }
           }
-          epilogue_store<EPI>(v, lane, row, n0 + c, m0 + q * 32, ldc, R, stg, &map_c, &map_g);
+          epilogue_store<EPI>(v, lane, row, n0 + c, m0 + q * 32, M, ldc, R, stg, &map_c, &map_g);
         }
       }
       tc_fence_before();
@@ -675,7 +678,7 @@ cudaError_t launch(const GemmArgs& g, cudaStream_t s) {
     }
     attr_set = true;
   }
-  const int tiles = (g.M / (BM * CG)) * (g.N / BN);
+  const int tiles = ((g.M + BM * CG - 1) / (BM * CG)) * (g.N / BN);
   const int full_grid = num_sms() / CG * CG;
   int rem = sk_tiles(tiles, full_grid / CG, g.K / BK);
   SkSlot* sk = rem ? sk_slot(s) : nullptr;
@@ -753,7 +756,7 @@ cudaError_t gemm_tc(const GemmArgs& g, cudaStream_t s) {
   if (!gemm_tc_supported(g)) return cudaErrorInvalidValue;
   // Pair tiles 256 x 256 whenever N allows (measured: smaller N tiles lose
   // more per-tile efficiency than they win back in wave quantisation).
-  if (pair_mode() && g.M % (2 * BM) == 0) {
+  if (pair_mode()) {  // M % 128 == 0 (supported): a half-empty last pair tile is fine
     if (g.N % 256 == 0) return launch_bn<256, 2>(g, s);
     if (g.N % 192 == 0 && g.b_kmajor) return launch_bn<192, 2>(g, s);
     if (g.N % 128 == 0) return launch_bn<128, 2>(g, s);
