@@ -47,6 +47,9 @@ CONFIGS = {
     # name: (N, h, heads, s, b, vocab, M, split, alpha)
     "gpt1.3b": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2),
     "gpt1.3b-ssd-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 0.0), 0.2),
+    # BASELINE configs[2] shape on this box (196 GB DRAM, 80 GB disk): half of
+    # the optimizer state (75.5 GB) on the NVMe tier, the other half in HBM
+    "gpt13b-nvme": (40, 5120, 40, 2048, 2, 50304, 16, (1.0, 1.0, 0.5), 0.2),
     "tiny": (4, 64, 4, 32, 2, 128, 4, (0.0, 0.0, 0.0), 0.25),
 }
 

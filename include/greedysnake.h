@@ -95,6 +95,26 @@ int64_t gs_plan_overlap_window(const gs_plan* plan);
 /* report_to_json(simulate(plan, machine)).dump()   simulator.hpp:34 */
 int gs_simulate_json(const gs_plan* plan, const gs_machine_spec* machine, char* buf, size_t cap, size_t* len);
 
+/* ---------------------------------------------------------------- planner
+ * offsim::PlannerSolution (planner.hpp:13-22 of the reference) */
+typedef struct gs_planner_solution {
+  int feasible, num_microbatches;
+  double alpha;
+  gs_split split;
+  double t_fwd_stage, t_bwd_stage, iteration_estimate, throughput_estimate;
+} gs_planner_solution;
+/* solve_config(model, machine, M, alpha)              planner.hpp:27-28 */
+int gs_solve_config(const gs_model_spec* model, const gs_machine_spec* machine, int num_microbatches, double alpha,
+                    gs_planner_solution* out);
+/* find_optimal_config(model, machine)                  planner.hpp:33 */
+int gs_find_optimal_config(const gs_model_spec* model, const gs_machine_spec* machine, gs_planner_solution* out);
+/* grid_search_config(model, machine, M, alpha, steps)  planner.hpp:38-40 */
+int gs_grid_search_config(const gs_model_spec* model, const gs_machine_spec* machine, int num_microbatches,
+                          double alpha, int steps, gs_planner_solution* out);
+/* solve_lp(A, b, c) over dense row-major A [m][n]; x[n]  simplex.hpp:17 */
+int gs_solve_lp(int m, int n, const double* A, const double* b, const double* c, int* feasible, int* bounded,
+                double* objective, double* x);
+
 /* ---------------------------------------------------------------- engine */
 typedef struct gs_engine_config {
   gs_model_spec model;     /* low_precision_bytes: 2 = bf16 training, 4 = fp32 parity mode */

@@ -230,4 +230,35 @@ double io_roofline(const ModelSpec& model, const MachineSpec& machine, u64 batch
                    double x_opt = 0.0);
 double compute_roofline(const ModelSpec& model, const MachineSpec& machine);
 
+// -------------------------------------------------------------- simplex
+// (reference API: proj/include/offsim/simplex.hpp)
+struct LpResult {
+  bool feasible = false;
+  bool bounded = true;
+  std::vector<double> x;
+  double objective = 0.0;
+};
+// min c.x  s.t.  A x <= b, x >= 0 (dense two-phase primal simplex, Bland's rule).
+LpResult solve_lp(const std::vector<std::vector<double>>& A, const std::vector<double>& b,
+                  const std::vector<double>& c);
+
+// -------------------------------------------------------------- planner
+// (reference API: proj/include/offsim/planner.hpp; Algorithm 1 of the paper)
+struct PlannerSolution {
+  bool feasible = false;
+  int num_microbatches = 0;
+  double alpha = 0.0;
+  StorageSplit split;
+  double t_fwd_stage = 0.0;  // per layer, all micro-batches
+  double t_bwd_stage = 0.0;
+  double iteration_estimate = 0.0;
+  double throughput_estimate = 0.0;  // samples/s over all GPUs
+};
+PlannerSolution solve_config(const ModelSpec& model, const MachineSpec& machine, int num_microbatches,
+                             double alpha);
+PlannerSolution find_optimal_config(const ModelSpec& model, const MachineSpec& machine);
+PlannerSolution grid_search_config(const ModelSpec& model, const MachineSpec& machine, int num_microbatches,
+                                   double alpha, int steps = 100);
+double whole_model_projection(const PlannerSolution& sol, const ModelSpec& model, const MachineSpec& machine);
+
 }  // namespace offsim

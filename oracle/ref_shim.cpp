@@ -9,6 +9,8 @@
 #include <string>
 
 #include "offsim/json_io.hpp"
+#include "offsim/planner.hpp"
+#include "offsim/simplex.hpp"
 #include "offsim/schedule.hpp"
 #include "offsim/simulator.hpp"
 #include "offsim/traffic.hpp"
@@ -73,6 +75,31 @@ int ref_ledger(int variant, const int* model, int mbs, int extra, const double* 
     else t = single_fb_traffic(model_of(model), mbs, extra != 0, split_of(split));
     for (int l = 0; l < 4; ++l)
       for (int d = 0; d < 5; ++d) out[l * 5 + d] = t.bytes[l][d];
+  });
+}
+// Planner: mode 0 solve_config(M, alpha), 1 find_optimal_config, 2
+// grid_search_config(M, alpha, steps).  out = {feasible, M, alpha, x_ckpt,
+// x_param, x_opt, t_fwd, t_bwd, iteration, throughput}
+int ref_planner(int mode, const int* model, const double* machine, int mbs, double alpha, int steps, double* out) {
+  return guard([&] {
+    PlannerSolution s = mode == 0   ? solve_config(model_of(model), machine_of(machine), mbs, alpha)
+                        : mode == 1 ? find_optimal_config(model_of(model), machine_of(machine))
+                                    : grid_search_config(model_of(model), machine_of(machine), mbs, alpha, steps);
+    const double v[10] = {s.feasible ? 1.0 : 0.0, (double)s.num_microbatches, s.alpha, s.split.x_ckpt,
+                          s.split.x_param, s.split.x_opt, s.t_fwd_stage, s.t_bwd_stage, s.iteration_estimate,
+                          s.throughput_estimate};
+    std::memcpy(out, v, sizeof(v));
+  });
+}
+// solve_lp over a dense row-major A [m x n]: out = {feasible, bounded, objective, x...}
+int ref_solve_lp(int m, int n, const double* A, const double* b, const double* c, double* out) {
+  return guard([&] {
+    std::vector<std::vector<double>> a(static_cast<size_t>(m), std::vector<double>(static_cast<size_t>(n)));
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < n; ++j) a[i][j] = A[i * n + j];
+    LpResult r = solve_lp(a, std::vector<double>(b, b + m), std::vector<double>(c, c + n));
+    out[0] = r.feasible; out[1] = r.bounded; out[2] = r.objective;
+    for (int j = 0; j < n && j < (int)r.x.size(); ++j) out[3 + j] = r.x[j];
   });
 }
 // report_to_json(simulate(plan_from_json(plan), machine)).dump()

@@ -305,6 +305,66 @@ def shard_range(params_per_layer: int, world: int, rank: int) -> tuple:
     return lo, min(params_per_layer, lo + ps)
 
 
+class _PlannerSolution(C.Structure):
+    _fields_ = [("feasible", C.c_int), ("num_microbatches", C.c_int), ("alpha", C.c_double), ("split", _Split),
+                ("t_fwd_stage", C.c_double), ("t_bwd_stage", C.c_double), ("iteration_estimate", C.c_double),
+                ("throughput_estimate", C.c_double)]
+
+
+@dataclass
+class PlannerSolution:
+    """offsim::PlannerSolution (planner.hpp:13-22)."""
+    feasible: bool
+    num_microbatches: int
+    alpha: float
+    split: "StorageSplit"
+    t_fwd_stage: float
+    t_bwd_stage: float
+    iteration_estimate: float
+    throughput_estimate: float
+
+
+def _solution(o: _PlannerSolution) -> PlannerSolution:
+    return PlannerSolution(bool(o.feasible), o.num_microbatches, o.alpha,
+                           StorageSplit(o.split.x_ckpt, o.split.x_param, o.split.x_opt), o.t_fwd_stage,
+                           o.t_bwd_stage, o.iteration_estimate, o.throughput_estimate)
+
+
+def solve_config(model: ModelSpec, machine: MachineSpec, num_microbatches: int, alpha: float) -> PlannerSolution:
+    """The storage-split LP for fixed (M, alpha) (planner.hpp:27-28)."""
+    out = _PlannerSolution()
+    check(lib().gs_solve_config(C.byref(model._c()), C.byref(machine._c()), num_microbatches, C.c_double(alpha),
+                                C.byref(out)))
+    return _solution(out)
+
+
+def find_optimal_config(model: ModelSpec, machine: MachineSpec) -> PlannerSolution:
+    """Algorithm 1's outer search over M and the alpha grid (planner.hpp:33)."""
+    out = _PlannerSolution()
+    check(lib().gs_find_optimal_config(C.byref(model._c()), C.byref(machine._c()), C.byref(out)))
+    return _solution(out)
+
+
+def grid_search_config(model: ModelSpec, machine: MachineSpec, num_microbatches: int, alpha: float,
+                       steps: int = 100) -> PlannerSolution:
+    """Exhaustive split grid, the LP's cross-check (planner.hpp:38-40)."""
+    out = _PlannerSolution()
+    check(lib().gs_grid_search_config(C.byref(model._c()), C.byref(machine._c()), num_microbatches,
+                                      C.c_double(alpha), steps, C.byref(out)))
+    return _solution(out)
+
+
+def solve_lp(A, b, c):
+    """min c.x s.t. A x <= b, x >= 0 (simplex.hpp:17): (feasible, bounded, objective, x)."""
+    m, n = len(A), len(c)
+    flat = (C.c_double * max(1, m * n))(*[v for row in A for v in row])
+    x = (C.c_double * n)()
+    f, bd, obj = C.c_int(), C.c_int(), C.c_double()
+    check(lib().gs_solve_lp(m, n, flat, (C.c_double * max(1, m))(*b), (C.c_double * n)(*c), C.byref(f), C.byref(bd),
+                            C.byref(obj), x))
+    return bool(f.value), bool(bd.value), obj.value, list(x)
+
+
 def simulate(plan: SchedulePlan, machine: MachineSpec) -> dict:
     """report_to_json(offsim::simulate(plan, machine)) (simulator.hpp:34)."""
     n = C.c_size_t()

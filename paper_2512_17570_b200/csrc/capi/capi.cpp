@@ -179,26 +179,76 @@ int gs_horizontal_traffic(const gs_model_spec* model, int mbs, const gs_split* s
   return guarded([&] { ledger_out(offsim::horizontal_traffic(model_of(model), mbs, split_of(split)), ledger); });
 }
 int64_t gs_plan_overlap_window(const gs_plan* plan) { return plan ? offsim::overlap_window(plan->plan) : -1; }
+static offsim::MachineSpec machine_of(const gs_machine_spec* m) {
+  if (!m) throw offsim::ValidationError("machine is NULL");
+  offsim::MachineSpec mc;
+  mc.gpu_mem_bytes = m->gpu_mem_bytes;
+  mc.cpu_usable_dram_bytes = m->cpu_usable_dram_bytes;
+  mc.pcie_h2d_bw = m->pcie_h2d_bw;
+  mc.pcie_d2h_bw = m->pcie_d2h_bw;
+  mc.ssd_read_bw = m->ssd_read_bw;
+  mc.ssd_write_bw = m->ssd_write_bw;
+  mc.fwd_compute_time_per_layer_per_mb = m->fwd_compute_time_per_layer_per_mb;
+  mc.bwd_compute_time_per_layer_per_mb = m->bwd_compute_time_per_layer_per_mb;
+  mc.cpu_step_throughput = m->cpu_step_throughput;
+  mc.fixed_overhead_time = m->fixed_overhead_time;
+  mc.num_gpus = m->num_gpus;
+  mc.gpu_working_set_bytes = m->gpu_working_set_bytes;
+  mc.ssd_duplex = m->ssd_duplex != 0;
+  return mc;
+}
+
 int gs_simulate_json(const gs_plan* plan, const gs_machine_spec* m, char* buf, size_t cap, size_t* len) {
   int rc = GS_OK;
   const int g = guarded([&] {
-    offsim::MachineSpec mc;
-    mc.gpu_mem_bytes = m->gpu_mem_bytes;
-    mc.cpu_usable_dram_bytes = m->cpu_usable_dram_bytes;
-    mc.pcie_h2d_bw = m->pcie_h2d_bw;
-    mc.pcie_d2h_bw = m->pcie_d2h_bw;
-    mc.ssd_read_bw = m->ssd_read_bw;
-    mc.ssd_write_bw = m->ssd_write_bw;
-    mc.fwd_compute_time_per_layer_per_mb = m->fwd_compute_time_per_layer_per_mb;
-    mc.bwd_compute_time_per_layer_per_mb = m->bwd_compute_time_per_layer_per_mb;
-    mc.cpu_step_throughput = m->cpu_step_throughput;
-    mc.fixed_overhead_time = m->fixed_overhead_time;
-    mc.num_gpus = m->num_gpus;
-    mc.gpu_working_set_bytes = m->gpu_working_set_bytes;
-    mc.ssd_duplex = m->ssd_duplex != 0;
-    rc = copy_string(offsim::report_to_json(offsim::simulate(plan->plan, mc)).dump(), buf, cap, len);
+    rc = copy_string(offsim::report_to_json(offsim::simulate(plan->plan, machine_of(m))).dump(), buf, cap, len);
   });
   return g != GS_OK ? g : rc;
+}
+
+static void solution_out(const offsim::PlannerSolution& s, gs_planner_solution* out) {
+  if (!out) throw offsim::ValidationError("planner: NULL output");
+  out->feasible = s.feasible ? 1 : 0;
+  out->num_microbatches = s.num_microbatches;
+  out->alpha = s.alpha;
+  out->split.x_ckpt = s.split.x_ckpt;
+  out->split.x_param = s.split.x_param;
+  out->split.x_opt = s.split.x_opt;
+  out->t_fwd_stage = s.t_fwd_stage;
+  out->t_bwd_stage = s.t_bwd_stage;
+  out->iteration_estimate = s.iteration_estimate;
+  out->throughput_estimate = s.throughput_estimate;
+}
+int gs_solve_config(const gs_model_spec* model, const gs_machine_spec* machine, int num_microbatches, double alpha,
+                    gs_planner_solution* out) {
+  return guarded([&] {
+    solution_out(offsim::solve_config(model_of(model), machine_of(machine), num_microbatches, alpha), out);
+  });
+}
+int gs_find_optimal_config(const gs_model_spec* model, const gs_machine_spec* machine, gs_planner_solution* out) {
+  return guarded([&] { solution_out(offsim::find_optimal_config(model_of(model), machine_of(machine)), out); });
+}
+int gs_grid_search_config(const gs_model_spec* model, const gs_machine_spec* machine, int num_microbatches,
+                          double alpha, int steps, gs_planner_solution* out) {
+  return guarded([&] {
+    solution_out(offsim::grid_search_config(model_of(model), machine_of(machine), num_microbatches, alpha, steps),
+                 out);
+  });
+}
+int gs_solve_lp(int m, int n, const double* A, const double* b, const double* c, int* feasible, int* bounded,
+                double* objective, double* x) {
+  return guarded([&] {
+    if (m < 0 || n < 1 || (m > 0 && (!A || !b)) || !c) throw offsim::ValidationError("solve_lp: bad arguments");
+    std::vector<std::vector<double>> a(static_cast<size_t>(m), std::vector<double>(static_cast<size_t>(n)));
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < n; ++j) a[static_cast<size_t>(i)][static_cast<size_t>(j)] = A[i * n + j];
+    const offsim::LpResult r = offsim::solve_lp(a, std::vector<double>(b, b + m), std::vector<double>(c, c + n));
+    if (feasible) *feasible = r.feasible ? 1 : 0;
+    if (bounded) *bounded = r.bounded ? 1 : 0;
+    if (objective) *objective = r.objective;
+    if (x)
+      for (int j = 0; j < n; ++j) x[j] = j < static_cast<int>(r.x.size()) ? r.x[static_cast<size_t>(j)] : 0.0;
+  });
 }
 
 // ------------------------------------------------------------------ engine

@@ -201,3 +201,27 @@ def ref_simulate_json(plan_json: str, machine) -> str:
 def ref_vertical_plan(g: Geometry, M: int, split=(0, 0, 0), alpha=0.0, lp=4, dp=1) -> dict:
     model = model_array(g.n_layers, g.hidden, g.heads, g.seq, g.mb_size, lp=lp, dp=dp)
     return json.loads(ref_plan_json("vertical", model, M, split, alpha))
+
+
+def ref_planner(mode: str, model, machine, mbs=1, alpha=0.0, steps=100):
+    """Reference planner (oracle/_ref): mode "solve" | "optimal" | "grid";
+    returns (feasible, M, alpha, x_ckpt, x_param, x_opt, t_fwd, t_bwd,
+    iteration, throughput)."""
+    lib = ref()
+    out = (C.c_double * 10)()
+    rc = lib.ref_planner({"solve": 0, "optimal": 1, "grid": 2}[mode], model, (C.c_double * 13)(*machine), mbs,
+                         C.c_double(alpha), steps, out)
+    if rc != 0:
+        raise RuntimeError(f"reference rc={rc}: {lib.ref_last_error().decode()}")
+    return tuple(out)
+
+
+def ref_solve_lp(A, b, c):
+    lib = ref()
+    m, n = len(A), len(c)
+    flat = (C.c_double * max(1, m * n))(*[v for row in A for v in row])
+    out = (C.c_double * (3 + n))()
+    rc = lib.ref_solve_lp(m, n, flat, (C.c_double * max(1, m))(*b), (C.c_double * n)(*c), out)
+    if rc != 0:
+        raise RuntimeError(f"reference rc={rc}: {lib.ref_last_error().decode()}")
+    return bool(out[0]), bool(out[1]), out[2], list(out[3:])
