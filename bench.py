@@ -191,7 +191,7 @@ def run_reference(args):
         times.append(dt)
     t_layer = float(np.mean(times))
     value = toks / (N * t_layer)
-    line = {"impl": "reference", "metric": METRIC,
+    line = {"impl": "reference", "metric": metric(args),
             "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_layer * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
@@ -201,9 +201,16 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def metric(args):
+    if args.config == "gpt1.3b":
+        return METRIC
+    return f"tokens/sec ({args.config} training, vertical schedule + alpha-delayed optimizer step)"
+
+
 def config_dict(args):
     N, h, H, s, b, V, M, split, alpha = CONFIGS[args.config]
     M = args.microbatches or M
+    alpha = args.alpha if args.alpha >= 0 else alpha
     alpha = alpha if args.schedule == "vertical" else 0.0
     return {"workload": f"{args.config}: GPT N={N} h={h} heads={H} s={s} b={b} vocab={V}, {args.schedule} schedule, "
                         f"M={M} micro-batches/iteration, split(x_ckpt,x_param,x_opt)={split}, alpha={alpha}",
@@ -270,6 +277,7 @@ def run_ours(args):
     import oracle_bindings as ob
     N, h, H, s, b, V, M, split, alpha = CONFIGS[args.config]
     M = args.microbatches or M
+    alpha = args.alpha if args.alpha >= 0 else alpha
     model = gs.ModelSpec(N, h, H, s, b, 2, 4, 3, world)  # ZeRO-3 over the ranks
     if args.schedule == "horizontal":
         alpha = 0.0
@@ -340,10 +348,18 @@ def run_ours(args):
     t_comp = flops_iter / (tf_sust * 1e12)
     t_h2d = float(led[0].sum()) / bw["h2d"]
     t_d2h = float(led[1].sum()) / bw["d2h"]
-    t_roof = max(t_comp, t_h2d, t_d2h)
+    t_ssd, nvme = 0.0, None
+    if float(led[2].sum() + led[3].sum()) > 0:
+        # the NVMe tier's own bandwidth (O_DIRECT, 8 x 8 MiB in flight), both
+        # directions concurrent as the SSD_R / SSD_W queues run
+        out = (C.c_double * 3)()
+        gs.check(gs.lib().gs_nvme_probe(os.environ.get("GS_NVME_DIR", "/tmp").encode(), C.c_uint64(4 << 30), out))
+        nvme = {"write_gbs": out[0], "read_gbs": out[1], "concurrent_gbs_per_direction": out[2]}
+        t_ssd = max(float(led[2].sum()), float(led[3].sum())) / (out[2] * 1e9)
+    t_roof = max(t_comp, t_h2d, t_d2h, t_ssd)
     ms_step = dev_ms / K
     other = {k: v for k, v in prof.items() if k != "gemm"}
-    line = {"metric": METRIC,
+    line = {"metric": metric(args),
             "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic tokens (uniform ids), random-init N(0,0.02) weights",
@@ -357,7 +373,8 @@ def run_ours(args):
             "roofline": roof,
             "iteration_roofline": {"t_roof_ms": t_roof * 1e3, "t_measured_ms": ms_step, "frac": t_roof / (ms_step / 1e3),
                                    "t_compute_ms": t_comp * 1e3, "t_pcie_h2d_ms": t_h2d * 1e3,
-                                   "t_pcie_d2h_ms": t_d2h * 1e3, "pcie_h2d_gbs": bw["h2d"] / 1e9,
+                                   "t_pcie_d2h_ms": t_d2h * 1e3, "t_ssd_ms": t_ssd * 1e3, "nvme": nvme,
+                                   "pcie_h2d_gbs": bw["h2d"] / 1e9,
                                    "pcie_d2h_gbs": bw["d2h"] / 1e9, "flops_per_iteration": flops_iter,
                                    "compute_roofline_tokens_s": tokens_per_step / t_comp},
             "offload_gb_per_iteration": {"ledger_h2d": float(led[0].sum()) / 1e9, "ledger_d2h": float(led[1].sum()) / 1e9,
@@ -384,6 +401,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="gpt1.3b", choices=sorted(CONFIGS))
     ap.add_argument("--microbatches", type=int, default=0)
+    ap.add_argument("--alpha", type=float, default=-1.0, help="override the config's delay ratio")
     ap.add_argument("--schedule", default="vertical", choices=["vertical", "horizontal"],
                     help="horizontal = the micro-batch-major ablation baseline (BASELINE configs[1])")
     ap.add_argument("--no-cpu-baseline", action="store_true")

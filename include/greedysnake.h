@@ -209,6 +209,10 @@ int gs_layer_backward(int dtype, int b, int s, int h, int heads, const void* W, 
  * on one stream with preallocated buffers; out = {fwd GPU ms, fwd host enqueue
  * ms, bwd GPU ms, bwd host enqueue ms} per call */
 int gs_layer_bench(int dtype, int b, int s, int h, int heads, int iters, double out[4]);
+/* diagnostics: the NVMe tier's O_DIRECT bandwidth on a scratch file in `dir`
+ * (`bytes` moved per direction): out = {write GB/s, read GB/s, per-direction
+ * GB/s with reads and writes concurrent} */
+int gs_nvme_probe(const char* dir, uint64_t bytes, double out[3]);
 /* number of device kernels launched through this library so far */
 int64_t gs_launch_count(void);
 

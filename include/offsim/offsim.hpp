@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdint>
 #include <map>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -260,5 +261,37 @@ PlannerSolution find_optimal_config(const ModelSpec& model, const MachineSpec& m
 PlannerSolution grid_search_config(const ModelSpec& model, const MachineSpec& machine, int num_microbatches,
                                    double alpha, int steps = 100);
 double whole_model_projection(const PlannerSolution& sol, const ModelSpec& model, const MachineSpec& machine);
+
+// ---------------------------------------------------------------- alloc
+// (reference API: proj/include/offsim/alloc.hpp) grouping of equal pinned
+// buffers into power-of-two requests
+struct AllocRequest {
+  int buffer_count = 0;
+  u64 requested_bytes = 0;
+  u64 granted_bytes = 0;
+};
+struct AllocPlan {
+  std::vector<AllocRequest> requests;
+  u64 total_requested = 0;
+  u64 total_granted = 0;
+};
+u64 next_pow2(u64 v);
+AllocPlan plan_alloc(int count, u64 buffer_bytes);
+
+// --------------------------------------------------------------- config
+// (reference API: proj/include/offsim/config.hpp) INI run description with
+// sections [model], [machine], optional [schedule] / [output].
+enum class OutputFormat { Json, Csv };
+struct RunConfig {
+  ModelSpec model;
+  MachineSpec machine;
+  ScheduleKind schedule;
+  int num_microbatches = 1;
+  int batch = 1;                      // SingleFB only
+  std::optional<StorageSplit> split;  // planner fills it when absent
+  OutputFormat format = OutputFormat::Json;
+  std::string out_path;               // empty = stdout
+};
+RunConfig parse_config(const std::string& path);
 
 }  // namespace offsim

@@ -11,9 +11,11 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "greedysnake.h"
+#include "host_tiers.hpp"
 #include "kernels.h"
 #include "layer_ops.hpp"
 #include "offsim/executor.hpp"
@@ -410,6 +412,35 @@ int gs_layer_backward(int dtype, int b, int s, int h, int heads, const void* W, 
   return layer_call(dtype, b, s, h, heads, false, W, x, dy, dx, dW, first, stream);
 }
 int64_t gs_launch_count(void) { return gs::launch_counter_ref(); }
+
+int gs_nvme_probe(const char* dir, uint64_t bytes, double out[3]) {
+  return guarded([&] {
+    if (!out || bytes < (64ull << 20)) throw offsim::ValidationError("nvme_probe: bytes >= 64 MiB and out required");
+    gs::engine::NvmeFile f(dir ? dir : "/tmp", true, 8);
+    const uint64_t half = gs::engine::align_up(bytes / 2, gs::engine::kNvmeAlign);
+    const uint64_t a = f.reserve(half), b2 = f.reserve(half);
+    f.finalize_size();
+    gs::engine::PinnedArena arena;
+    uint8_t* buf = arena.alloc(2 * half);
+    for (uint64_t i = 0; i < 2 * half; i += 4096) buf[i] = static_cast<uint8_t>(i >> 12);
+    using clk = std::chrono::steady_clock;
+    auto secs = [](clk::time_point t0) { return std::chrono::duration<double>(clk::now() - t0).count(); };
+    auto t0 = clk::now();
+    f.write(a, buf, half);
+    f.write(b2, buf + half, half);
+    out[0] = 2.0 * half / secs(t0) / 1e9;  // sequential write GB/s
+    t0 = clk::now();
+    f.read(a, buf, half);
+    f.read(b2, buf + half, half);
+    out[1] = 2.0 * half / secs(t0) / 1e9;  // sequential read GB/s
+    // both directions at once (the SSD_R and SSD_W queues run concurrently)
+    t0 = clk::now();
+    std::thread w([&] { f.write(a, buf, half); });
+    f.read(b2, buf + half, half);
+    w.join();
+    out[2] = half / secs(t0) / 1e9;  // per-direction GB/s when concurrent
+  });
+}
 
 int gs_layer_bench(int dtype, int b, int s, int h, int heads, int iters, double out[4]) {
   return guarded([&] {

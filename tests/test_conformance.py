@@ -10,7 +10,7 @@ from conftest import requires_reference
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SUITES = ["test_model", "test_machine", "test_traffic", "test_schedule", "test_simulator", "test_roofline",
-          "test_json_io", "test_simplex", "test_planner"]
+          "test_json_io", "test_simplex", "test_planner", "test_config", "test_alloc"]
 
 
 @pytest.fixture(scope="module")
