@@ -383,6 +383,8 @@ def run_ours(args):
                                          "extension_d2h": float(rep.extension[1].sum()) / 1e9},
             "ledger_equals_plan": bool(np.array_equal(led, gs.plan_traffic(plan))),
             "kernel_ms_per_step": {k: v[1] * v[3] / max(v[2], 1) / K for k, v in prof.items()},
+            "kernel_ms_note": "1 launch in 16 per class bracketed by CUDA events, extrapolated; event overhead "
+                              "inflates short kernels (LayerNorm ~10 us); device-time shares: profiles/ launch list",
             "losses": rep.losses,
             "model_vs_measured": calib,
             "clocks": clk.summary()}

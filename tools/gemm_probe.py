@@ -36,7 +36,10 @@ T, h = 4096, 2048
 rows = []
 for name, M, N, K, ak, bk, epi in [
         ("fwd_qkv", T, 3 * h, h, 1, 1, 0), ("fwd_fc1", T, 4 * h, h, 1, 1, 3), ("fwd_fc2", T, h, 4 * h, 1, 1, 1),
-        ("dgrad_fc2", T, 4 * h, h, 1, 0, 0), ("wgrad_fc1", 4 * h, h, T, 0, 0, 2), ("sq8192", 8192, 8192, 8192, 1, 1, 0)]:
+        ("dgrad_fc2", T, 4 * h, h, 1, 0, 0), ("wgrad_fc1", 4 * h, h, T, 0, 0, 2), ("sq8192", 8192, 8192, 8192, 1, 1, 0),
+        # GPT-65B layer shapes (h = 8192): QKV, FC2 (K = 4h), FC1 weight gradient
+        ("h8192_qkv", T, 3 * 8192, 8192, 1, 1, 0), ("h8192_fc2", T, 8192, 4 * 8192, 1, 1, 1),
+        ("h8192_wgrad_fc1", 4 * 8192, 8192, T, 0, 0, 2)]:
     A = torch.randn(M * K, device=d).bfloat16()
     B = torch.randn(N * K, device=d).bfloat16()
     Cc = torch.empty(M * N, device=d, dtype=torch.float32 if epi == 2 else torch.bfloat16)
@@ -77,7 +80,8 @@ rows.append(dict(kernel="layer_recompute_bwd", gpu_ms=out[2], host_enqueue_ms=ou
 # cuBLAS (torch.matmul) on the same GEMM shapes / operand majors, for context
 for name, M, N, K, ak, bk in [("cublas_fwd_qkv", T, 3 * h, h, 1, 1), ("cublas_fwd_fc1", T, 4 * h, h, 1, 1),
                               ("cublas_fwd_fc2", T, h, 4 * h, 1, 1), ("cublas_dgrad_fc2", T, 4 * h, h, 1, 0),
-                              ("cublas_wgrad_fc1", 4 * h, h, T, 0, 0)]:
+                              ("cublas_wgrad_fc1", 4 * h, h, T, 0, 0), ("cublas_h8192_qkv", T, 3 * 8192, 8192, 1, 1),
+                              ("cublas_h8192_fc2", T, 8192, 4 * 8192, 1, 1)]:
     A = torch.randn(M, K, device=d).bfloat16() if ak else torch.randn(K, M, device=d).bfloat16().t()
     B = torch.randn(N, K, device=d).bfloat16().t() if bk else torch.randn(K, N, device=d).bfloat16()
     ms = timed(lambda: A @ B)
