@@ -75,6 +75,14 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+// A operand from tensor memory (TS form): A = [128 lanes][K] bf16 pairs
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
 __device__ __forceinline__ void tld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -1280,6 +1288,293 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
   }
 }
 
+// ---------------------------------------------------------- backward v4
+// v3 with P^T kept in tensor memory: the softmax warps tcgen05.st P^T (bf16
+// pairs) over the dP^T half they have just read, and dV += P^T dO runs as a
+// TS-MMA (A operand from TMEM).  That frees the P^T shared-memory tile and,
+// with a 16-query dQ staging tile, pays for a 4-slot Q / dO ring, so the
+// ~2k-cycle TMA round trip of block i+4 overlaps two block periods.
+// v3 description (unchanged parts):
+// Same math; the MMA issue order and buffering are arranged so that neither
+// the Q/dO loads nor the dQ drain sit on the tensor pipe's critical path:
+//   per block i the MMA warp issues dQ^T(i) first (commit dq_full), then
+//   dV(i), dK(i) (commit q_empty / pds_empty), then S^T/dP^T(i+2).  The drain
+//   of dQ^T(i) overlaps dV/dK(i); the softmax of block i+1 overlaps
+//   dQ/dV/dK(i); the single P^T/dS^T buffer is rewritten while S/dP(i+2)
+//   run; Q/dO/L/D use a 3-slot ring so block i+2's loads start one block
+//   earlier than in v2.  dQ^T leaves through a 32-query fp32 staging half.
+//   TMEM: [0,128)/[128,256) S^T|dP^T of block i&1 (dQ^T(i) overwrites the
+//   S^T half after the softmax read it), [256,384) dV, [384,512) dK.
+constexpr int kQS4 = 4;  // Q / dO ring depth
+constexpr int kDqRows4 = kBQb / 4;  // dQ staging rows
+struct FaBwdSmem4 {
+  uint8_t K[kTile], V[kTile];
+  uint8_t Q[kQS4][kHalf], dO[kQS4][kHalf];
+  uint8_t dST[kPT];
+  float dq_stage[kDqRows4][kD];
+  float L[kQS4][kBQb], D[kQS4][kBQb];
+  uint64_t kv_full, q_full[kQS4], q_empty[kQS4], s_full[2], ps_full, pds_empty, dq_full[2], dq_empty[2], mma_done;
+  uint32_t tmem;
+};
+
+__global__ void __launch_bounds__(kThreadsBwd2, 1)
+    fa_bwd_tc4_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_q,
+                      const __grid_constant__ CUtensorMap map_do, const __grid_constant__ CUtensorMap map_dq,
+                      const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv, int s,
+                      int h, int H, float scale, int dq_mode, long long* __restrict__ tr) {
+  extern __shared__ __align__(1024) uint8_t rawb4[];
+  FaBwdSmem4& sm = *reinterpret_cast<FaBwdSmem4*>(rawb4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.y;  // grid (b*H, s/128): key block 0 (most query blocks) first
+  const int bh = blockIdx.x, bi = bh / H, j = bh % H;
+  const int row0 = bi * s;
+  const int k0 = kb * kBK;
+  const int qb0 = k0 / kBQb, nq = s / kBQb - qb0;
+  const float scale_log2 = scale * 1.4426950408889634f;
+  // GS_ATTN_TRACE diagnostics: clock64 stamps of CTA (0, 0)'s pipeline events
+  // tr[ev * 64 + i]: 0 mma ps_full(i) seen, 1 mma S(i) issued, 2 softmax
+  // s_full(i) seen, 3 softmax math done, 4 softmax P/dS written, 5 drain
+  // dq_full(i) seen, 6 drain dq_empty(i) arrived, 7 producer Q(i) issued
+  long long* trc = (tr && blockIdx.x == 0 && blockIdx.y == 0) ? tr : nullptr;
+#define GS_TR4(ev, i)                                            \
+  do {                                                           \
+    if (trc && (i) < 64) trc[(ev) * 64 + (i)] = clock64();       \
+  } while (0)
+
+  if (threadIdx.x == 0) {
+    bar_init(&sm.kv_full, 1);
+    for (int i = 0; i < kQS4; ++i) {
+      bar_init(&sm.q_full[i], 1);
+      bar_init(&sm.q_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&sm.s_full[i], 1);
+      bar_init(&sm.dq_full[i], 1);
+      bar_init(&sm.dq_empty[i], 128);
+    }
+    bar_init(&sm.ps_full, 128);
+    bar_init(&sm.pds_empty, 1);
+    bar_init(&sm.mma_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = sm.tmem;
+  constexpr uint32_t kDV = 256, kDK = 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_do)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_q)) : "memory");
+      bar_expect(&sm.kv_full, 2 * kTile);
+      for (int c = 0; c < 2; ++c) {
+        tma2d(sm.K + c * 16384, &map_qkv, &sm.kv_full, h + j * kD + 64 * c, row0 + k0);
+        tma2d(sm.V + c * 16384, &map_qkv, &sm.kv_full, 2 * h + j * kD + 64 * c, row0 + k0);
+      }
+      for (int i = 0; i < nq; ++i) {
+        const int sl = i % kQS4, q0 = (qb0 + i) * kBQb;
+        bar_wait(&sm.q_empty[sl], ((i / kQS4) & 1) ^ 1);
+        bar_expect(&sm.q_full[sl], 2 * kHalf + 2 * kBQb * 4);
+        for (int c = 0; c < 2; ++c) {
+          tma2d(sm.Q[sl] + c * 8192, &map_q, &sm.q_full[sl], j * kD + 64 * c, row0 + q0);
+          tma2d(sm.dO[sl] + c * 8192, &map_do, &sm.q_full[sl], j * kD + 64 * c, row0 + q0);
+        }
+        bulk_g2s(sm.L[sl], lse + (long long)bh * s + q0, kBQb * 4, &sm.q_full[sl]);
+        bulk_g2s(sm.D[sl], Dg + (long long)bh * s + q0, kBQb * 4, &sm.q_full[sl]);
+        GS_TR4(7, i);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t ka = su32(sm.K), va = su32(sm.V), da = su32(sm.dST);
+      bar_wait(&sm.kv_full, 0);
+      auto issue_s = [&](int i) {  // S^T, dP^T of block i into TMEM buffer i&1
+        const int buf = i & 1, sl = i % kQS4;
+        bar_wait(&sm.q_full[sl], (i / kQS4) & 1);
+        bar_wait(&sm.dq_empty[buf], ((i >> 1) & 1) ^ 1);  // dQ^T of block i-2 drained
+        GS_TR4(1, i);
+        fence_after();
+        const uint32_t qa = su32(sm.Q[sl]), oa = su32(sm.dO[sl]);
+        const uint32_t t0 = tmem + buf * 128;
+#pragma unroll
+        for (int ks = 0; ks < kD / 16; ++ks) {
+          mma(t0, desc_k(ka, ks, 128), desc_k(qa, ks, 64), idesc2(64, false, false), ks != 0);
+          mma(t0 + 64, desc_k(va, ks, 128), desc_k(oa, ks, 64), idesc2(64, false, false), ks != 0);
+        }
+        commit(&sm.s_full[buf]);
+      };
+      issue_s(0);
+      if (nq > 1) issue_s(1);
+      for (int i = 0; i < nq; ++i) {
+        const int buf = i & 1, sl = i % kQS4;
+        bar_wait(&sm.ps_full, i & 1);
+        GS_TR4(0, i);
+        fence_after();
+        // dQ^T(i) = K^T dS^T into the (already read) S^T half of buffer i&1
+#pragma unroll
+        for (int ks = 0; ks < kBK / 16; ++ks)
+          mma(tmem + buf * 128, desc_mn(ka, ks, 16384), desc_mn(da, ks, 8192), idesc2(64, true, true), ks != 0);
+        commit(&sm.dq_full[buf]);
+        const uint32_t qa = su32(sm.Q[sl]), oa = su32(sm.dO[sl]);
+#pragma unroll
+        for (int ks = 0; ks < kBQb / 16; ++ks) {
+          // A = P^T in TMEM (dP^T half of buffer i&1, 8 columns per 16 queries)
+          mma_ts(tmem + kDV, tmem + buf * 128 + 64 + ks * 8, desc_mn(oa, ks, 8192), idesc2(128, false, true),
+                 (i | ks) != 0);
+          mma(tmem + kDK, desc_k(da, ks, 128), desc_mn(qa, ks, 8192), idesc2(128, false, true), (i | ks) != 0);
+        }
+        commit(&sm.q_empty[sl]);
+        commit(&sm.pds_empty);
+        if (i + 2 < nq) issue_s(i + 2);
+      }
+      commit(&sm.mma_done);
+    }
+  } else if (warp >= 4 && warp < 8) {
+    const int r = (warp - 4) * 32 + lane;  // key row
+    const uint32_t lb = ((uint32_t)((warp & 3) * 32)) << 16;
+    const int key = k0 + r;
+    const uint32_t swz = (uint32_t)(r & 7);
+    const int rowoff = (r >> 3) * 1024 + (r & 7) * 128;
+    for (int i = 0; i < nq; ++i) {
+      const int buf = i & 1, sl = i % kQS4, q0 = (qb0 + i) * kBQb;
+      bar_wait(&sm.q_full[sl], (i / kQS4) & 1);  // L, D of this block
+      bar_wait(&sm.s_full[buf], (i >> 1) & 1);
+      if (r == 0) GS_TR4(2, i);
+      fence_after();
+      float p[kBQb], ds[kBQb];
+      // only the two query blocks on the diagonal (i < 2) hold masked pairs
+      const bool diag = q0 < k0 + kBK;
+#pragma unroll
+      for (int c = 0; c < kBQb / 32; ++c) {
+        uint32_t a[32], b[32];
+        tld32(tmem + lb + buf * 128 + c * 32, a);
+        tld32(tmem + lb + buf * 128 + 64 + c * 32, b);
+        tld_wait();
+        if (diag) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const int qi = c * 32 + q;
+            float pv = ex2(fmaf(__uint_as_float(a[q]), scale_log2, -sm.L[sl][qi]));
+            if (q0 + qi < key) pv = 0.0f;  // causal
+            p[qi] = pv;
+            ds[qi] = pv * (__uint_as_float(b[q]) - sm.D[sl][qi]);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const int qi = c * 32 + q;
+            const float pv = ex2(fmaf(__uint_as_float(a[q]), scale_log2, -sm.L[sl][qi]));
+            p[qi] = pv;
+            ds[qi] = pv * (__uint_as_float(b[q]) - sm.D[sl][qi]);
+          }
+        }
+      }
+      if (r == 0) GS_TR4(3, i);
+      {  // P^T -> TMEM over the consumed dP^T half (lane = key row)
+        uint32_t pk[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) pk[k] = pack(p[2 * k], p[2 * k + 1]);
+        tst32(tmem + lb + buf * 128 + 64, pk);
+      }
+      bar_wait(&sm.pds_empty, (i & 1) ^ 1);  // MMAs of block i-1 done with dS^T
+#pragma unroll
+      for (int pc = 0; pc < 8; ++pc) {
+        const float* w = ds + pc * 8;
+        *reinterpret_cast<uint4*>(sm.dST + rowoff + ((pc ^ swz) << 4)) =
+            make_uint4(pack(w[0], w[1]), pack(w[2], w[3]), pack(w[4], w[5]), pack(w[6], w[7]));
+      }
+      tst_wait();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      fence_before();
+      bar_arrive(&sm.ps_full);
+      if (r == 0) GS_TR4(4, i);
+    }
+    bar_wait(&sm.mma_done, 0);
+    fence_after();
+    bf16* out = dqkv + (long long)(row0 + key) * 3 * h + h + j * kD;
+#pragma unroll
+    for (int c = 0; c < kD / 32; ++c) {
+      uint32_t rr[32];
+      tld32(tmem + lb + kDK + c * 32, rr);
+      tld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack(__uint_as_float(rr[8 * q]) * scale, __uint_as_float(rr[8 * q + 1]) * scale);
+        w.y = pack(__uint_as_float(rr[8 * q + 2]) * scale, __uint_as_float(rr[8 * q + 3]) * scale);
+        w.z = pack(__uint_as_float(rr[8 * q + 4]) * scale, __uint_as_float(rr[8 * q + 5]) * scale);
+        w.w = pack(__uint_as_float(rr[8 * q + 6]) * scale, __uint_as_float(rr[8 * q + 7]) * scale);
+        *reinterpret_cast<uint4*>(out + c * 32 + 8 * q) = w;
+      }
+    }
+  } else if (warp >= 8) {
+    const int r = (warp - 8) * 32 + lane;  // d row of dQ^T; key row for dV
+    const uint32_t lb = ((uint32_t)((warp & 3) * 32)) << 16;
+    for (int i = 0; i < nq; ++i) {
+      const int buf = i & 1;
+      bar_wait(&sm.dq_full[buf], (i >> 1) & 1);
+      if (r == 0) GS_TR4(5, i);
+      fence_after();
+      uint32_t rr[kBQb];
+      tld32(tmem + lb + buf * 128, *reinterpret_cast<uint32_t(*)[32]>(rr));
+      tld32(tmem + lb + buf * 128 + 32, *reinterpret_cast<uint32_t(*)[32]>(rr + 32));
+      tld_wait();
+      fence_before();
+      bar_arrive(&sm.dq_empty[buf]);  // TMEM buffer free for S/dP(i+2)
+      if (r == 0) GS_TR4(6, i);
+#pragma unroll
+      for (int half = 0; half < kBQb / kDqRows4; ++half) {
+        if (r == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < kDqRows4; ++q) sm.dq_stage[q][r] = __uint_as_float(rr[half * kDqRows4 + q]) * scale;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+        if (r == 0 && dq_mode == 0) {
+          const int q0 = (qb0 + i) * kBQb + half * kDqRows4;
+          asm volatile(
+              "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                  reinterpret_cast<uint64_t>(&map_dq)),
+              "r"(su32(&sm.dq_stage[0][0])), "r"(j * kD), "r"(row0 + q0)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    }
+    if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    bar_wait(&sm.mma_done, 0);
+    fence_after();
+    bf16* out = dqkv + (long long)(row0 + k0 + r) * 3 * h + 2 * h + j * kD;
+#pragma unroll
+    for (int c = 0; c < kD / 32; ++c) {
+      uint32_t rr2[32];
+      tld32(tmem + lb + kDV + c * 32, rr2);
+      tld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack(__uint_as_float(rr2[8 * q]), __uint_as_float(rr2[8 * q + 1]));
+        w.y = pack(__uint_as_float(rr2[8 * q + 2]), __uint_as_float(rr2[8 * q + 3]));
+        w.z = pack(__uint_as_float(rr2[8 * q + 4]), __uint_as_float(rr2[8 * q + 5]));
+        w.w = pack(__uint_as_float(rr2[8 * q + 6]), __uint_as_float(rr2[8 * q + 7]));
+        *reinterpret_cast<uint4*>(out + c * 32 + 8 * q) = w;
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1363,6 +1658,30 @@ cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s,
 
 // dqkv: writes the dK / dV columns; dq_acc (fp32 [b*s][h], zeroed by the
 // caller) receives dQ; D = rowsum(dO * O) per (bh, q).
+// GS_ATTN_TRACE=1: clock64 timeline of CTA (0,0) of the backward (stderr)
+static long long* attn_trace_begin(cudaStream_t st) {
+  static const bool on = getenv("GS_ATTN_TRACE") != nullptr;
+  if (!on) return nullptr;
+  long long* tr = nullptr;
+  cudaMalloc(&tr, 8 * 64 * sizeof(long long));
+  cudaMemsetAsync(tr, 0, 8 * 64 * sizeof(long long), st);
+  return tr;
+}
+static void attn_trace_end(long long* tr, cudaStream_t st) {
+  if (!tr) return;
+  long long hbuf[8 * 64];
+  cudaMemcpyAsync(hbuf, tr, sizeof(hbuf), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(tr);
+  const long long t0 = hbuf[7 * 64];
+  fprintf(stderr, "[attn trace] ev: 0 mma_ps_full 1 mma_S_issue 2 sm_s_full 3 sm_math 4 sm_written 5 dq_full 6 dq_empty 7 prod_Q\n");
+  for (int i = 0; i < 32; ++i) {
+    fprintf(stderr, "[attn trace] %2d", i);
+    for (int ev = 0; ev < 8; ++ev) fprintf(stderr, " %7lld", hbuf[ev * 64 + i] ? hbuf[ev * 64 + i] - t0 : -1);
+    fprintf(stderr, "\n");
+  }
+}
+
 cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* lse2, const float* D,
                              void* dqkv,
                              float* dq_acc, int b, int s, int h, int H, cudaStream_t st) {
@@ -1386,19 +1705,34 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  static const int variant = [] {  // GS_ATTN_BWD=1: unpipelined kernel, 2: v2; default 3
+  static const int variant = [] {  // GS_ATTN_BWD=1: unpipelined, 2: v2, 3: v3; default 4
     const char* e = getenv("GS_ATTN_BWD");
-    return e ? atoi(e) : 3;
+    return e ? atoi(e) : 4;
   }();
   CUtensorMap mdq;
   {
     const cuuint64_t dims[2] = {(cuuint64_t)h, (cuuint64_t)b * s};
     const cuuint64_t strides[1] = {(cuuint64_t)h * 4};
-    const cuuint32_t box[2] = {128, (cuuint32_t)(variant == 3 ? kBQb / 2 : kBQb)};
+    const cuuint32_t box[2] = {128, (cuuint32_t)(variant == 4 ? kDqRows4 : variant == 3 ? kBQb / 2 : kBQb)};
     if (encoder()(&mdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq_acc, dims, strides, box, elem,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
+  }
+  if (variant == 4) {
+    const int smem4 = (int)sizeof(FaBwdSmem4);
+    static bool init4 = false;
+    if (!init4) {
+      cudaError_t e = cudaFuncSetAttribute(fa_bwd_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4);
+      if (e != cudaSuccess) return e;
+      init4 = true;
+    }
+    count_launch();
+    long long* tr = attn_trace_begin(st);
+    fa_bwd_tc4_kernel<<<dim3(b * H, s / kBK), kThreadsBwd2, smem4, st>>>(mq, mq64, md, mdq, lse2, D, (bf16*)dqkv, s,
+                                                                          h, H, 1.0f / sqrtf((float)kD), 0, tr);
+    attn_trace_end(tr, st);
+    return cudaGetLastError();
   }
   if (variant == 3) {
     const int smem3 = (int)sizeof(FaBwdSmem3);
@@ -1413,28 +1747,11 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
       const char* e = getenv("GS_ATTN_DQ_EXPERIMENT");
       return e ? atoi(e) : 0;
     }();
-    static const bool trace = getenv("GS_ATTN_TRACE") != nullptr;
-    long long* tr = nullptr;
-    if (trace) {
-      cudaMalloc(&tr, 8 * 64 * sizeof(long long));
-      cudaMemsetAsync(tr, 0, 8 * 64 * sizeof(long long), st);
-    }
+    long long* tr = attn_trace_begin(st);
     // v3 takes the log2-domain lse (lse2 = lse * log2 e, from fa_prep)
     fa_bwd_tc3_kernel<<<dim3(b * H, s / kBK), kThreadsBwd2, smem3, st>>>(mq, mq64, md, mdq, lse2, D, (bf16*)dqkv, s,
                                                                           h, H, 1.0f / sqrtf((float)kD), dq_mode, tr);
-    if (trace) {
-      long long hbuf[8 * 64];
-      cudaMemcpyAsync(hbuf, tr, sizeof(hbuf), cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
-      cudaFree(tr);
-      long long t0 = hbuf[7 * 64];
-      fprintf(stderr, "[attn trace] ev: 0 mma_ps_full 1 mma_S_issue 2 sm_s_full 3 sm_math 4 sm_written 5 dq_full 6 dq_empty 7 prod_Q\n");
-      for (int i = 0; i < 32; ++i) {
-        fprintf(stderr, "[attn trace] %2d", i);
-        for (int ev = 0; ev < 8; ++ev) fprintf(stderr, " %7lld", hbuf[ev * 64 + i] ? hbuf[ev * 64 + i] - t0 : -1);
-        fprintf(stderr, "\n");
-      }
-    }
+    attn_trace_end(tr, st);
     return cudaGetLastError();
   }
   if (variant == 2) {
