@@ -254,8 +254,20 @@ def calibrate_and_simulate(gs, eng, plan, model, tokens, K, dev_ms):
                              gpu_working_set_bytes=1 << 30, ssd_duplex=True)
     sim = gs.simulate(plan, machine)
     measured = dev_ms / K
+    # the planner (Algorithm 1, planner.cpp:72-201) on the same measured
+    # constants: its projection of this configuration, and its own choice
+    pd = plan.as_dict() if len(plan) < 20000 else None
+    here = gs.solve_config(model, machine, pd["microbatches"], pd["alpha"]) if pd else None
+    best = gs.find_optimal_config(model, machine)
+    planner = {"this_config_projection_ms": here.iteration_estimate * 1e3 if here and here.feasible else None,
+               "this_config_lp_split": [here.split.x_ckpt, here.split.x_param, here.split.x_opt] if here else None,
+               "optimal": {"microbatches": best.num_microbatches, "alpha": best.alpha,
+                           "split": [best.split.x_ckpt, best.split.x_param, best.split.x_opt],
+                           "projected_iteration_ms": best.iteration_estimate * 1e3,
+                           "projected_tokens_s": best.throughput_estimate * model.seq_len} if best.feasible else None}
     return {"method": "MachineSpec from this run's executor trace (mean task times, per-link achieved "
                       "bandwidth, Adam elements/s) -> offsim::simulate (proj/src/simulator.cpp:77)",
+            "planner": planner,
             "predicted_iteration_ms": sim["iteration_time"] * 1e3, "measured_iteration_ms": measured,
             "gap": sim["iteration_time"] * 1e3 / measured - 1.0, "bound_class": sim["bound_class"],
             "utilization": sim["utilization"],
@@ -335,8 +347,16 @@ def run_ours(args):
     # dominant kernel: the tcgen05 GEMM (fp32 accumulate, bf16 operands)
     gemm_flops, gemm_ms, gemm_sampled, gemm_all = prof.get("gemm", (0.0, 0.0, 0, 0))
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    # traffic: DRAM bytes per GEMM launch from the committed ncu launch list of
+    # this command (profiles/, dram__bytes_read + write per launch), if present
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "round1_gemm_traffic.json")
+    if args.config == "gpt1.3b" and os.path.exists(tpath):
+        t = json.load(open(tpath))
+        traffic, traffic_src = t.get("gemm_dram_bytes_per_launch"), t.get("source")
     roof = {"bound": "tensor", "achieved": achieved, "peak": tf_sust, "unit": "TFLOP/s",
-            "frac": achieved / tf_sust, "traffic": None, "kernel": "tc_gemm_kernel (tcgen05, all layer GEMMs)",
+            "frac": achieved / tf_sust, "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write)",
+            "traffic_source": traffic_src, "kernel": "tc_gemm_kernel (tcgen05, all layer GEMMs)",
             "launches_timed": gemm_sampled, "launches_total": gemm_all,
             "avg_launch_ms": gemm_ms / max(gemm_sampled, 1), "flops_per_launch": gemm_flops / max(gemm_sampled, 1),
             "method": "CUDA events around 1 in 16 tcgen05 GEMM launches on the compute stream, timed region",

@@ -1,0 +1,20 @@
+#!/bin/bash
+# End-of-round evidence on one B200 (run under gpurun): GPU tests, smoke,
+# both bench arms, the batch / schedule sweep, the executor trace summary, and
+# ncu --set full captures of the top kernels (raw pages exported to CSV).
+out=gpurun_out
+mkdir -p $out
+timeout 900 python -m pytest tests -m gpu -x -q > $out/final_pytest.log 2>&1; echo "rc=$?" >> $out/final_pytest.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $out/final_smoke.log 2>&1; echo "rc=$?" >> $out/final_smoke.log
+timeout 900 python bench.py > $out/final_bench.log 2>&1
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $out/final_bench_ref.log 2>&1
+timeout 300 python tools/gemm_probe.py > $out/final_probe.jsonl 2>&1
+timeout 1500 python tools/sweep.py > $out/final_sweep.jsonl 2> $out/final_sweep.err
+timeout 600 python tools/trace_gaps.py > $out/final_trace_gaps.txt 2>&1
+for k in "tc_gemm_kernel:0:qkv" "tc_gemm_kernel:23:fc1" "fa_fwd_tc2:3:fafwd" "fa_bwd_tc4:3:fabwd"; do
+  IFS=: read -r name skip tag <<< "$k"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$name -s $skip -c 1 \
+    -o $out/final_prof_$tag -f python tools/gemm_probe.py > $out/final_ncu_$tag.log 2>&1
+  ncu -i $out/final_prof_$tag.ncu-rep --page raw --csv > $out/final_raw_$tag.csv 2>/dev/null
+done
+ls -la $out

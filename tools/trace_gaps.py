@@ -45,3 +45,19 @@ for kind in ("fwd", "bwd", "fixed_ops"):
         print(kind, "n", len(d), "mean ms", np.mean(d), "max", np.max(d), "sum", np.sum(d))
 cpu = [r for r in recs if r["resource"] == "cpu_step"]
 print("cpu_step sum ms", sum(r["t_end_ms"] - r["t_start_ms"] for r in cpu))
+# PCIe copy behaviour: per-task achieved rate and the idle time between
+# consecutive copies on each copy stream, forward vs backward phase
+first_bwd = min(r["t_start_ms"] for r in gpu if tasks[r["task"]]["kind"] == "bwd")
+for res in ("pcie_h2d", "pcie_d2h"):
+    rr = sorted([r for r in recs if r["resource"] == res], key=lambda r: r["t_start_ms"])
+    for phase, sel in (("fwd", lambda r: r["t_end_ms"] <= first_bwd), ("bwd", lambda r: r["t_start_ms"] >= first_bwd)):
+        ph = [r for r in rr if sel(r)]
+        if not ph:
+            continue
+        rates = [r["bytes"] / max(1e-9, (r["t_end_ms"] - r["t_start_ms"]) / 1e3) / 1e9 for r in ph if r["bytes"] > (4 << 20)]
+        idle = sum(max(0.0, b["t_start_ms"] - a["t_end_ms"]) for a, b in zip(ph, ph[1:]))
+        span = ph[-1]["t_end_ms"] - ph[0]["t_start_ms"]
+        byts = sum(r["bytes"] for r in ph)
+        print(f"{res} {phase}: {len(ph)} copies, {byts / 1e9:.2f} GB in {span:.1f} ms span "
+              f"({byts / 1e9 / (span / 1e3):.1f} GB/s), idle between copies {idle:.1f} ms, "
+              f"median copy rate {np.median(rates) if rates else 0:.1f} GB/s")
