@@ -50,6 +50,11 @@ CONFIGS = {
     # BASELINE configs[2] shape on this box (196 GB DRAM, 80 GB disk): half of
     # the optimizer state (75.5 GB) on the NVMe tier, the other half in HBM
     "gpt13b-nvme": (40, 5120, 40, 2048, 2, 50304, 16, (1.0, 1.0, 0.5), 0.2),
+    # GPT-65B layer geometry (h = 8192, 64 heads, b = 2) on a 4-layer slice of
+    # the vertical plan (M = 32, BASELINE configs[3] per-rank batch): the full
+    # 80-layer model needs 258 GB of CPU-resident fp32 grads (> this box's
+    # DRAM); per-stage work is per layer, so tokens/s x 4/80 projects it
+    "gpt65b-4layer": (4, 8192, 64, 2048, 2, 50304, 32, (1.0, 1.0, 1.0), 0.2),
     "tiny": (4, 64, 4, 32, 2, 128, 4, (0.0, 0.0, 0.0), 0.25),
 }
 
@@ -408,6 +413,11 @@ def run_ours(args):
             "losses": rep.losses,
             "model_vs_measured": calib,
             "clocks": clk.summary()}
+    if args.config == "gpt65b-4layer":
+        line["projection_80_layers"] = {
+            "tokens_s": value * N / 80.0, "method": "4-layer slice tokens/s x 4/80: every stage's compute and "
+            "transfers are per layer, so an 80-layer iteration takes 20x the slice's (pipeline fill ignored)",
+            "compute_roofline_tokens_s_80_layers": tokens_per_step / (t_comp * 80.0 / N)}
     if not args.no_cpu_baseline:
         dt, toks, threads, desc = cpu_sample(args.config)
         line["cpu_baseline"] = {"value": toks / (N * dt), "unit": "tokens/s", "cores": threads, "kind": "port",
