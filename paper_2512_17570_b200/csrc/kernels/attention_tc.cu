@@ -135,6 +135,23 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA / ALU pipes (FA4-style MUFU offload): x = j + f with
+// j = round(x) (magic-number add), 2^f on [-0.5, 0.5] by a degree-4 minimax
+// polynomial (max relative error 2.7e-6, far below bf16's 2^-9), then j added
+// into the exponent bits.  Valid for x >= -126 (results below flush to ~0).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;  // 1.5 * 2^23: round to nearest integer
+  const float j = t - 12582912.0f;
+  const float f = x - j;
+  float p = 9.5699895e-3f;  // relative-minimax fit on [-0.5, 0.5], |err| < 2.7e-6
+  p = fmaf(p, f, 5.5917580e-2f);
+  p = fmaf(p, f, 2.4024744e-1f);
+  p = fmaf(p, f, 6.9312185e-1f);
+  p = fmaf(p, f, 9.9999930e-1f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
 __device__ __forceinline__ uint32_t pack(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -340,24 +357,29 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
 }
 
 // ------------------------------------------------------------ forward v2
-// 64-key blocks: 112 KB of shared memory and 256 TMEM columns per CTA, so two
-// CTAs share an SM and one CTA's softmax overlaps the other's MMAs.
+// 64-key blocks: 96 KB of shared memory and 256 TMEM columns per CTA, so two
+// CTAs share an SM and one CTA's softmax overlaps the other's MMAs.  P never
+// touches shared memory: the softmax warps tcgen05.st it (bf16 pairs) over
+// the S buffer they have just read, and O += P V is a TS-MMA (A from TMEM).
+// With P double-buffered that way, softmax(kb) no longer waits for PV(kb-1)
+// except to rescale O (rare: lazy rescaling below).
 constexpr int kBK2 = 64;
 constexpr int kKV2 = kBK2 * kD * 2;  // 16 KB
 struct FaSmem2 {
   uint8_t Q[kTile];          // [2 d-chunks][128 rows][128 B]
   uint8_t K[2][kKV2];        // [2 d-chunks][64 rows][128 B]
   uint8_t V[2][kKV2];
-  uint8_t P[kBQ * kBK2 * 2]; // [128 rows][128 B] (64 keys)
   // K and V slots are released separately: K(kb) right after S(kb), so the
   // load of K(kb+2) overlaps softmax(kb) instead of waiting for PV(kb)
-  uint64_t q_full, k_full[2], v_full[2], k_empty[2], v_empty[2], s_full[2], p_full, o_done;
+  uint64_t q_full, k_full[2], v_full[2], k_empty[2], v_empty[2], s_full[2], p_full[2], o_done;
   uint32_t tmem;
 };
 
+template <int POLY>  // POLY: every 4th exponential on the FMA pipes instead of the SFU
 __global__ void __launch_bounds__(256, 2)
     fa_fwd_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
-                      bf16* __restrict__ o, float* __restrict__ lse, int s, int h, int H, float scale_log2) {
+                      bf16* __restrict__ o, float* __restrict__ lse, int s, int h, int H, float scale_log2,
+                      long long* __restrict__ tr) {
   extern __shared__ __align__(1024) uint8_t raw2[];
   FaSmem2& sm = *reinterpret_cast<FaSmem2*>(raw2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -367,6 +389,14 @@ __global__ void __launch_bounds__(256, 2)
   const int bh = blockIdx.x, bi = bh / H, j = bh % H;
   const int row0 = bi * s, q0 = qb * kBQ;
   const int nblk = (q0 + kBQ) / kBK2;  // causal: keys < q0 + 128
+  // GS_ATTN_TRACE: clock64 stamps of CTA (0, 0) (the heaviest tile):
+  // 0 MMA S(kb) issued, 1 MMA P(kb) seen, 2 softmax S(kb) seen, 3 softmax
+  // math done, 4 softmax P(kb) published, 5 producer K(kb), 6 producer V(kb)
+  long long* trc = (tr && blockIdx.x == 0 && blockIdx.y == 0) ? tr : nullptr;
+#define GS_TRF(ev, i)                                       \
+  do {                                                      \
+    if (trc && (i) < 64) trc[(ev) * 64 + (i)] = clock64();  \
+  } while (0)
 
   if (threadIdx.x == 0) {
     bar_init(&sm.q_full, 1);
@@ -376,8 +406,8 @@ __global__ void __launch_bounds__(256, 2)
       bar_init(&sm.k_empty[i], 1);
       bar_init(&sm.v_empty[i], 1);
       bar_init(&sm.s_full[i], 1);
+      bar_init(&sm.p_full[i], 128);
     }
-    bar_init(&sm.p_full, 128);
     bar_init(&sm.o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -402,15 +432,17 @@ __global__ void __launch_bounds__(256, 2)
         bar_expect(&sm.k_full[buf], kKV2);
         for (int c = 0; c < 2; ++c)
           tma2d(sm.K[buf] + c * 8192, &map_kv, &sm.k_full[buf], h + j * kD + 64 * c, row0 + kb * kBK2);
+        GS_TRF(5, kb);
         bar_wait(&sm.v_empty[buf], ((kb >> 1) & 1) ^ 1);
         bar_expect(&sm.v_full[buf], kKV2);
         for (int c = 0; c < 2; ++c)
           tma2d(sm.V[buf] + c * 8192, &map_kv, &sm.v_full[buf], 2 * h + j * kD + 64 * c, row0 + kb * kBK2);
+        GS_TRF(6, kb);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t qa = su32(sm.Q), pa = su32(sm.P);
+      const uint32_t qa = su32(sm.Q);
       bar_wait(&sm.q_full, 0);
       auto issue_s = [&](int kb) {
         const int buf = kb & 1;
@@ -425,19 +457,21 @@ __global__ void __launch_bounds__(256, 2)
               ks != 0);
         commit(&sm.s_full[buf]);
         commit(&sm.k_empty[buf]);
+        GS_TRF(0, kb);
       };
       issue_s(0);
       for (int kb = 0; kb < nblk; ++kb) {
         const int buf = kb & 1;
         if (kb + 1 < nblk) issue_s(kb + 1);
-        bar_wait(&sm.p_full, kb & 1);
+        bar_wait(&sm.p_full[buf], (kb >> 1) & 1);
+        GS_TRF(1, kb);
         bar_wait(&sm.v_full[buf], (kb >> 1) & 1);
         fence_after();
         const uint32_t va = su32(sm.V[buf]);
 #pragma unroll
-        for (int ks = 0; ks < kBK2 / 16; ++ks)
-          mma(tmem + 128, sdesc(pa + ks * 32, 16, 1024), sdesc(va + ks * 2048, 8192, 1024), idesc(true),
-              (kb | ks) != 0);
+        for (int ks = 0; ks < kBK2 / 16; ++ks)  // A = P(kb) in TMEM: 8 columns per 16 keys
+          mma_ts(tmem + 128, tmem + buf * 64 + ks * 8, sdesc(va + ks * 2048, 8192, 1024), idesc(true),
+                 (kb | ks) != 0);
         commit(&sm.o_done);
         commit(&sm.v_empty[buf]);
       }
@@ -447,11 +481,10 @@ __global__ void __launch_bounds__(256, 2)
     const int qrow = q0 + r;
     const uint32_t lane_base = ((uint32_t)((warp - 4) * 32)) << 16;
     float m_run = -INFINITY, l_run = 0.0f;
-    const uint32_t swz = (uint32_t)(r & 7);
-    uint8_t* prow = sm.P + (r >> 3) * 1024 + (r & 7) * 128;
     for (int kb = 0; kb < nblk; ++kb) {
       const int buf = kb & 1;
       bar_wait(&sm.s_full[buf], (kb >> 1) & 1);
+      if (r == 0) GS_TRF(2, kb);
       fence_after();
       float sv[kBK2];
 #pragma unroll
@@ -460,15 +493,18 @@ __global__ void __launch_bounds__(256, 2)
         tld32(tmem + lane_base + buf * 64 + c * 32, rr);
         tld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(rr[i]) * scale_log2;
+        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(rr[i]);  // raw scores
       }
       const bool mask = (kb + 1) * kBK2 > q0;  // blocks crossing the diagonal
-      float mx = m_run;
+      // max over the raw scores (scale > 0 keeps the order); the log2-domain
+      // scale folds into the exponent's FFMA below
+      float mraw = -INFINITY;
 #pragma unroll
       for (int i = 0; i < kBK2; ++i) {
         if (mask && kb * kBK2 + i > qrow) sv[i] = -INFINITY;
-        mx = fmaxf(mx, sv[i]);
+        mraw = fmaxf(mraw, sv[i]);
       }
+      const float mx = fmaxf(m_run, mraw * scale_log2);
       // Lazy rescaling: the running max only moves when the block max exceeds
       // it by more than 2^8 (P <= 256 stays exact in bf16 / fp32); O and l
       // are then consistent with the stale max and the final O / l, lse are
@@ -478,24 +514,25 @@ __global__ void __launch_bounds__(256, 2)
       const float m_new = bump ? mx : m_run;
       const float corr = bump ? ex2(m_run - mx) : 1.0f;
       float rs = 0.0f;
+      const float nm = -m_new;
 #pragma unroll
       for (int i = 0; i < kBK2; ++i) {
-        sv[i] = ex2(sv[i] - m_new);
+        const float x = fmaf(sv[i], scale_log2, nm);
+        sv[i] = (POLY && (i & 3) == 3) ? ex2_poly(x) : ex2(x);
         rs += sv[i];
       }
       l_run = l_run * corr + rs;
       m_run = m_new;
-      if (kb > 0) {  // PV(kb-1) done: P free, O final for the rescale
-        bar_wait(&sm.o_done, (kb - 1) & 1);
-        fence_after();
-      }
+      if (r == 0) GS_TRF(3, kb);
+      {  // P(kb) -> TMEM over the S buffer just read (lane = query row)
+        uint32_t pk[32];
 #pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        const float* v = sv + p * 8;
-        *reinterpret_cast<uint4*>(prow + ((p ^ swz) << 4)) =
-            make_uint4(pack(v[0], v[1]), pack(v[2], v[3]), pack(v[4], v[5]), pack(v[6], v[7]));
+        for (int k = 0; k < 32; ++k) pk[k] = pack(sv[2 * k], sv[2 * k + 1]);
+        tst32(tmem + lane_base + buf * 64, pk);
       }
       if (kb > 0 && __any_sync(0xffffffffu, bump)) {
+        bar_wait(&sm.o_done, (kb - 1) & 1);  // PV(kb-1) done: O final for the rescale
+        fence_after();
 #pragma unroll
         for (int c = 0; c < kD / 32; ++c) {
           uint32_t rr[32];
@@ -505,11 +542,11 @@ __global__ void __launch_bounds__(256, 2)
           for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * corr);
           tst32(tmem + lane_base + 128 + c * 32, rr);
         }
-        tst_wait();
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tst_wait();
       fence_before();
-      bar_arrive(&sm.p_full);
+      bar_arrive(&sm.p_full[buf]);
+      if (r == 0) GS_TRF(4, kb);
     }
     bar_wait(&sm.o_done, (nblk - 1) & 1);
     fence_after();
@@ -1609,6 +1646,33 @@ static int fwd_variant() {  // GS_ATTN_FWD=1: 128-key single-CTA kernel; default
   return v;
 }
 
+// GS_ATTN_TRACE=1: clock64 timeline of CTA (0,0) of the backward (stderr)
+static long long* attn_trace_begin(cudaStream_t st) {
+  static const bool on = getenv("GS_ATTN_TRACE") != nullptr;
+  if (!on) return nullptr;
+  long long* tr = nullptr;
+  cudaMalloc(&tr, 8 * 64 * sizeof(long long));
+  cudaMemsetAsync(tr, 0, 8 * 64 * sizeof(long long), st);
+  return tr;
+}
+static void attn_trace_end(long long* tr, cudaStream_t st,
+                           const char* legend = "0 mma_ps_full 1 mma_S_issue 2 sm_s_full 3 sm_math 4 sm_written "
+                                                "5 dq_full 6 dq_empty 7 prod_Q",
+                           int t0_event = 7) {
+  if (!tr) return;
+  long long hbuf[8 * 64];
+  cudaMemcpyAsync(hbuf, tr, sizeof(hbuf), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(tr);
+  const long long t0 = hbuf[t0_event * 64];
+  fprintf(stderr, "[attn trace] ev: %s\n", legend);
+  for (int i = 0; i < 32; ++i) {
+    fprintf(stderr, "[attn trace] %2d", i);
+    for (int ev = 0; ev < 8; ++ev) fprintf(stderr, " %7lld", hbuf[ev * 64 + i] ? hbuf[ev * 64 + i] - t0 : -1);
+    fprintf(stderr, "\n");
+  }
+}
+
 cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s, int h, int H, cudaStream_t st) {
   if (fwd_variant() == 2) {
     CUtensorMap mq, mkv;
@@ -1623,15 +1687,24 @@ cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s,
         return cudaErrorInvalidValue;
     }
     const int smem = (int)sizeof(FaSmem2);
+    static const int poly = [] {  // GS_ATTN_POLY=1: FMA-pipe exp2 for 1 in 4 elements
+      const char* e = getenv("GS_ATTN_POLY");
+      return e ? atoi(e) : 0;
+    }();
+    auto kern = poly ? fa_fwd_tc2_kernel<1> : fa_fwd_tc2_kernel<0>;
     static bool init2 = false;
     if (!init2) {
-      cudaError_t e = cudaFuncSetAttribute(fa_fwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
+      for (auto k : {fa_fwd_tc2_kernel<0>, fa_fwd_tc2_kernel<1>}) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+      }
       init2 = true;
     }
     count_launch();
-    fa_fwd_tc2_kernel<<<dim3(b * H, s / kBQ), 256, smem, st>>>(mq, mkv, (bf16*)o, lse, s, h, H,
-                                                               1.4426950408889634f / sqrtf((float)kD));
+    long long* tr = attn_trace_begin(st);
+    kern<<<dim3(b * H, s / kBQ), 256, smem, st>>>(mq, mkv, (bf16*)o, lse, s, h, H,
+                                                               1.4426950408889634f / sqrtf((float)kD), tr);
+    attn_trace_end(tr, st, "0 mma_S_issue 1 mma_P_seen 2 sm_S_seen 3 sm_math 4 sm_P_pub 5 prod_K 6 prod_V", 5);
     return cudaGetLastError();
   }
   CUtensorMap map;
@@ -1658,30 +1731,6 @@ cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s,
 
 // dqkv: writes the dK / dV columns; dq_acc (fp32 [b*s][h], zeroed by the
 // caller) receives dQ; D = rowsum(dO * O) per (bh, q).
-// GS_ATTN_TRACE=1: clock64 timeline of CTA (0,0) of the backward (stderr)
-static long long* attn_trace_begin(cudaStream_t st) {
-  static const bool on = getenv("GS_ATTN_TRACE") != nullptr;
-  if (!on) return nullptr;
-  long long* tr = nullptr;
-  cudaMalloc(&tr, 8 * 64 * sizeof(long long));
-  cudaMemsetAsync(tr, 0, 8 * 64 * sizeof(long long), st);
-  return tr;
-}
-static void attn_trace_end(long long* tr, cudaStream_t st) {
-  if (!tr) return;
-  long long hbuf[8 * 64];
-  cudaMemcpyAsync(hbuf, tr, sizeof(hbuf), cudaMemcpyDeviceToHost, st);
-  cudaStreamSynchronize(st);
-  cudaFree(tr);
-  const long long t0 = hbuf[7 * 64];
-  fprintf(stderr, "[attn trace] ev: 0 mma_ps_full 1 mma_S_issue 2 sm_s_full 3 sm_math 4 sm_written 5 dq_full 6 dq_empty 7 prod_Q\n");
-  for (int i = 0; i < 32; ++i) {
-    fprintf(stderr, "[attn trace] %2d", i);
-    for (int ev = 0; ev < 8; ++ev) fprintf(stderr, " %7lld", hbuf[ev * 64 + i] ? hbuf[ev * 64 + i] - t0 : -1);
-    fprintf(stderr, "\n");
-  }
-}
-
 cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* lse2, const float* D,
                              void* dqkv,
                              float* dq_acc, int b, int s, int h, int H, cudaStream_t st) {

@@ -11,10 +11,10 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $out/final_b
 timeout 300 python tools/gemm_probe.py > $out/final_probe.jsonl 2>&1
 timeout 1500 python tools/sweep.py > $out/final_sweep.jsonl 2> $out/final_sweep.err
 timeout 600 python tools/trace_gaps.py > $out/final_trace_gaps.txt 2>&1
-for k in "tc_gemm_kernel:0:qkv" "tc_gemm_kernel:23:fc1" "fa_fwd_tc2:3:fafwd" "fa_bwd_tc4:3:fabwd"; do
-  IFS=: read -r name skip tag <<< "$k"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$name -s $skip -c 1 \
-    -o $out/final_prof_$tag -f python tools/gemm_probe.py > $out/final_ncu_$tag.log 2>&1
+for k in "tc_gemm_kernel:qkv" "tc_gemm_kernel:fc1" "tc_gemm_kernel:wgrad" "fa_fwd_tc2:attn_fwd" "fa_bwd_tc4:attn_bwd"; do
+  IFS=: read -r name tag <<< "$k"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$name -s 2 -c 1 \
+    -o $out/final_prof_$tag -f python tools/ncu_targets.py $tag > $out/final_ncu_$tag.log 2>&1
   ncu -i $out/final_prof_$tag.ncu-rep --page raw --csv > $out/final_raw_$tag.csv 2>/dev/null
 done
 ls -la $out

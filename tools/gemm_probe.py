@@ -34,19 +34,6 @@ def timed(fn, reps=20):
 
 T, h = 4096, 2048
 rows = []
-for name, M, N, K, ak, bk, epi in [
-        ("fwd_qkv", T, 3 * h, h, 1, 1, 0), ("fwd_fc1", T, 4 * h, h, 1, 1, 3), ("fwd_fc2", T, h, 4 * h, 1, 1, 1),
-        ("dgrad_fc2", T, 4 * h, h, 1, 0, 0), ("wgrad_fc1", 4 * h, h, T, 0, 0, 2), ("sq8192", 8192, 8192, 8192, 1, 1, 0),
-        # GPT-65B layer shapes (h = 8192): QKV, FC2 (K = 4h), FC1 weight gradient
-        ("h8192_qkv", T, 3 * 8192, 8192, 1, 1, 0), ("h8192_fc2", T, 8192, 4 * 8192, 1, 1, 1),
-        ("h8192_wgrad_fc1", 4 * 8192, 8192, T, 0, 0, 2)]:
-    A = torch.randn(M * K, device=d).bfloat16()
-    B = torch.randn(N * K, device=d).bfloat16()
-    Cc = torch.empty(M * N, device=d, dtype=torch.float32 if epi == 2 else torch.bfloat16)
-    R = torch.randn(M * N, device=d).bfloat16() if epi == 1 else None
-    G = torch.empty(M * N, device=d, dtype=torch.bfloat16) if epi == 3 else None
-    ms = timed(lambda: gs.check(lib.gs_gemm(1, M, N, K, p(A), ak, p(B), bk, p(Cc), p(R), p(G), epi, None)))
-    rows.append(dict(gemm=name, M=M, N=N, K=K, ms=ms, tflops=2 * M * N * K / ms / 1e9))
 # attention fwd / bwd at b=2, s=2048, h=2048, H=16
 b, s, H = 2, 2048, 16
 qkv = torch.randn(b * s, 3 * h, device=d).bfloat16()
@@ -77,6 +64,21 @@ out = (C.c_double * 4)()
 gs.check(lib.gs_layer_bench(1, 2, 2048, 2048, 16, 20, out))
 rows.append(dict(kernel="layer_fwd", gpu_ms=out[0], host_enqueue_ms=out[1]))
 rows.append(dict(kernel="layer_recompute_bwd", gpu_ms=out[2], host_enqueue_ms=out[3]))
+# GEMMs last: the GPT-65B shapes heat the GPU and would lower the clocks
+# the attention / layer measurements see
+for name, M, N, K, ak, bk, epi in [
+        ("fwd_qkv", T, 3 * h, h, 1, 1, 0), ("fwd_fc1", T, 4 * h, h, 1, 1, 3), ("fwd_fc2", T, h, 4 * h, 1, 1, 1),
+        ("dgrad_fc2", T, 4 * h, h, 1, 0, 0), ("wgrad_fc1", 4 * h, h, T, 0, 0, 2), ("sq8192", 8192, 8192, 8192, 1, 1, 0),
+        # GPT-65B layer shapes (h = 8192): QKV, FC2 (K = 4h), FC1 weight gradient
+        ("h8192_qkv", T, 3 * 8192, 8192, 1, 1, 0), ("h8192_fc2", T, 8192, 4 * 8192, 1, 1, 1),
+        ("h8192_wgrad_fc1", 4 * 8192, 8192, T, 0, 0, 2)]:
+    A = torch.randn(M * K, device=d).bfloat16()
+    B = torch.randn(N * K, device=d).bfloat16()
+    Cc = torch.empty(M * N, device=d, dtype=torch.float32 if epi == 2 else torch.bfloat16)
+    R = torch.randn(M * N, device=d).bfloat16() if epi == 1 else None
+    G = torch.empty(M * N, device=d, dtype=torch.bfloat16) if epi == 3 else None
+    ms = timed(lambda: gs.check(lib.gs_gemm(1, M, N, K, p(A), ak, p(B), bk, p(Cc), p(R), p(G), epi, None)))
+    rows.append(dict(gemm=name, M=M, N=N, K=K, ms=ms, tflops=2 * M * N * K / ms / 1e9))
 # cuBLAS (torch.matmul) on the same GEMM shapes / operand majors, for context
 for name, M, N, K, ak, bk in [("cublas_fwd_qkv", T, 3 * h, h, 1, 1), ("cublas_fwd_fc1", T, 4 * h, h, 1, 1),
                               ("cublas_fwd_fc2", T, h, 4 * h, 1, 1), ("cublas_dgrad_fc2", T, 4 * h, h, 1, 0),
