@@ -134,6 +134,10 @@ bool alloc_workspace(const Dims& d, Workspace& ws) {
   get(&ws.attn_work, attention_bwd_workspace(d.b, d.s, d.h, d.H));
   get(reinterpret_cast<void**>(&ws.logits), sizeof(float) * T * d.V);
   get(&ws.dlogits, T * d.V * eb);
+  if (ok && (cudaStreamCreateWithFlags(&ws.side, cudaStreamNonBlocking) != cudaSuccess ||
+             cudaEventCreateWithFlags(&ws.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+             cudaEventCreateWithFlags(&ws.ev_join, cudaEventDisableTiming) != cudaSuccess))
+    ok = false;
   return ok;
 }
 
@@ -143,6 +147,9 @@ void free_workspace(Workspace& ws) {
                   ws.dlogits};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (ws.side) cudaStreamDestroy(ws.side);
+  if (ws.ev_fork) cudaEventDestroy(ws.ev_fork);
+  if (ws.ev_join) cudaEventDestroy(ws.ev_join);
   ws = Workspace{};
 }
 
@@ -204,23 +211,43 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
   float* dWo = dW + 3 * h2;
   float* dW1 = dW + 4 * h2;
   float* dW2 = dW + 8 * h2;
+  // Weight gradients run on ws.side once their inputs exist (fork), the
+  // data-gradient chain stays on st; every input a wgrad reads is left intact
+  // until this call returns, and the join below orders dW and the workspace
+  // before the next task.  Side GEMMs are profiled on their own stream: they
+  // overlap dgrad work, so their event times (and the roofline built from
+  // them) err on the long side.
+  cudaStream_t sd = ws.side ? ws.side : st;
+  auto fork = [&]() -> cudaError_t {
+    if (sd == st) return cudaSuccess;
+    GS_TRY(cudaEventRecord(ws.ev_fork, st));
+    return cudaStreamWaitEvent(sd, ws.ev_fork, 0);
+  };
   // MLP
-  GS_TRY(mm(d, h, 4 * h, T, dy, false, ws.g, false, dW2, wg, st, lc, nullptr, nullptr, ws.prof));          // dW2 (+)= dy^T g
+  GS_TRY(fork());
+  GS_TRY(mm(d, h, 4 * h, T, dy, false, ws.g, false, dW2, wg, sd, lc, nullptr, nullptr, ws.prof));                                    // dW2 (+)= dy^T g
   // du = (dy W2) * gelu'(u): GELU backward fused into the dgrad epilogue
   GS_TRY(mm(d, T, 4 * h, h, dy, true, w2, false, ws.big, Epi::MulGeluGrad, st, lc, ws.u, nullptr, ws.prof));
-  GS_TRY(mm(d, 4 * h, h, T, ws.big, false, ws.c, false, dW1, wg, st, lc, nullptr, nullptr, ws.prof));       // dW1 (+)= du^T c
+  GS_TRY(fork());
+  GS_TRY(mm(d, 4 * h, h, T, ws.big, false, ws.c, false, dW1, wg, sd, lc, nullptr, nullptr, ws.prof));                                // dW1 (+)= du^T c
   GS_TRY(mm(d, T, h, 4 * h, ws.big, true, w1, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));  // dc = du W1
   GS_PROF(Norm, layernorm_bwd(d.dt, ws.x1, ws.m2, ws.r2, ws.tmp, dy, ws.dx1, T, h, st));  // dx1 = dy + LN2'
   // attention
-  GS_TRY(mm(d, h, h, T, ws.dx1, false, ws.o, false, dWo, wg, st, lc, nullptr, nullptr, ws.prof));           // dWo (+)= dx1^T o
+  GS_TRY(fork());
+  GS_TRY(mm(d, h, h, T, ws.dx1, false, ws.o, false, dWo, wg, sd, lc, nullptr, nullptr, ws.prof));                                    // dWo (+)= dx1^T o
   GS_TRY(mm(d, T, h, h, ws.dx1, true, wo, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));    // do = dx1 Wo
   {
     Scope sc(ws.prof, KernelProfiler::AttnBwd, 5.0 * d.b * d.H * (double)d.s * d.s * (h / d.H), st);
     GS_TRY(attention_bwd(d.dt, ws.qkv, ws.o, ws.lse, ws.tmp, ws.dqkv, ws.attn_work, d.b, d.s, h, d.H, st));
   }
-  GS_TRY(mm(d, 3 * h, h, T, ws.dqkv, false, ws.a, false, dWqkv, wg, st, lc, nullptr, nullptr, ws.prof));    // dWqkv (+)= dqkv^T a
+  GS_TRY(fork());
+  GS_TRY(mm(d, 3 * h, h, T, ws.dqkv, false, ws.a, false, dWqkv, wg, sd, lc, nullptr, nullptr, ws.prof));                             // dWqkv (+)= dqkv^T a
   GS_TRY(mm(d, T, h, 3 * h, ws.dqkv, true, wqkv, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));  // da = dqkv Wqkv
   GS_PROF(Norm, layernorm_bwd(d.dt, x, ws.m1, ws.r1, ws.tmp, ws.dx1, dx, T, h, st));  // dx = dx1 + LN1'
+  if (sd != st) {  // join
+    GS_TRY(cudaEventRecord(ws.ev_join, sd));
+    GS_TRY(cudaStreamWaitEvent(st, ws.ev_join, 0));
+  }
   lc.n += 6;
   return cudaSuccess;
 }

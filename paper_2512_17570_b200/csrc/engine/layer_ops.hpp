@@ -63,6 +63,12 @@ struct Workspace {
   void* dlogits = nullptr;
   void* z = nullptr;
   uint64_t bytes = 0;
+  // Second compute stream for the weight-gradient GEMMs: they are off the
+  // backward's critical path (dgrad -> LN' -> attention' -> ...), so they
+  // run concurrently and fill the dgrad kernels' tail waves and the small
+  // kernels in between; joined back before layer_backward returns.
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // Allocates every buffer of `ws`; returns false on cudaMalloc failure.
