@@ -364,7 +364,9 @@ def run_ours(args):
             "traffic_source": traffic_src, "kernel": "tc_gemm_kernel (tcgen05, all layer GEMMs)",
             "launches_timed": gemm_sampled, "launches_total": gemm_all,
             "avg_launch_ms": gemm_ms / max(gemm_sampled, 1), "flops_per_launch": gemm_flops / max(gemm_sampled, 1),
-            "method": "CUDA events around 1 in 16 tcgen05 GEMM launches on the compute stream, timed region",
+            "method": "CUDA events around 1 in 16 of the forward / recompute tcgen05 GEMM launches (QKV, out-proj, "
+                      "FC1+GELU, FC2+residual, LM head), which run alone on the compute stream; the backward GEMMs "
+                      "overlap each other on two streams and are not timed; timed region",
             "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)"}
     # iteration roofline (north star): max of compute at peak and ledger bytes over measured links
     bw = pcie_bandwidth(torch)

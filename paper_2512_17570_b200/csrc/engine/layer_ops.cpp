@@ -192,6 +192,19 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
   const Epi wg = first ? Epi::StoreF32 : Epi::AccumF32;
   GS_TRY(forward_body(d, W, x, ws, st, lc));  // recompute from the checkpoint
 
+  // Weight gradients run on ws.side once their inputs exist (fork), the
+  // data-gradient chain stays on st; every input a wgrad reads is left intact
+  // until this call returns, and the join below orders dW and the workspace
+  // before the next task.  GEMMs from here on overlap each other, so none is
+  // event-timed (a per-launch duration would not be the kernel's own);
+  // bench.py's GEMM roofline samples the forward / recompute GEMMs, which run
+  // alone on the compute stream.
+  cudaStream_t sd = ws.side ? ws.side : st;
+  auto fork = [&]() -> cudaError_t {
+    if (sd == st) return cudaSuccess;
+    GS_TRY(cudaEventRecord(ws.ev_fork, st));
+    return cudaStreamWaitEvent(sd, ws.ev_fork, 0);
+  };
   const void* dy = dy_in;
   if (head) {
     // y = block output; tied head on LN_f(y); dy = d(CE)/dy
@@ -199,10 +212,11 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
     GS_PROF(Norm, layernorm_fwd(d.dt, ws.y, ws.z, ws.mz, ws.rz, T, h, st));
     GS_TRY(mm(d, T, d.V, h, ws.z, true, head->wte, true, ws.logits, Epi::StoreF32, st, lc, nullptr, nullptr, ws.prof));
     GS_PROF(Other, softmax_xent(ws.logits, ws.dlogits, d.dt, head->tokens, d.b, d.s, d.V, head->scale, head->loss_sum, st));
-    // dwte += dlogits^T z  (M=V, N=h, K=T)
-    GS_TRY(mm(d, d.V, h, T, ws.dlogits, false, ws.z, false, head->dwte, Epi::AccumF32, st, lc, nullptr, nullptr, ws.prof));
+    // dwte += dlogits^T z  (M=V, N=h, K=T), concurrent with dz
+    GS_TRY(fork());
+    GS_TRY(mm(d, d.V, h, T, ws.dlogits, false, ws.z, false, head->dwte, Epi::AccumF32, sd, lc));
     // dz = dlogits . wte   (M=T, N=h, K=V)
-    GS_TRY(mm(d, T, h, d.V, ws.dlogits, true, head->wte, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));
+    GS_TRY(mm(d, T, h, d.V, ws.dlogits, true, head->wte, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, nullptr));
     GS_PROF(Norm, layernorm_bwd(d.dt, ws.y, ws.mz, ws.rz, ws.tmp, nullptr, ws.dy, T, h, st));
     dy = ws.dy;
     lc.n += 3;
@@ -211,38 +225,26 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
   float* dWo = dW + 3 * h2;
   float* dW1 = dW + 4 * h2;
   float* dW2 = dW + 8 * h2;
-  // Weight gradients run on ws.side once their inputs exist (fork), the
-  // data-gradient chain stays on st; every input a wgrad reads is left intact
-  // until this call returns, and the join below orders dW and the workspace
-  // before the next task.  Side GEMMs are profiled on their own stream: they
-  // overlap dgrad work, so their event times (and the roofline built from
-  // them) err on the long side.
-  cudaStream_t sd = ws.side ? ws.side : st;
-  auto fork = [&]() -> cudaError_t {
-    if (sd == st) return cudaSuccess;
-    GS_TRY(cudaEventRecord(ws.ev_fork, st));
-    return cudaStreamWaitEvent(sd, ws.ev_fork, 0);
-  };
   // MLP
   GS_TRY(fork());
-  GS_TRY(mm(d, h, 4 * h, T, dy, false, ws.g, false, dW2, wg, sd, lc, nullptr, nullptr, ws.prof));                                    // dW2 (+)= dy^T g
+  GS_TRY(mm(d, h, 4 * h, T, dy, false, ws.g, false, dW2, wg, sd, lc));                                    // dW2 (+)= dy^T g
   // du = (dy W2) * gelu'(u): GELU backward fused into the dgrad epilogue
-  GS_TRY(mm(d, T, 4 * h, h, dy, true, w2, false, ws.big, Epi::MulGeluGrad, st, lc, ws.u, nullptr, ws.prof));
+  GS_TRY(mm(d, T, 4 * h, h, dy, true, w2, false, ws.big, Epi::MulGeluGrad, st, lc, ws.u, nullptr, nullptr));
   GS_TRY(fork());
-  GS_TRY(mm(d, 4 * h, h, T, ws.big, false, ws.c, false, dW1, wg, sd, lc, nullptr, nullptr, ws.prof));                                // dW1 (+)= du^T c
-  GS_TRY(mm(d, T, h, 4 * h, ws.big, true, w1, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));  // dc = du W1
+  GS_TRY(mm(d, 4 * h, h, T, ws.big, false, ws.c, false, dW1, wg, sd, lc));                                // dW1 (+)= du^T c
+  GS_TRY(mm(d, T, h, 4 * h, ws.big, true, w1, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, nullptr));  // dc = du W1
   GS_PROF(Norm, layernorm_bwd(d.dt, ws.x1, ws.m2, ws.r2, ws.tmp, dy, ws.dx1, T, h, st));  // dx1 = dy + LN2'
   // attention
   GS_TRY(fork());
-  GS_TRY(mm(d, h, h, T, ws.dx1, false, ws.o, false, dWo, wg, sd, lc, nullptr, nullptr, ws.prof));                                    // dWo (+)= dx1^T o
-  GS_TRY(mm(d, T, h, h, ws.dx1, true, wo, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));    // do = dx1 Wo
+  GS_TRY(mm(d, h, h, T, ws.dx1, false, ws.o, false, dWo, wg, sd, lc));                                    // dWo (+)= dx1^T o
+  GS_TRY(mm(d, T, h, h, ws.dx1, true, wo, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, nullptr));    // do = dx1 Wo
   {
     Scope sc(ws.prof, KernelProfiler::AttnBwd, 5.0 * d.b * d.H * (double)d.s * d.s * (h / d.H), st);
     GS_TRY(attention_bwd(d.dt, ws.qkv, ws.o, ws.lse, ws.tmp, ws.dqkv, ws.attn_work, d.b, d.s, h, d.H, st));
   }
   GS_TRY(fork());
-  GS_TRY(mm(d, 3 * h, h, T, ws.dqkv, false, ws.a, false, dWqkv, wg, sd, lc, nullptr, nullptr, ws.prof));                             // dWqkv (+)= dqkv^T a
-  GS_TRY(mm(d, T, h, 3 * h, ws.dqkv, true, wqkv, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, ws.prof));  // da = dqkv Wqkv
+  GS_TRY(mm(d, 3 * h, h, T, ws.dqkv, false, ws.a, false, dWqkv, wg, sd, lc));                             // dWqkv (+)= dqkv^T a
+  GS_TRY(mm(d, T, h, 3 * h, ws.dqkv, true, wqkv, false, ws.tmp, Epi::Store, st, lc, nullptr, nullptr, nullptr));  // da = dqkv Wqkv
   GS_PROF(Norm, layernorm_bwd(d.dt, x, ws.m1, ws.r1, ws.tmp, ws.dx1, dx, T, h, st));  // dx = dx1 + LN1'
   if (sd != st) {  // join
     GS_TRY(cudaEventRecord(ws.ev_join, sd));
