@@ -33,8 +33,6 @@ constexpr int kD = 128;       // head dim
 constexpr int kBQ = 128;      // queries per CTA
 constexpr int kBK = 128;      // keys per block
 constexpr int kTile = kBQ * kD * 2;  // 32 KB: one 128 x 128 bf16 tile
-constexpr int kThreadsFa = 256;      // backward: warp 0 TMA, 1 MMA, 2 TMEM alloc, 4-7 compute
-constexpr int kThreadsFwd = 384;     // forward: warps 4-11 softmax, two per TMEM lane quarter
 
 // ---------------------------------------------------------------- PTX
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -155,205 +153,6 @@ __device__ __forceinline__ float ex2_poly(float x) {
 __device__ __forceinline__ uint32_t pack(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
-}
-
-struct FaSmem {
-  // tiles (1024-aligned): Q, K[2], V[2], P
-  uint8_t tiles[6][kTile];
-  uint64_t q_full, k_full[2], v_full[2], kv_empty[2], s_full[2], p_full, o_done;
-  uint32_t tmem;
-  float rmax[2][2][kBQ];  // [block parity][column half][row] partial row maxima
-  float rsum[2][kBQ];     // [column half][row] partial row sums (end of kernel)
-};
-
-__global__ void __launch_bounds__(kThreadsFwd, 1)
-    fa_fwd_tc_kernel(const __grid_constant__ CUtensorMap map, bf16* __restrict__ o, float* __restrict__ lse, int s,
-                     int h, int H, float scale_log2) {
-  extern __shared__ uint8_t raw[];
-  FaSmem& sm = *reinterpret_cast<FaSmem*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* Qs = sm.tiles[0];
-  uint8_t* Ks[2] = {sm.tiles[1], sm.tiles[2]};
-  uint8_t* Vs[2] = {sm.tiles[3], sm.tiles[4]};
-  uint8_t* Ps = sm.tiles[5];
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qb = gridDim.x - 1 - blockIdx.x;  // heavy tiles first
-  const int bh = blockIdx.y, bi = bh / H, j = bh % H;
-  const int row0 = bi * s;                   // first token row of this sequence
-  const int q0 = qb * kBQ;
-  const int nblk = qb + 1;                   // causal: key blocks 0..qb
-
-  if (threadIdx.x == 0) {
-    bar_init(&sm.q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      bar_init(&sm.k_full[i], 1);
-      bar_init(&sm.v_full[i], 1);
-      bar_init(&sm.kv_empty[i], 1);
-      bar_init(&sm.s_full[i], 1);
-    }
-    bar_init(&sm.p_full, 256);
-    bar_init(&sm.o_done, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = sm.tmem;  // S0: cols 0-127, S1: 128-255, O: 256-383
-
-  if (warp == 0) {
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map)) : "memory");
-      bar_expect(&sm.q_full, kTile);
-      for (int c = 0; c < 2; ++c) tma2d(Qs + c * 16384, &map, &sm.q_full, j * kD + 64 * c, row0 + q0);
-      for (int kb = 0; kb < nblk; ++kb) {
-        const int buf = kb & 1;
-        bar_wait(&sm.kv_empty[buf], ((kb >> 1) & 1) ^ 1);
-        bar_expect(&sm.k_full[buf], kTile);
-        for (int c = 0; c < 2; ++c)
-          tma2d(Ks[buf] + c * 16384, &map, &sm.k_full[buf], h + j * kD + 64 * c, row0 + kb * kBK);
-        bar_expect(&sm.v_full[buf], kTile);
-        for (int c = 0; c < 2; ++c)
-          tma2d(Vs[buf] + c * 16384, &map, &sm.v_full[buf], 2 * h + j * kD + 64 * c, row0 + kb * kBK);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t qa = su32(Qs), pa = su32(Ps);
-      bar_wait(&sm.q_full, 0);
-      auto issue_s = [&](int kb) {
-        const int buf = kb & 1;
-        bar_wait(&sm.k_full[buf], (kb >> 1) & 1);
-        fence_after();
-        const uint32_t ka = su32(Ks[buf]);
-#pragma unroll
-        for (int ks = 0; ks < kD / 16; ++ks)
-          mma(tmem + buf * 128, desc_kmajor(qa, ks), desc_kmajor(ka, ks), idesc(false), ks != 0);
-        commit(&sm.s_full[buf]);
-      };
-      issue_s(0);
-      for (int kb = 0; kb < nblk; ++kb) {
-        const int buf = kb & 1;
-        if (kb + 1 < nblk) issue_s(kb + 1);  // overlaps softmax of block kb
-        bar_wait(&sm.p_full, kb & 1);        // P_kb in smem, O rescaled
-        bar_wait(&sm.v_full[buf], (kb >> 1) & 1);
-        fence_after();
-        const uint32_t va = su32(Vs[buf]);
-#pragma unroll
-        for (int ks = 0; ks < kBK / 16; ++ks)
-          mma(tmem + 256, desc_kmajor(pa, ks), desc_mnmajor(va, ks), idesc(true), (kb | ks) != 0);
-        commit(&sm.o_done);          // P consumed, O updated
-        commit(&sm.kv_empty[buf]);   // K/V slot free
-      }
-    }
-  } else if (warp >= 4) {
-    // ===== softmax: warps 4-7 and 8-11 cover TMEM lane quarters twice; the
-    // first set owns key columns 0-63 (and O columns 0-63), the second 64-127.
-    const int wq = (warp - 4) & 3, half = (warp - 4) >> 2;
-    const int r = wq * 32 + lane;  // query row = TMEM lane
-    const int qrow = q0 + r;
-    const uint32_t lane_base = ((uint32_t)(wq * 32)) << 16;
-    const int c0 = half * 64;      // first key column (and O column) of this thread
-    float m_run = -INFINITY, l_run = 0.0f;
-    const uint32_t swz = (uint32_t)(r & 7);
-    uint8_t* prow = Ps + half * 16384 + (r >> 3) * 1024 + (r & 7) * 128;
-    for (int kb = 0; kb < nblk; ++kb) {
-      const int buf = kb & 1;
-      bar_wait(&sm.s_full[buf], (kb >> 1) & 1);
-      fence_after();
-      float sv[64];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t rr[32];
-        tld32(tmem + lane_base + buf * 128 + c0 + c * 32, rr);
-        tld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(rr[i]) * scale_log2;
-      }
-      const bool diag = kb == qb;
-      float mx = m_run;
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        if (diag && kb * kBK + c0 + i > qrow) sv[i] = -INFINITY;
-        mx = fmaxf(mx, sv[i]);
-      }
-      // row max across the two column halves (double-buffered exchange)
-      sm.rmax[buf][half][r] = mx;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      mx = fmaxf(mx, sm.rmax[buf][half ^ 1][r]);
-      const float corr = exp2f(m_run - mx);
-      float rs = 0.0f;
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        sv[i] = exp2f(sv[i] - mx);
-        rs += sv[i];
-      }
-      l_run = l_run * corr + rs;
-      m_run = mx;
-      // previous PV must be done before P is overwritten and O rescaled
-      if (kb > 0) {
-        bar_wait(&sm.o_done, (kb - 1) & 1);
-        fence_after();
-        // tcgen05.ld/st are warp-collective: rescale when any row of the warp moved
-        if (__any_sync(0xffffffffu, corr != 1.0f)) {
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint32_t rr[32];
-            tld32(tmem + lane_base + 256 + c0 + c * 32, rr);
-            tld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * corr);
-            tst32(tmem + lane_base + 256 + c0 + c * 32, rr);
-          }
-          tst_wait();
-        }
-      }
-      // P row half -> K-major 128B-swizzled chunk `half`: 16-byte piece p
-      // (8 keys) stored at slot p ^ (row % 8)
-#pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        const float* v = sv + p * 8;
-        uint4 w = make_uint4(pack(v[0], v[1]), pack(v[2], v[3]), pack(v[4], v[5]), pack(v[6], v[7]));
-        *reinterpret_cast<uint4*>(prow + ((p ^ swz) << 4)) = w;
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
-      fence_before();
-      bar_arrive(&sm.p_full);
-    }
-    // epilogue: combine the row sums, wait for the last PV, normalise, write
-    sm.rsum[half][r] = l_run;
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    const float l_tot = l_run + sm.rsum[half ^ 1][r];
-    bar_wait(&sm.o_done, (nblk - 1) & 1);
-    fence_after();
-    const float inv = 1.0f / l_tot;
-    bf16* orow = o + (long long)(row0 + qrow) * h + j * kD + c0;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      uint32_t rr[32];
-      tld32(tmem + lane_base + 256 + c0 + c * 32, rr);
-      tld_wait();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 w;
-        w.x = pack(__uint_as_float(rr[8 * q]) * inv, __uint_as_float(rr[8 * q + 1]) * inv);
-        w.y = pack(__uint_as_float(rr[8 * q + 2]) * inv, __uint_as_float(rr[8 * q + 3]) * inv);
-        w.z = pack(__uint_as_float(rr[8 * q + 4]) * inv, __uint_as_float(rr[8 * q + 5]) * inv);
-        w.w = pack(__uint_as_float(rr[8 * q + 6]) * inv, __uint_as_float(rr[8 * q + 7]) * inv);
-        *reinterpret_cast<uint4*>(orow + c * 32 + 8 * q) = w;
-      }
-    }
-    if (half == 0) lse[(long long)bh * s + qrow] = (m_run + log2f(l_tot)) * 0.6931471805599453f;
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  }
 }
 
 // ------------------------------------------------------------ forward v2
@@ -592,15 +391,6 @@ constexpr int kBQb = 64;                      // queries per backward block
 constexpr int kHalf = kBQb * kD * 2;          // 16 KB: 64 x 128 bf16
 constexpr int kPT = kBK * kBQb * 2;           // 16 KB: 128 keys x 64 queries bf16
 
-struct FaBwdSmem {
-  uint8_t K[kTile], V[kTile];
-  uint8_t Q[2][kHalf], dO[2][kHalf];
-  uint8_t PT[kPT], dST[kPT];
-  float L[2][kBQb], D[2][kBQb];
-  float dq_stage[kBQb][kD];  // dQ tile for the TMA reduce-add into dq_acc
-  uint64_t kv_full, q_full[2], q_empty[2], s_full, ps_full, dq_full;
-  uint32_t tmem;
-};
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -623,434 +413,7 @@ constexpr uint32_t idesc2(int n, bool a_mn, bool b_mn) {
          ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
-__global__ void __launch_bounds__(kThreadsFa, 1)
-    fa_bwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_q,
-                     const __grid_constant__ CUtensorMap map_do, const __grid_constant__ CUtensorMap map_dq,
-                     const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv,
-                     float* __restrict__ dq_acc, int s, int h, int H, float scale) {
-  extern __shared__ uint8_t raw[];
-  FaBwdSmem& sm = *reinterpret_cast<FaBwdSmem*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkb = gridDim.x;
-  const int kb = nkb - 1 - blockIdx.x;          // few query blocks last
-  const int bh = blockIdx.y, bi = bh / H, j = bh % H;
-  const int row0 = bi * s;
-  const int k0 = kb * kBK;
-  const int qb0 = k0 / kBQb, nq = s / kBQb - qb0;  // query blocks from the diagonal
-  const float scale_log2 = scale * 1.4426950408889634f;
-
-  if (threadIdx.x == 0) {
-    bar_init(&sm.kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      bar_init(&sm.q_full[i], 1);
-      bar_init(&sm.q_empty[i], 1);
-    }
-    bar_init(&sm.s_full, 1);
-    bar_init(&sm.ps_full, 128);
-    bar_init(&sm.dq_full, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = sm.tmem;
-  constexpr uint32_t kST = 0, kDPT = 64, kDV = 128, kDK = 256, kDQ = 384;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_do)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_q)) : "memory");
-      bar_expect(&sm.kv_full, 2 * kTile);
-      for (int c = 0; c < 2; ++c) {
-        tma2d(sm.K + c * 16384, &map_qkv, &sm.kv_full, h + j * kD + 64 * c, row0 + k0);
-        tma2d(sm.V + c * 16384, &map_qkv, &sm.kv_full, 2 * h + j * kD + 64 * c, row0 + k0);
-      }
-      for (int i = 0; i < nq; ++i) {
-        const int buf = i & 1, q0 = (qb0 + i) * kBQb;
-        bar_wait(&sm.q_empty[buf], ((i >> 1) & 1) ^ 1);
-        bar_expect(&sm.q_full[buf], 2 * kHalf + 2 * kBQb * 4);
-        for (int c = 0; c < 2; ++c) {
-          tma2d(sm.Q[buf] + c * 8192, &map_q, &sm.q_full[buf], j * kD + 64 * c, row0 + q0);
-          tma2d(sm.dO[buf] + c * 8192, &map_do, &sm.q_full[buf], j * kD + 64 * c, row0 + q0);
-        }
-        bulk_g2s(sm.L[buf], lse + (long long)bh * s + q0, kBQb * 4, &sm.q_full[buf]);
-        bulk_g2s(sm.D[buf], Dg + (long long)bh * s + q0, kBQb * 4, &sm.q_full[buf]);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t ka = su32(sm.K), va = su32(sm.V), pa = su32(sm.PT), da = su32(sm.dST);
-      bar_wait(&sm.kv_full, 0);
-      for (int i = 0; i < nq; ++i) {
-        const int buf = i & 1;
-        const uint32_t qa = su32(sm.Q[buf]), oa = su32(sm.dO[buf]);
-        bar_wait(&sm.q_full[buf], (i >> 1) & 1);
-        fence_after();
-        // S^T and dP^T (TMEM of block i-1 was read before ps_full(i-1))
-#pragma unroll
-        for (int ks = 0; ks < kD / 16; ++ks) {
-          mma(tmem + kST, desc_k(ka, ks, 128), desc_k(qa, ks, 64), idesc2(64, false, false), ks != 0);
-          mma(tmem + kDPT, desc_k(va, ks, 128), desc_k(oa, ks, 64), idesc2(64, false, false), ks != 0);
-        }
-        commit(&sm.s_full);
-        bar_wait(&sm.ps_full, i & 1);
-        fence_after();
-#pragma unroll
-        for (int ks = 0; ks < kBQb / 16; ++ks) {
-          mma(tmem + kDV, desc_k(pa, ks, 128), desc_mn(oa, ks, 8192), idesc2(128, false, true), (i | ks) != 0);
-          mma(tmem + kDK, desc_k(da, ks, 128), desc_mn(qa, ks, 8192), idesc2(128, false, true), (i | ks) != 0);
-        }
-#pragma unroll
-        for (int ks = 0; ks < kBK / 16; ++ks)
-          mma(tmem + kDQ, desc_mn(ka, ks, 16384), desc_mn(da, ks, 8192), idesc2(64, true, true), ks != 0);
-        commit(&sm.dq_full);
-        commit(&sm.q_empty[buf]);
-      }
-    }
-  } else if (warp >= 4) {
-    const int r = (warp - 4) * 32 + lane;          // key row (S^T, dP^T, dK, dV) / d lane (dQ^T)
-    const uint32_t lb = ((uint32_t)((warp - 4) * 32)) << 16;
-    const int key = k0 + r;
-    const uint32_t swz = (uint32_t)(r & 7);
-    const int rowoff = (r >> 3) * 1024 + (r & 7) * 128;
-    auto drain_dq = [&](int i) {  // dQ^T of block i -> smem [q][d] -> TMA reduce-add into dq_acc
-      bar_wait(&sm.dq_full, i & 1);
-      fence_after();
-      if (r == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
-      asm volatile("bar.sync 2, 128;" ::: "memory");
-#pragma unroll
-      for (int c = 0; c < kBQb / 32; ++c) {
-        uint32_t rr[32];
-        tld32(tmem + lb + kDQ + c * 32, rr);
-        tld_wait();
-#pragma unroll
-        for (int q = 0; q < 32; ++q) sm.dq_stage[c * 32 + q][r] = __uint_as_float(rr[q]) * scale;
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync 2, 128;" ::: "memory");
-      if (r == 0) {
-        const int q0 = (qb0 + i) * kBQb;
-        asm volatile(
-            "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                reinterpret_cast<uint64_t>(&map_dq)),
-            "r"(su32(&sm.dq_stage[0][0])), "r"(j * kD), "r"(row0 + q0)
-            : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-    };
-    for (int i = 0; i < nq; ++i) {
-      const int buf = i & 1, q0 = (qb0 + i) * kBQb;
-      bar_wait(&sm.q_full[buf], (i >> 1) & 1);  // L, D of this block
-      bar_wait(&sm.s_full, i & 1);
-      fence_after();
-      float p[kBQb], ds[kBQb];
-#pragma unroll
-      for (int c = 0; c < kBQb / 32; ++c) {
-        uint32_t a[32], b[32];
-        tld32(tmem + lb + kST + c * 32, a);
-        tld32(tmem + lb + kDPT + c * 32, b);
-        tld_wait();
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const int qi = c * 32 + q;
-          float pv = exp2f(__uint_as_float(a[q]) * scale_log2 - sm.L[buf][qi] * 1.4426950408889634f);
-          if (q0 + qi < key) pv = 0.0f;  // causal
-          p[qi] = pv;
-          ds[qi] = pv * (__uint_as_float(b[q]) - sm.D[buf][qi]);
-        }
-      }
-      if (i > 0) drain_dq(i - 1);  // also: MMAs of block i-1 finished reading P^T / dS^T
-#pragma unroll
-      for (int pc = 0; pc < 8; ++pc) {
-        const float* v = p + pc * 8;
-        const float* w = ds + pc * 8;
-        *reinterpret_cast<uint4*>(sm.PT + rowoff + ((pc ^ swz) << 4)) =
-            make_uint4(pack(v[0], v[1]), pack(v[2], v[3]), pack(v[4], v[5]), pack(v[6], v[7]));
-        *reinterpret_cast<uint4*>(sm.dST + rowoff + ((pc ^ swz) << 4)) =
-            make_uint4(pack(w[0], w[1]), pack(w[2], w[3]), pack(w[4], w[5]), pack(w[6], w[7]));
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      fence_before();
-      bar_arrive(&sm.ps_full);
-    }
-    drain_dq(nq - 1);  // dq_full of the last block also covers dK / dV
-    if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    bf16* krow = dqkv + (long long)(row0 + key) * 3 * h + h + j * kD;
-#pragma unroll
-    for (int part = 0; part < 2; ++part) {  // 0: dK (scaled), 1: dV
-      bf16* out = krow + part * h;
-      const float f = part == 0 ? scale : 1.0f;
-#pragma unroll
-      for (int c = 0; c < kD / 32; ++c) {
-        uint32_t rr[32];
-        tld32(tmem + lb + (part == 0 ? kDK : kDV) + c * 32, rr);
-        tld_wait();
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 w;
-          w.x = pack(__uint_as_float(rr[8 * q]) * f, __uint_as_float(rr[8 * q + 1]) * f);
-          w.y = pack(__uint_as_float(rr[8 * q + 2]) * f, __uint_as_float(rr[8 * q + 3]) * f);
-          w.z = pack(__uint_as_float(rr[8 * q + 4]) * f, __uint_as_float(rr[8 * q + 5]) * f);
-          w.w = pack(__uint_as_float(rr[8 * q + 6]) * f, __uint_as_float(rr[8 * q + 7]) * f);
-          *reinterpret_cast<uint4*>(out + c * 32 + 8 * q) = w;
-        }
-      }
-    }
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  }
-}
-
-// ---------------------------------------------------------- backward v2
-// Same math as fa_bwd_tc_kernel, pipelined across query blocks:
-//   TMEM  [0,128)/[128,256): S^T | dP^T of block i&1 (64 + 64 columns); after
-//         the softmax warps have read them, dQ^T of that block overwrites the
-//         S^T half.  [256,384) dV, [384,512) dK.
-//   SMEM  P^T / dS^T double-buffered, so the MMA warp issues S/dP(i+1) before
-//         dV/dK/dQ(i) and the softmax of block i+1 overlaps those MMAs.
-//   warps 0 TMA, 1 MMA, 2 TMEM alloc, 4-7 softmax (thread = key row, then dK
-//         epilogue), 8-11 dQ drain (thread = d row: TMEM -> smem -> TMA
-//         reduce-add into dq_acc; then the dV epilogue).
-constexpr int kThreadsBwd2 = 384;
-struct FaBwdSmem2 {
-  uint8_t K[kTile], V[kTile];
-  uint8_t Q[2][kHalf], dO[2][kHalf];
-  uint8_t PT[2][kPT], dST[2][kPT];
-  float dq_stage[kBQb][kD];
-  float L[2][kBQb], D[2][kBQb];
-  uint64_t kv_full, q_full[2], q_empty[2], s_full[2], ps_full[2], pds_empty[2], dq_full[2], dq_empty[2];
-  uint32_t tmem;
-};
-
-__global__ void __launch_bounds__(kThreadsBwd2, 1)
-    fa_bwd_tc2_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_q,
-                      const __grid_constant__ CUtensorMap map_do, const __grid_constant__ CUtensorMap map_dq,
-                      const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv, int s,
-                      int h, int H, float scale) {
-  extern __shared__ __align__(1024) uint8_t rawb[];
-  FaBwdSmem2& sm = *reinterpret_cast<FaBwdSmem2*>(rawb);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // grid (b*H, s/128): key block 0 (the most query blocks) of every head is
-  // launched first, the short diagonal-only blocks last (LPT order)
-  const int kb = blockIdx.y;
-  const int bh = blockIdx.x, bi = bh / H, j = bh % H;
-  const int row0 = bi * s;
-  const int k0 = kb * kBK;
-  const int qb0 = k0 / kBQb, nq = s / kBQb - qb0;
-  const float scale_log2 = scale * 1.4426950408889634f;
-
-  if (threadIdx.x == 0) {
-    bar_init(&sm.kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      bar_init(&sm.q_full[i], 1);
-      bar_init(&sm.q_empty[i], 1);
-      bar_init(&sm.s_full[i], 1);
-      bar_init(&sm.ps_full[i], 128);
-      bar_init(&sm.pds_empty[i], 1);
-      bar_init(&sm.dq_full[i], 1);
-      bar_init(&sm.dq_empty[i], 128);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = sm.tmem;
-  constexpr uint32_t kDV = 256, kDK = 384;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_do)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_q)) : "memory");
-      bar_expect(&sm.kv_full, 2 * kTile);
-      for (int c = 0; c < 2; ++c) {
-        tma2d(sm.K + c * 16384, &map_qkv, &sm.kv_full, h + j * kD + 64 * c, row0 + k0);
-        tma2d(sm.V + c * 16384, &map_qkv, &sm.kv_full, 2 * h + j * kD + 64 * c, row0 + k0);
-      }
-      for (int i = 0; i < nq; ++i) {
-        const int buf = i & 1, q0 = (qb0 + i) * kBQb;
-        bar_wait(&sm.q_empty[buf], ((i >> 1) & 1) ^ 1);
-        bar_expect(&sm.q_full[buf], 2 * kHalf + 2 * kBQb * 4);
-        for (int c = 0; c < 2; ++c) {
-          tma2d(sm.Q[buf] + c * 8192, &map_q, &sm.q_full[buf], j * kD + 64 * c, row0 + q0);
-          tma2d(sm.dO[buf] + c * 8192, &map_do, &sm.q_full[buf], j * kD + 64 * c, row0 + q0);
-        }
-        bulk_g2s(sm.L[buf], lse + (long long)bh * s + q0, kBQb * 4, &sm.q_full[buf]);
-        bulk_g2s(sm.D[buf], Dg + (long long)bh * s + q0, kBQb * 4, &sm.q_full[buf]);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t ka = su32(sm.K), va = su32(sm.V);
-      bar_wait(&sm.kv_full, 0);
-      auto issue_s = [&](int i) {  // S^T, dP^T of block i into TMEM buffer i&1
-        const int buf = i & 1;
-        bar_wait(&sm.q_full[buf], (i >> 1) & 1);
-        bar_wait(&sm.dq_empty[buf], ((i >> 1) & 1) ^ 1);  // dQ^T of block i-2 drained
-        fence_after();
-        const uint32_t qa = su32(sm.Q[buf]), oa = su32(sm.dO[buf]);
-        const uint32_t t0 = tmem + buf * 128;
-#pragma unroll
-        for (int ks = 0; ks < kD / 16; ++ks) {
-          mma(t0, desc_k(ka, ks, 128), desc_k(qa, ks, 64), idesc2(64, false, false), ks != 0);
-          mma(t0 + 64, desc_k(va, ks, 128), desc_k(oa, ks, 64), idesc2(64, false, false), ks != 0);
-        }
-        commit(&sm.s_full[buf]);
-      };
-      issue_s(0);
-      for (int i = 0; i < nq; ++i) {
-        const int buf = i & 1;
-        if (i + 1 < nq) issue_s(i + 1);
-        bar_wait(&sm.ps_full[buf], (i >> 1) & 1);
-        fence_after();
-        const uint32_t qa = su32(sm.Q[buf]), oa = su32(sm.dO[buf]);
-        const uint32_t pa = su32(sm.PT[buf]), da = su32(sm.dST[buf]);
-#pragma unroll
-        for (int ks = 0; ks < kBQb / 16; ++ks) {
-          mma(tmem + kDV, desc_k(pa, ks, 128), desc_mn(oa, ks, 8192), idesc2(128, false, true), (i | ks) != 0);
-          mma(tmem + kDK, desc_k(da, ks, 128), desc_mn(qa, ks, 8192), idesc2(128, false, true), (i | ks) != 0);
-        }
-#pragma unroll
-        for (int ks = 0; ks < kBK / 16; ++ks)
-          mma(tmem + buf * 128, desc_mn(ka, ks, 16384), desc_mn(da, ks, 8192), idesc2(64, true, true), ks != 0);
-        commit(&sm.dq_full[buf]);
-        commit(&sm.q_empty[buf]);
-        commit(&sm.pds_empty[buf]);
-      }
-    }
-  } else if (warp >= 4 && warp < 8) {
-    const int r = (warp - 4) * 32 + lane;  // key row
-    const uint32_t lb = ((uint32_t)((warp & 3) * 32)) << 16;
-    const int key = k0 + r;
-    const uint32_t swz = (uint32_t)(r & 7);
-    const int rowoff = (r >> 3) * 1024 + (r & 7) * 128;
-    for (int i = 0; i < nq; ++i) {
-      const int buf = i & 1, q0 = (qb0 + i) * kBQb;
-      bar_wait(&sm.q_full[buf], (i >> 1) & 1);  // L, D of this block
-      bar_wait(&sm.s_full[buf], (i >> 1) & 1);
-      fence_after();
-      float p[kBQb], ds[kBQb];
-#pragma unroll
-      for (int c = 0; c < kBQb / 32; ++c) {
-        uint32_t a[32], b[32];
-        tld32(tmem + lb + buf * 128 + c * 32, a);
-        tld32(tmem + lb + buf * 128 + 64 + c * 32, b);
-        tld_wait();
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const int qi = c * 32 + q;
-          float pv = exp2f(__uint_as_float(a[q]) * scale_log2 - sm.L[buf][qi] * 1.4426950408889634f);
-          if (q0 + qi < key) pv = 0.0f;  // causal
-          p[qi] = pv;
-          ds[qi] = pv * (__uint_as_float(b[q]) - sm.D[buf][qi]);
-        }
-      }
-      bar_wait(&sm.pds_empty[buf], ((i >> 1) & 1) ^ 1);  // MMAs of block i-2 done with PT/dST[buf]
-#pragma unroll
-      for (int pc = 0; pc < 8; ++pc) {
-        const float* v = p + pc * 8;
-        const float* w = ds + pc * 8;
-        *reinterpret_cast<uint4*>(sm.PT[buf] + rowoff + ((pc ^ swz) << 4)) =
-            make_uint4(pack(v[0], v[1]), pack(v[2], v[3]), pack(v[4], v[5]), pack(v[6], v[7]));
-        *reinterpret_cast<uint4*>(sm.dST[buf] + rowoff + ((pc ^ swz) << 4)) =
-            make_uint4(pack(w[0], w[1]), pack(w[2], w[3]), pack(w[4], w[5]), pack(w[6], w[7]));
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      fence_before();
-      bar_arrive(&sm.ps_full[buf]);
-    }
-    // dK epilogue: the last dq_full commit covers every MMA
-    bar_wait(&sm.dq_full[(nq - 1) & 1], ((nq - 1) >> 1) & 1);
-    fence_after();
-    bf16* out = dqkv + (long long)(row0 + key) * 3 * h + h + j * kD;
-#pragma unroll
-    for (int c = 0; c < kD / 32; ++c) {
-      uint32_t rr[32];
-      tld32(tmem + lb + kDK + c * 32, rr);
-      tld_wait();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 w;
-        w.x = pack(__uint_as_float(rr[8 * q]) * scale, __uint_as_float(rr[8 * q + 1]) * scale);
-        w.y = pack(__uint_as_float(rr[8 * q + 2]) * scale, __uint_as_float(rr[8 * q + 3]) * scale);
-        w.z = pack(__uint_as_float(rr[8 * q + 4]) * scale, __uint_as_float(rr[8 * q + 5]) * scale);
-        w.w = pack(__uint_as_float(rr[8 * q + 6]) * scale, __uint_as_float(rr[8 * q + 7]) * scale);
-        *reinterpret_cast<uint4*>(out + c * 32 + 8 * q) = w;
-      }
-    }
-  } else if (warp >= 8) {
-    const int r = (warp - 8) * 32 + lane;  // d row of dQ^T; key row for dV
-    const uint32_t lb = ((uint32_t)((warp & 3) * 32)) << 16;
-    for (int i = 0; i < nq; ++i) {
-      const int buf = i & 1;
-      bar_wait(&sm.dq_full[buf], (i >> 1) & 1);
-      fence_after();
-      // TMEM -> registers first and release the buffer at once (the MMA warp
-      // waits on it before S/dP(i+2)); only then wait for the previous TMA
-      // reduce to finish reading the staging tile.
-      uint32_t rr[kBQb];
-      tld32(tmem + lb + buf * 128, *reinterpret_cast<uint32_t(*)[32]>(rr));
-      tld32(tmem + lb + buf * 128 + 32, *reinterpret_cast<uint32_t(*)[32]>(rr + 32));
-      tld_wait();
-      fence_before();
-      bar_arrive(&sm.dq_empty[buf]);
-      if (r == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
-      asm volatile("bar.sync 3, 128;" ::: "memory");
-#pragma unroll
-      for (int q = 0; q < kBQb; ++q) sm.dq_stage[q][r] = __uint_as_float(rr[q]) * scale;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync 3, 128;" ::: "memory");
-      if (r == 0) {
-        const int q0 = (qb0 + i) * kBQb;
-        asm volatile(
-            "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                reinterpret_cast<uint64_t>(&map_dq)),
-            "r"(su32(&sm.dq_stage[0][0])), "r"(j * kD), "r"(row0 + q0)
-            : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-    }
-    if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    // dV epilogue (the last dq_full already waited above covers every MMA)
-    bf16* out = dqkv + (long long)(row0 + k0 + r) * 3 * h + 2 * h + j * kD;
-#pragma unroll
-    for (int c = 0; c < kD / 32; ++c) {
-      uint32_t rr[32];
-      tld32(tmem + lb + kDV + c * 32, rr);
-      tld_wait();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 w;
-        w.x = pack(__uint_as_float(rr[8 * q]), __uint_as_float(rr[8 * q + 1]));
-        w.y = pack(__uint_as_float(rr[8 * q + 2]), __uint_as_float(rr[8 * q + 3]));
-        w.z = pack(__uint_as_float(rr[8 * q + 4]), __uint_as_float(rr[8 * q + 5]));
-        w.w = pack(__uint_as_float(rr[8 * q + 6]), __uint_as_float(rr[8 * q + 7]));
-        *reinterpret_cast<uint4*>(out + c * 32 + 8 * q) = w;
-      }
-    }
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  }
-}
-
+constexpr int kThreadsBwd = 384;  // warps 0 TMA, 1 MMA, 2 TMEM alloc, 4-7 softmax, 8-11 dQ drain
 // ---------------------------------------------------------- backward v3
 // Same math; the MMA issue order and buffering are arranged so that neither
 // the Q/dO loads nor the dQ drain sit on the tensor pipe's critical path:
@@ -1073,11 +436,11 @@ struct FaBwdSmem3 {
   uint32_t tmem;
 };
 
-__global__ void __launch_bounds__(kThreadsBwd2, 1)
+__global__ void __launch_bounds__(kThreadsBwd, 1)
     fa_bwd_tc3_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_q,
                       const __grid_constant__ CUtensorMap map_do, const __grid_constant__ CUtensorMap map_dq,
                       const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv, int s,
-                      int h, int H, float scale, int dq_mode, long long* __restrict__ tr) {
+                      int h, int H, float scale, long long* __restrict__ tr) {
   extern __shared__ __align__(1024) uint8_t rawb3[];
   FaBwdSmem3& sm = *reinterpret_cast<FaBwdSmem3*>(rawb3);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1286,7 +649,7 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
         for (int q = 0; q < kBQb / 2; ++q) sm.dq_stage[q][r] = __uint_as_float(rr[half * (kBQb / 2) + q]) * scale;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync 3, 128;" ::: "memory");
-        if (r == 0 && dq_mode == 0) {
+        if (r == 0) {
           const int q0 = (qb0 + i) * kBQb + half * (kBQb / 2);
           asm volatile(
               "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -1354,11 +717,11 @@ struct FaBwdSmem4 {
   uint32_t tmem;
 };
 
-__global__ void __launch_bounds__(kThreadsBwd2, 1)
+__global__ void __launch_bounds__(kThreadsBwd, 1)
     fa_bwd_tc4_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_q,
                       const __grid_constant__ CUtensorMap map_do, const __grid_constant__ CUtensorMap map_dq,
                       const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv, int s,
-                      int h, int H, float scale, int dq_mode, long long* __restrict__ tr) {
+                      int h, int H, float scale, long long* __restrict__ tr) {
   extern __shared__ __align__(1024) uint8_t rawb4[];
   FaBwdSmem4& sm = *reinterpret_cast<FaBwdSmem4*>(rawb4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1573,7 +936,7 @@ __global__ void __launch_bounds__(kThreadsBwd2, 1)
         for (int q = 0; q < kDqRows4; ++q) sm.dq_stage[q][r] = __uint_as_float(rr[half * kDqRows4 + q]) * scale;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync 3, 128;" ::: "memory");
-        if (r == 0 && dq_mode == 0) {
+        if (r == 0) {
           const int q0 = (qb0 + i) * kBQb + half * kDqRows4;
           asm volatile(
               "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -1638,13 +1001,6 @@ bool attention_tc_supported(DType dt, int s, int h, int H) {
   return !off && dt == DType::BF16 && h / H == kD && h % H == 0 && s % kBQ == 0 && encoder() != nullptr;
 }
 
-static int fwd_variant() {  // GS_ATTN_FWD=1: 128-key single-CTA kernel; default 2: 64-key, 2 CTAs/SM
-  static int v = [] {
-    const char* e = getenv("GS_ATTN_FWD");
-    return e ? atoi(e) : 2;
-  }();
-  return v;
-}
 
 // GS_ATTN_TRACE=1: clock64 timeline of CTA (0,0) of the backward (stderr)
 static long long* attn_trace_begin(cudaStream_t st) {
@@ -1674,58 +1030,36 @@ static void attn_trace_end(long long* tr, cudaStream_t st,
 }
 
 cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s, int h, int H, cudaStream_t st) {
-  if (fwd_variant() == 2) {
-    CUtensorMap mq, mkv;
-    const cuuint64_t dims[2] = {(cuuint64_t)3 * h, (cuuint64_t)b * s};
-    const cuuint64_t strides[1] = {(cuuint64_t)3 * h * 2};
-    const cuuint32_t elem[2] = {1, 1};
-    for (int rows : {128, 64}) {
-      const cuuint32_t box[2] = {64, (cuuint32_t)rows};
-      if (encoder()(rows == 128 ? &mq : &mkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims,
-                    strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return cudaErrorInvalidValue;
-    }
-    const int smem = (int)sizeof(FaSmem2);
-    static const int poly = [] {  // GS_ATTN_POLY=1: FMA-pipe exp2 for 1 in 4 elements
-      const char* e = getenv("GS_ATTN_POLY");
-      return e ? atoi(e) : 0;
-    }();
-    auto kern = poly ? fa_fwd_tc2_kernel<1> : fa_fwd_tc2_kernel<0>;
-    static bool init2 = false;
-    if (!init2) {
-      for (auto k : {fa_fwd_tc2_kernel<0>, fa_fwd_tc2_kernel<1>}) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-      }
-      init2 = true;
-    }
-    count_launch();
-    long long* tr = attn_trace_begin(st);
-    kern<<<dim3(b * H, s / kBQ), 256, smem, st>>>(mq, mkv, (bf16*)o, lse, s, h, H,
-                                                               1.4426950408889634f / sqrtf((float)kD), tr);
-    attn_trace_end(tr, st, "0 mma_S_issue 1 mma_P_seen 2 sm_S_seen 3 sm_math 4 sm_P_pub 5 prod_K 6 prod_V", 5);
-    return cudaGetLastError();
-  }
-  CUtensorMap map;
+  CUtensorMap mq, mkv;
   const cuuint64_t dims[2] = {(cuuint64_t)3 * h, (cuuint64_t)b * s};
   const cuuint64_t strides[1] = {(cuuint64_t)3 * h * 2};
-  const cuuint32_t box[2] = {64, 128};
   const cuuint32_t elem[2] = {1, 1};
-  if (encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims, strides, box, elem,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return cudaErrorInvalidValue;
-  const int smem = (int)sizeof(FaSmem) + 1024;
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(fa_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    init = true;
+  for (int rows : {128, 64}) {
+    const cuuint32_t box[2] = {64, (cuuint32_t)rows};
+    if (encoder()(rows == 128 ? &mq : &mkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims,
+                  strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
   }
-  const float scale_log2 = 1.4426950408889634f / sqrtf((float)kD);
+  const int smem = (int)sizeof(FaSmem2);
+  static const int poly = [] {  // GS_ATTN_POLY=1: FMA-pipe exp2 for 1 in 4 elements
+    const char* e = getenv("GS_ATTN_POLY");
+    return e ? atoi(e) : 0;
+  }();
+  auto kern = poly ? fa_fwd_tc2_kernel<1> : fa_fwd_tc2_kernel<0>;
+  static bool init2 = false;
+  if (!init2) {
+    for (auto k : {fa_fwd_tc2_kernel<0>, fa_fwd_tc2_kernel<1>}) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+    }
+    init2 = true;
+  }
   count_launch();
-  fa_fwd_tc_kernel<<<dim3(s / kBQ, b * H), kThreadsFwd, smem, st>>>(map, (bf16*)o, lse, s, h, H, scale_log2);
+  long long* tr = attn_trace_begin(st);
+  kern<<<dim3(b * H, s / kBQ), 256, smem, st>>>(mq, mkv, (bf16*)o, lse, s, h, H,
+                                                             1.4426950408889634f / sqrtf((float)kD), tr);
+  attn_trace_end(tr, st, "0 mma_S_issue 1 mma_P_seen 2 sm_S_seen 3 sm_math 4 sm_P_pub 5 prod_K 6 prod_V", 5);
   return cudaGetLastError();
 }
 
@@ -1754,7 +1088,7 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  static const int variant = [] {  // GS_ATTN_BWD=1: unpipelined, 2: v2, 3: v3; default 4
+  static const int variant = [] {  // GS_ATTN_BWD=3: v3 (P^T in smem, 3-slot ring); default 4
     const char* e = getenv("GS_ATTN_BWD");
     return e ? atoi(e) : 4;
   }();
@@ -1762,7 +1096,7 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
   {
     const cuuint64_t dims[2] = {(cuuint64_t)h, (cuuint64_t)b * s};
     const cuuint64_t strides[1] = {(cuuint64_t)h * 4};
-    const cuuint32_t box[2] = {128, (cuuint32_t)(variant == 4 ? kDqRows4 : variant == 3 ? kBQb / 2 : kBQb)};
+    const cuuint32_t box[2] = {128, (cuuint32_t)(variant == 4 ? kDqRows4 : kBQb / 2)};
     if (encoder()(&mdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq_acc, dims, strides, box, elem,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -1778,8 +1112,8 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
     }
     count_launch();
     long long* tr = attn_trace_begin(st);
-    fa_bwd_tc4_kernel<<<dim3(b * H, s / kBK), kThreadsBwd2, smem4, st>>>(mq, mq64, md, mdq, lse2, D, (bf16*)dqkv, s,
-                                                                          h, H, 1.0f / sqrtf((float)kD), 0, tr);
+    fa_bwd_tc4_kernel<<<dim3(b * H, s / kBK), kThreadsBwd, smem4, st>>>(mq, mq64, md, mdq, lse2, D, (bf16*)dqkv, s,
+                                                                          h, H, 1.0f / sqrtf((float)kD), tr);
     attn_trace_end(tr, st);
     return cudaGetLastError();
   }
@@ -1792,41 +1126,14 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
       init3 = true;
     }
     count_launch();
-    static const int dq_mode = [] {  // GS_ATTN_DQ_EXPERIMENT=1 skips the dQ reduce (timing only, wrong dQ)
-      const char* e = getenv("GS_ATTN_DQ_EXPERIMENT");
-      return e ? atoi(e) : 0;
-    }();
     long long* tr = attn_trace_begin(st);
     // v3 takes the log2-domain lse (lse2 = lse * log2 e, from fa_prep)
-    fa_bwd_tc3_kernel<<<dim3(b * H, s / kBK), kThreadsBwd2, smem3, st>>>(mq, mq64, md, mdq, lse2, D, (bf16*)dqkv, s,
-                                                                          h, H, 1.0f / sqrtf((float)kD), dq_mode, tr);
+    fa_bwd_tc3_kernel<<<dim3(b * H, s / kBK), kThreadsBwd, smem3, st>>>(mq, mq64, md, mdq, lse2, D, (bf16*)dqkv, s,
+                                                                          h, H, 1.0f / sqrtf((float)kD), tr);
     attn_trace_end(tr, st);
     return cudaGetLastError();
   }
-  if (variant == 2) {
-    const int smem2 = (int)sizeof(FaBwdSmem2);
-    static bool init2 = false;
-    if (!init2) {
-      cudaError_t e = cudaFuncSetAttribute(fa_bwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-      if (e != cudaSuccess) return e;
-      init2 = true;
-    }
-    count_launch();
-    fa_bwd_tc2_kernel<<<dim3(b * H, s / kBK), kThreadsBwd2, smem2, st>>>(mq, mq64, md, mdq, lse, D, (bf16*)dqkv, s,
-                                                                          h, H, 1.0f / sqrtf((float)kD));
-    return cudaGetLastError();
-  }
-  const int smem = (int)sizeof(FaBwdSmem) + 1024;
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(fa_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
-  count_launch();
-  fa_bwd_tc_kernel<<<dim3(s / kBK, b * H), kThreadsFa, smem, st>>>(mq, mq64, md, mdq, lse, D, (bf16*)dqkv, dq_acc, s, h, H,
-                                                                    1.0f / sqrtf((float)kD));
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;  // GS_ATTN_BWD must be 3 or 4
 }
 
 }  // namespace gs
