@@ -347,15 +347,24 @@ __device__ __forceinline__ void st4<__nv_bfloat16>(__nv_bfloat16* p, float a, fl
   *reinterpret_cast<uint2*>(p) = *reinterpret_cast<const uint2*>(v);
 }
 
-// One row (token) per block: max, sum of exp, then d(CE)/dlogits = (softmax
-// - onehot) * scale.  fp32 logits are read with 16-byte loads when V % 4 == 0
-// (the row stays in L2 between the three passes); SFU exponentials (__expf,
-// relative error ~2^-21) for the sum and the gradient, libm log for the loss.
+// One row (token) per block.  Pass 1: each thread keeps an online (max, sum
+// of exp) over its 16-byte vectors, combined across the block; pass 2 writes
+// d(CE)/dlogits = (softmax - onehot) * scale.  The row is read twice (the
+// second read mostly from L2) instead of three times; SFU exponentials
+// (__expf, relative error ~2^-21), libm log for the loss.
+__device__ __forceinline__ void online_add(float& m, float& z, float x) {
+  if (x > m) {
+    z = z * __expf(m - x) + 1.0f;
+    m = x;
+  } else {
+    z += __expf(x - m);
+  }
+}
 template <typename T>
 __global__ void __launch_bounds__(kRowThreads) xent_kernel(const float* __restrict__ logits, T* dlogits,
                                                            const int32_t* __restrict__ tok, int s, int V,
                                                            float scale, double* loss_sum) {
-  __shared__ float red[8];
+  __shared__ float red_m[8], red_z[8];
   const long long row = blockIdx.x;
   const int bi = (int)(row / s), t = (int)(row % s);
   const int target = tok[bi * (s + 1) + t + 1];
@@ -364,21 +373,37 @@ __global__ void __launch_bounds__(kRowThreads) xent_kernel(const float* __restri
   const bool vec = (V & 3) == 0;
   const int V4 = vec ? V / 4 : 0;
   const float4* l4 = reinterpret_cast<const float4*>(lr);
-  float mx = -INFINITY;
+  float m = -INFINITY, z = 0.0f;
   for (int v = threadIdx.x; v < V4; v += kRowThreads) {
     const float4 x = l4[v];
-    mx = fmaxf(mx, fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
+    const float mx = fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w));
+    if (mx > m) {
+      z *= __expf(m - mx);
+      m = mx;
+    }
+    z += __expf(x.x - m) + __expf(x.y - m) + __expf(x.z - m) + __expf(x.w - m);
   }
-  for (int v = 4 * V4 + threadIdx.x; v < V; v += kRowThreads) mx = fmaxf(mx, lr[v]);
-  mx = block_max256(mx, red);
-  float z = 0.0f;
-  for (int v = threadIdx.x; v < V4; v += kRowThreads) {
-    const float4 x = l4[v];
-    z += __expf(x.x - mx) + __expf(x.y - mx) + __expf(x.z - mx) + __expf(x.w - mx);
+  for (int v = 4 * V4 + threadIdx.x; v < V; v += kRowThreads) online_add(m, z, lr[v]);
+  // combine (m, z) pairs: warp shuffles, then the 8 warps through shared memory
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float mo = __shfl_xor_sync(0xffffffffu, m, o), zo = __shfl_xor_sync(0xffffffffu, z, o);
+    const float mn = fmaxf(m, mo);
+    z = (m == -INFINITY ? 0.0f : z * __expf(m - mn)) + (mo == -INFINITY ? 0.0f : zo * __expf(mo - mn));
+    m = mn;
   }
-  for (int v = 4 * V4 + threadIdx.x; v < V; v += kRowThreads) z += __expf(lr[v] - mx);
-  z = block_sum256(z, red);
-  const float lse = mx + logf(z);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    red_m[w] = m;
+    red_z[w] = z;
+  }
+  __syncthreads();
+  float M = -INFINITY;
+  for (int i = 0; i < kRowThreads / 32; ++i) M = fmaxf(M, red_m[i]);
+  float Z = 0.0f;
+  for (int i = 0; i < kRowThreads / 32; ++i)
+    if (red_m[i] != -INFINITY) Z += red_z[i] * __expf(red_m[i] - M);
+  const float lse = M + logf(Z);
   for (int v = threadIdx.x; v < V4; v += kRowThreads) {
     const float4 x = l4[v];
     const int e = 4 * v;

@@ -16,5 +16,8 @@ for k in "tc_gemm_kernel:qkv" "tc_gemm_kernel:fc1" "tc_gemm_kernel:wgrad" "fa_fw
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$name -s 2 -c 1 \
     -o $out/final_prof_$tag -f python tools/ncu_targets.py $tag > $out/final_ncu_$tag.log 2>&1
   ncu -i $out/final_prof_$tag.ncu-rep --page raw --csv > $out/final_raw_$tag.csv 2>/dev/null
+  ncu -i $out/final_prof_$tag.ncu-rep --page source --csv --print-source sass > $out/final_sass_$tag.csv 2>/dev/null
+  gzip -f $out/final_sass_$tag.csv
+  rm -f $out/final_prof_$tag.ncu-rep   # keep gpurun_out under the 64 MiB copy-back limit
 done
 ls -la $out
