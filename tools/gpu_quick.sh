@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_engine.py -x -q > gpurun_out/t_k.log 2>&1; echo "rc=$?" >> gpurun_out/t_k.log
-timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench23.log 2>&1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/torchrun1.log 2>&1; echo "rc=$?" >> gpurun_out/torchrun1.log
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29512 bench.py --impl reference --gpus 1 --steps 2 --warmup 3 > gpurun_out/torchrun1_ref.log 2>&1; echo "rc=$?" >> gpurun_out/torchrun1_ref.log
