@@ -2,9 +2,13 @@
 
 #include <cuda_runtime.h>
 #include <fcntl.h>
+#include <linux/io_uring.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
 #include <unistd.h>
 
 #include <cerrno>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -79,6 +83,89 @@ void ThreadPool::run_all(std::vector<std::function<void()>>& jobs) {
   batch_ = nullptr;
 }
 
+// ------------------------------------------------------------------ io_uring
+Uring::Uring(unsigned depth) : depth_(depth) {
+  io_uring_params p{};
+  fd_ = static_cast<int>(syscall(__NR_io_uring_setup, depth, &p));
+  if (fd_ < 0) return;
+  sq_len_ = p.sq_off.array + p.sq_entries * sizeof(unsigned);
+  cq_len_ = p.cq_off.cqes + p.cq_entries * sizeof(io_uring_cqe);
+  sqes_len_ = p.sq_entries * sizeof(io_uring_sqe);
+  sq_ptr_ = mmap(nullptr, sq_len_, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd_, IORING_OFF_SQ_RING);
+  cq_ptr_ = mmap(nullptr, cq_len_, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd_, IORING_OFF_CQ_RING);
+  sqes_ = mmap(nullptr, sqes_len_, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd_, IORING_OFF_SQES);
+  if (sq_ptr_ == MAP_FAILED || cq_ptr_ == MAP_FAILED || sqes_ == MAP_FAILED) {
+    close(fd_);
+    fd_ = -1;
+    return;
+  }
+  auto at = [](void* base, unsigned off) { return reinterpret_cast<unsigned*>(static_cast<uint8_t*>(base) + off); };
+  sq_head_ = at(sq_ptr_, p.sq_off.head);
+  sq_tail_ = at(sq_ptr_, p.sq_off.tail);
+  sq_mask_ = at(sq_ptr_, p.sq_off.ring_mask);
+  sq_array_ = at(sq_ptr_, p.sq_off.array);
+  cq_head_ = at(cq_ptr_, p.cq_off.head);
+  cq_tail_ = at(cq_ptr_, p.cq_off.tail);
+  cq_mask_ = at(cq_ptr_, p.cq_off.ring_mask);
+  cqes_ = static_cast<uint8_t*>(cq_ptr_) + p.cq_off.cqes;
+}
+
+Uring::~Uring() {
+  if (sq_ptr_ && sq_ptr_ != MAP_FAILED) munmap(sq_ptr_, sq_len_);
+  if (cq_ptr_ && cq_ptr_ != MAP_FAILED) munmap(cq_ptr_, cq_len_);
+  if (sqes_ && sqes_ != MAP_FAILED) munmap(sqes_, sqes_len_);
+  if (fd_ >= 0) close(fd_);
+}
+
+std::string Uring::transfer(int file_fd, bool write, uint64_t off, uint8_t* buf, uint64_t bytes, uint64_t piece) {
+  struct Req {
+    uint64_t pos, len;
+  };
+  std::vector<Req> todo;
+  for (uint64_t pos = 0; pos < bytes; pos += piece) todo.push_back({pos, std::min(piece, bytes - pos)});
+  size_t next = 0;
+  unsigned inflight = 0;
+  io_uring_sqe* sqes = static_cast<io_uring_sqe*>(sqes_);
+  io_uring_cqe* cqes = static_cast<io_uring_cqe*>(cqes_);
+  while (next < todo.size() || inflight > 0) {
+    unsigned queued = 0;
+    unsigned tail = __atomic_load_n(sq_tail_, __ATOMIC_RELAXED);
+    while (next < todo.size() && inflight + queued < depth_) {
+      const unsigned idx = tail & *sq_mask_;
+      io_uring_sqe& e = sqes[idx];
+      std::memset(&e, 0, sizeof(e));
+      e.opcode = write ? IORING_OP_WRITE : IORING_OP_READ;
+      e.fd = file_fd;
+      e.addr = reinterpret_cast<uint64_t>(buf + todo[next].pos);
+      e.len = static_cast<uint32_t>(todo[next].len);
+      e.off = off + todo[next].pos;
+      e.user_data = next;
+      sq_array_[idx] = idx;
+      ++tail;
+      ++next;
+      ++queued;
+    }
+    __atomic_store_n(sq_tail_, tail, __ATOMIC_RELEASE);
+    const long r = syscall(__NR_io_uring_enter, fd_, queued, 1, IORING_ENTER_GETEVENTS, nullptr, 0);
+    if (r < 0 && errno != EINTR) return std::string("io_uring_enter: ") + std::strerror(errno);
+    inflight += queued;
+    unsigned head = __atomic_load_n(cq_head_, __ATOMIC_RELAXED);
+    const unsigned ctail = __atomic_load_n(cq_tail_, __ATOMIC_ACQUIRE);
+    for (; head != ctail; ++head) {
+      const io_uring_cqe& c = cqes[head & *cq_mask_];
+      --inflight;
+      Req& q = todo[static_cast<size_t>(c.user_data)];
+      if (c.res < 0) return std::string(write ? "write: " : "read: ") + std::strerror(-c.res);
+      if (c.res == 0) return std::string(write ? "write" : "read") + ": unexpected EOF";
+      if (static_cast<uint64_t>(c.res) < q.len) {  // short transfer: queue the rest
+        todo.push_back({q.pos + static_cast<uint64_t>(c.res), q.len - static_cast<uint64_t>(c.res)});
+      }
+    }
+    __atomic_store_n(cq_head_, head, __ATOMIC_RELEASE);
+  }
+  return {};
+}
+
 NvmeFile::NvmeFile(const std::string& dir, bool odirect, int threads) : read_pool_(threads), write_pool_(threads) {
   std::string tmpl = dir + "/greedysnake_tier_XXXXXX";
   std::vector<char> buf(tmpl.begin(), tmpl.end());
@@ -97,6 +184,15 @@ NvmeFile::NvmeFile(const std::string& dir, bool odirect, int threads) : read_poo
   }
   if (fd_ < 0) throw offsim::ValidationError("cannot open NVMe tier file " + path_);
   unlink(path_.c_str());  // anonymous: space is released when the engine closes
+  const char* e = getenv("GS_NVME_URING");
+  if (!e || atoi(e) != 0) {
+    read_ring_ = std::make_unique<Uring>(32);
+    write_ring_ = std::make_unique<Uring>(32);
+    if (!read_ring_->ok() || !write_ring_->ok()) {
+      read_ring_.reset();
+      write_ring_.reset();
+    }
+  }
 }
 
 NvmeFile::~NvmeFile() {
@@ -118,6 +214,13 @@ void NvmeFile::finalize_size() {
 uint64_t NvmeFile::io(bool wr, uint64_t off, void* buf, uint64_t bytes) {
   if (bytes == 0) return 0;
   const uint64_t total = align_up(bytes, kNvmeAlign);
+  if (read_ring_) {
+    std::lock_guard<std::mutex> g(wr ? write_mu_ : read_mu_);
+    const std::string err =
+        (wr ? write_ring_ : read_ring_)->transfer(fd_, wr, off, static_cast<uint8_t*>(buf), total, 2ull << 20);
+    if (!err.empty()) throw std::runtime_error("NVMe tier (io_uring): " + err);
+    return total;
+  }
   constexpr uint64_t kChunk = 8ull << 20;
   std::vector<std::function<void()>> jobs;
   std::mutex err_mu;

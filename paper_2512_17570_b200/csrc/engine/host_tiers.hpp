@@ -7,6 +7,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -52,8 +53,35 @@ class ThreadPool {
   bool stop_ = false;
 };
 
+// Minimal io_uring submission/completion queue over raw syscalls (liburing
+// is not in the image): O_DIRECT reads / writes of fixed-size pieces with up
+// to `depth` in flight.  One ring per direction; not thread-safe by itself.
+class Uring {
+ public:
+  explicit Uring(unsigned depth);
+  ~Uring();
+  bool ok() const { return fd_ >= 0; }
+  // Transfers [off, off + bytes) between the file and buf in `piece`-byte
+  // requests, keeping the queue full; short transfers are resubmitted.
+  // Returns an error string (empty on success).
+  std::string transfer(int file_fd, bool write, uint64_t off, uint8_t* buf, uint64_t bytes, uint64_t piece);
+
+ private:
+  int fd_ = -1;
+  unsigned depth_ = 0;
+  void* sq_ptr_ = nullptr;
+  void* cq_ptr_ = nullptr;
+  void* sqes_ = nullptr;
+  size_t sq_len_ = 0, cq_len_ = 0, sqes_len_ = 0;
+  unsigned *sq_head_ = nullptr, *sq_tail_ = nullptr, *sq_mask_ = nullptr, *sq_array_ = nullptr;
+  unsigned *cq_head_ = nullptr, *cq_tail_ = nullptr, *cq_mask_ = nullptr;
+  void* cqes_ = nullptr;
+};
+
 // The NVMe tier: one preallocated file, regions handed out 4 KiB-aligned.
-// Transfers are split into <= chunk-sized pieces issued concurrently.
+// Transfers are split into <= chunk-sized pieces issued concurrently —
+// through io_uring (queue depth 32) when the kernel allows it, else on a
+// small pread/pwrite thread pool (GS_NVME_URING=0 forces the pool).
 class NvmeFile {
  public:
   NvmeFile(const std::string& dir, bool odirect, int threads);
@@ -75,9 +103,14 @@ class NvmeFile {
   int fd_ = -1;
   bool direct_ = false;
   uint64_t size_ = 0;
-  // separate pools so the SSD_R and SSD_W queues (distinct dispatcher
-  // threads, full-duplex device) never share a batch
+  // separate pools / rings so the SSD_R and SSD_W queues (distinct
+  // dispatcher threads, full-duplex device) never share a batch
   ThreadPool read_pool_, write_pool_;
+  std::unique_ptr<Uring> read_ring_, write_ring_;
+  std::mutex read_mu_, write_mu_;
+
+ public:
+  bool uring() const { return read_ring_ != nullptr; }
 };
 
 }  // namespace gs::engine

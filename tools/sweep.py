@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--model", default="gpt1.3b", choices=["gpt1.3b", "gpt13b"],
+                    help="gpt13b: BASELINE configs[2] shape, half the Adam state on NVMe, M and alpha sweep")
     args = ap.parse_args()
     import torch
     import oracle_bindings as ob
@@ -40,6 +42,10 @@ def main():
     rows = [("vertical", 0.2, (1, 1, 1), m) for m in ([1, 4, 16] if args.quick else [1, 2, 4, 8, 16, 32])]
     rows += [("vertical", 0.0, (1, 1, 1), 16), ("horizontal", 0.0, (1, 1, 1), 16)]
     rows += [("vertical", 0.2, (1, 1, 0), 16), ("vertical", 0.0, (1, 1, 0), 16)]
+    if args.model == "gpt13b":
+        # 75.5 GB of Adam state on the NVMe tier (this box: 80 GB disk, 196 GB DRAM)
+        N, h, H = 40, 5120, 40
+        rows = [("vertical", a, (1, 1, 0.5), m) for m in (8, 16, 32) for a in (0.2, 0.0)]
     model = gs.ModelSpec(N, h, H, s, b, 2, 4, 3, 1)
     g = ob.Geometry(n_layers=N, hidden=h, heads=H, seq=s, mb_size=b, vocab=V)
     for sched, alpha, split, M in rows:
