@@ -46,7 +46,7 @@ const std::map<std::string, std::vector<std::string>> kOptions = {
     {"traffic", {"out", "format", "schedule", "microbatches", "alpha", "split"}},
     {"alloc-plan", {"count", "size"}},
     {"run", {"out", "format", "schedule", "microbatches", "alpha", "split", "iterations", "warmup", "vocab",
-             "nvme-dir", "seed", "device", "lp-bytes"}},
+             "nvme-dir", "seed", "device", "lp-bytes", "from-plan"}},
 };
 
 Args parse_args(int argc, char** argv) {
@@ -195,19 +195,23 @@ std::string fmt(double v) {
   return o.str();
 }
 
+SchedulePlan read_plan(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw ValidationError("cannot open plan JSON: " + path);
+  Json j;
+  try {
+    in >> j;
+  } catch (const std::exception& e) {
+    throw ValidationError(std::string("bad plan JSON: ") + e.what());
+  }
+  return plan_from_json(j);
+}
+
 int cmd_simulate(const Args& a) {
   const RunConfig cfg = load(a);
   SchedulePlan plan;
   if (a.has("from-plan")) {
-    std::ifstream in(a.get("from-plan"));
-    if (!in) throw ValidationError("cannot open plan JSON: " + a.get("from-plan"));
-    Json j;
-    try {
-      in >> j;
-    } catch (const std::exception& e) {
-      throw ValidationError(std::string("bad plan JSON: ") + e.what());
-    }
-    plan = plan_from_json(j);
+    plan = read_plan(a.get("from-plan"));
   } else {
     plan = build(cfg);
   }
@@ -342,7 +346,9 @@ int cmd_alloc(const Args& a) {
 int cmd_run(const Args& a) {
   RunConfig cfg = load(a);
   if (a.has("lp-bytes")) cfg.model.low_precision_bytes = to_int(a.get("lp-bytes"), "--lp-bytes");
-  const SchedulePlan plan = build(cfg);
+  // --from-plan: execute a dumped plan (e.g. the reference CLI's
+  // `simulate --emit-plan`) instead of building one from the config
+  const SchedulePlan plan = a.has("from-plan") ? read_plan(a.get("from-plan")) : build(cfg);
   ExecConfig ec;
   ec.model = cfg.model;
   ec.vocab_size = a.has("vocab") ? to_int(a.get("vocab"), "--vocab") : 50304;

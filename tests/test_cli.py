@@ -113,3 +113,21 @@ def test_run_tiny_config_on_gpu(tmp_path):
     cfg.write_text(TINY)
     j = json.loads(offsim("run", str(cfg), "--iterations", "2", "--vocab", "128", "--lp-bytes", "4"))
     assert j["ledger_equals_plan"] is True and len(j["losses"]) == 2 and j["measured_iteration_time"] > 0
+
+
+@requires_reference
+@pytest.mark.gpu
+def test_run_executes_a_reference_dumped_plan(tmp_path):
+    """A plan produced by the reference's own builder (plan_to_json, the
+    `simulate --emit-plan` format) executes here unchanged; the executed
+    ledger equals the plan's."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    cfg = tmp_path / "tiny.ini"
+    cfg.write_text(TINY)
+    plan = tmp_path / "ref_plan.json"
+    plan.write_text(ob.ref_plan_json("vertical", ob.model_array(4, 64, 4, 32, 2, lp=4), 4, (1, 1, 0.5), 0.25))
+    j = json.loads(offsim("run", str(cfg), "--from-plan", str(plan), "--iterations", "2", "--vocab", "128",
+                          "--lp-bytes", "4"))
+    assert j["ledger_equals_plan"] is True and len(j["losses"]) == 2
