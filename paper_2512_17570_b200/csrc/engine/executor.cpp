@@ -955,10 +955,18 @@ void Executor::Impl::compute_task(const Task& t, int it) {
   LaunchCounter lc;
   if (t.kind == TaskKind::FixedOps) {
     const long long tok_n = 1LL * M * d.b * (d.s + 1);
+    // token ids of this iteration: host tokens are read from the mapped
+    // pinned buffer by an SM copy kernel (a cudaMemcpy would queue on the
+    // copy engines behind the plan's bulk parameter / checkpoint DMA)
     const int32_t* src = run_tokens + static_cast<long long>(it) * tok_n;
-    cuda_check(cudaMemcpyAsync(dev_tok[slot], src, 4 * tok_n,
-                               run_tokens_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s_gpu),
-               "tokens");
+    const uint32_t* from = reinterpret_cast<const uint32_t*>(src);
+    if (!run_tokens_dev) {
+      void* dp = nullptr;
+      cuda_check(cudaHostGetDevicePointer(&dp, const_cast<int32_t*>(src), 0), "token device pointer");
+      from = static_cast<const uint32_t*>(dp);
+    }
+    cuda_check(gs::copy_words(reinterpret_cast<uint32_t*>(dev_tok[slot]), from, tok_n, s_gpu), "tokens");
+    lc.n += 1;
     cuda_check(cudaMemsetAsync(dev_loss + it, 0, sizeof(double), s_gpu), "loss");
     if (fixed_done < git) {  // embedding / head step with the previous iteration's grads
       if (dp && ncclAllReduce(fx_grad, fx_grad, static_cast<size_t>(n_fixed), ncclFloat, ncclSum, comm, s_gpu) !=

@@ -24,7 +24,7 @@ uint8_t* PinnedArena::alloc(uint64_t bytes) {
   if (bytes == 0) return nullptr;
   const uint64_t n = align_up(bytes, kNvmeAlign);
   void* p = nullptr;
-  if (cudaHostAlloc(&p, n, cudaHostAllocPortable) != cudaSuccess || !p)
+  if (cudaHostAlloc(&p, n, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess || !p)
     throw offsim::InfeasibleError("pinned host allocation of " + std::to_string(n) + " bytes failed");
   std::memset(p, 0, n);
   blocks_.push_back(p);

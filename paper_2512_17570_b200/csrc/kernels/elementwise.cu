@@ -563,6 +563,17 @@ cudaError_t add(DType dt, const void* a, const void* b, void* y, long long n, cu
 }
 cudaError_t fill_zero(void* p, size_t bytes, cudaStream_t s) { return cudaMemsetAsync(p, 0, bytes, s); }
 
+__global__ void copy_words_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+cudaError_t copy_words(uint32_t* dst, const uint32_t* src, long long n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  copy_words_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, src, n);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t embed_fwd(DType dt, const void* wte, const void* wpe, const int32_t* tok, void* x0, int b, int s,
                       int h, cudaStream_t st) {
   GS_DISPATCH(dt, embed_fwd_kernel<T><<<b * s, 256, 0, st>>>((const T*)wte, (const T*)wpe, tok, (T*)x0, s, h));
