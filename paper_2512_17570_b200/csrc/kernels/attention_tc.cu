@@ -347,6 +347,11 @@ __global__ void __launch_bounds__(256, 2)
       bar_arrive(&sm.p_full[buf]);
       if (r == 0) GS_TRF(4, kb);
     }
+    // o_done completes once per PV.  Seeing S(nblk-1) only guarantees
+    // PV(nblk-3), so the barrier may still be in phase nblk-2: wait for that
+    // phase first, then for PV(nblk-1) (a parity wait is only unambiguous one
+    // phase ahead).
+    if (nblk >= 2) bar_wait(&sm.o_done, (nblk - 2) & 1);
     bar_wait(&sm.o_done, (nblk - 1) & 1);
     fence_after();
     const float inv = 1.0f / l_run;

@@ -169,6 +169,14 @@ def test_attention_fwd_bwd(dtype, b, s, h, H, amp):
     tol = 1e-2 if dtype == BF16 else 1e-5
     assert rel(o.float(), o_ref) < tol
     assert rel(lse.view(b, H, s), lse_ref) < 1e-4
+    # no row may be off (a pipeline race shows up as whole wrong warps of
+    # rows while the global norm still looks fine); repeat runs bit-identical
+    row_err = (o.float() - o_ref).view(b * s, H, -1).norm(dim=-1) / o_ref.view(b * s, H, -1).norm(dim=-1).clamp_min(1e-6)
+    assert float(row_err.max()) < (0.05 if dtype == BF16 else 1e-4)
+    o2 = torch.empty_like(o)
+    gs.check(lib.gs_attention_fwd(dtype, ptr(qkv), ptr(o2), ptr(lse), b, s, h, H, None))
+    torch.cuda.synchronize()
+    assert torch.equal(o, o2)
     dout = torch.randn(b * s, h, device=d).to(tdt)
     o_ref.backward(dout.float())
     dqkv = torch.empty_like(qkv)
