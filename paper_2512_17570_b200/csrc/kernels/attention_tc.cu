@@ -342,16 +342,17 @@ __global__ void __launch_bounds__(256, 2)
           tst32(tmem + lane_base + 128 + c * 32, rr);
         }
       }
+      // o_done completes once per PV and a parity wait is only unambiguous
+      // one phase ahead.  Before this warp's p_full(kb) arrive the barrier is
+      // in phase kb-1 or kb (PV(kb) cannot be issued yet), so observe PV(kb-1)
+      // here on the last block; after the arrive it is in phase nblk-1 or
+      // nblk and the epilogue's wait for PV(nblk-1) cannot alias.
+      if (kb == nblk - 1 && kb > 0) bar_wait(&sm.o_done, (kb - 1) & 1);
       tst_wait();
       fence_before();
       bar_arrive(&sm.p_full[buf]);
       if (r == 0) GS_TRF(4, kb);
     }
-    // o_done completes once per PV.  Seeing S(nblk-1) only guarantees
-    // PV(nblk-3), so the barrier may still be in phase nblk-2: wait for that
-    // phase first, then for PV(nblk-1) (a parity wait is only unambiguous one
-    // phase ahead).
-    if (nblk >= 2) bar_wait(&sm.o_done, (nblk - 2) & 1);
     bar_wait(&sm.o_done, (nblk - 1) & 1);
     fence_after();
     const float inv = 1.0f / l_run;

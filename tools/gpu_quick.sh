@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
 timeout 300 python tools/attn_accuracy.py > gpurun_out/attn_acc.txt 2>&1
-timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q -k attention > gpurun_out/t_attn2.log 2>&1; echo "rc=$?" >> gpurun_out/t_attn2.log
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
