@@ -1,4 +1,6 @@
 mkdir -p gpurun_out
-timeout 300 python tools/attn_accuracy.py > gpurun_out/attn_acc.txt 2>&1
-timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+rm -f gpurun_out/prio_ab.txt
+for r in 1 2; do for p in 0 1 2; do
+  GS_STREAM_PRIO=$p timeout 600 python bench.py > gpurun_out/b.log 2>&1
+  echo "prio=$p $(tail -1 gpurun_out/b.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"], d["clocks"]["sm_mhz"])')" >> gpurun_out/prio_ab.txt
+done; done
