@@ -39,12 +39,17 @@ def copies():
     return ev0, ev1
 
 
-for mode in ("alone", "with_gemm", "alone"):
+for mode in ("alone", "with_gemm", "with_gemm_capped", "alone"):
     torch.cuda.synchronize()
-    if mode == "with_gemm":
+    if mode.startswith("with_gemm"):
         with torch.cuda.stream(s3):
-            for _ in range(200):
+            # "capped": ~1 s of GEMMs queued, copies start behind 0.4 s of them
+            # so the GPU is at its power cap while they run
+            for _ in range(200 if mode == "with_gemm" else 6000):
                 gs.check(lib.gs_gemm(1, M, N, K, p(A), 1, p(B), 1, p(Cc), None, p(G), 3, C.c_void_p(s3.cuda_stream)))
+    if mode == "with_gemm_capped":
+
+        import time; time.sleep(0.4)
     e0, e1 = copies()
     torch.cuda.synchronize()
     print(json.dumps({"mode": mode, "gbs_per_direction": n * chunk / (e0.elapsed_time(e1) / 1e3) / 1e9}), flush=True)

@@ -61,3 +61,23 @@ for res in ("pcie_h2d", "pcie_d2h"):
         print(f"{res} {phase}: {len(ph)} copies, {byts / 1e9:.2f} GB in {span:.1f} ms span "
               f"({byts / 1e9 / (span / 1e3):.1f} GB/s), idle between copies {idle:.1f} ms, "
               f"median copy rate {np.median(rates) if rates else 0:.1f} GB/s")
+
+# One forward stage in detail: every task on every resource, times relative to
+# the stage's first compute task.
+stage = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+st_tasks = [r for r in gpu if tasks[r["task"]]["kind"] == "fwd" and tasks[r["task"]]["stage"] == stage]
+ts0 = min(r["t_start_ms"] for r in st_tasks); ts1 = max(r["t_end_ms"] for r in st_tasks)
+print(f"\nforward stage {stage}: compute {ts0 - t0:.2f} .. {ts1 - t0:.2f} ms ({ts1 - ts0:.2f} ms, {len(st_tasks)} tasks)")
+window = [r for r in recs if r["t_end_ms"] >= ts0 - 2 and r["t_start_ms"] <= ts1 + 2]
+d2h = [r for r in recs if r["resource"] == "pcie_d2h"]
+for r in sorted(window, key=lambda r: (r["resource"], r["t_start_ms"])):
+    t = tasks[r["task"]]
+    dur = r["t_end_ms"] - r["t_start_ms"]
+    ov = 0.0
+    if r["resource"] == "pcie_h2d":
+        for q in d2h:
+            ov += max(0.0, min(q["t_end_ms"], r["t_end_ms"]) - max(q["t_start_ms"], r["t_start_ms"]))
+    rate = r["bytes"] / max(1e-9, dur / 1e3) / 1e9 if r["bytes"] else 0.0
+    print(f"  {r['resource']:9s} {t['kind']:12s} L{t['layer']:<3d} mb{t['microbatch']:<3d} "
+          f"{r['t_start_ms'] - ts0:8.3f} {r['t_end_ms'] - ts0:8.3f}  {r['bytes'] / 1e6:8.2f} MB  {rate:6.1f} GB/s"
+          + (f"  d2h-overlap {ov / max(dur, 1e-9):.2f}" if r["resource"] == "pcie_h2d" else ""))
