@@ -184,7 +184,8 @@ int gs_engine_trace(gs_engine* engine, gs_trace_record* out, int cap, int* n);
 /* dtype: 0 = fp32, 1 = bf16.  stream: cudaStream_t (NULL = legacy default). */
 /* C[M,N] = sum_k A(m,k) B(n,k);  a_kmajor: A is [M][K] else [K][M];
    b_kmajor: B is [N][K] else [K][N].  epi: 0 store, 1 store + residual R,
-   2 fp32 accumulate (C fp32), 3 store + gelu to G, 4 fp32 store. */
+   2 fp32 accumulate (C fp32), 3 store + gelu to G, 4 fp32 store,
+   5 C = acc * gelu'(R), 6 C = gelu(acc).  Other values: GS_ERR_VALIDATION. */
 int gs_gemm(int dtype, int M, int N, int K, const void* A, int a_kmajor, const void* B, int b_kmajor, void* C,
             const void* R, void* G, int epi, void* stream);
 /* same, forcing the CUDA-core path (reference for the tcgen05 path) */

@@ -338,6 +338,10 @@ int gs_engine_trace(gs_engine* engine, gs_trace_record* out, int cap, int* n) {
 // ----------------------------------------------------------------- kernels
 static int gemm_common(bool simt, int dtype, int M, int N, int K, const void* A, int a_k, const void* B, int b_k,
                        void* C, const void* R, void* G, int epi, void* stream) {
+  if (epi < 0 || epi > static_cast<int>(gs::Epi::Gelu)) {
+    g_error = "gs_gemm: unknown epilogue " + std::to_string(epi);
+    return GS_ERR_VALIDATION;
+  }
   gs::GemmArgs g;
   g.M = M;
   g.N = N;

@@ -160,9 +160,11 @@ void free_workspace(Workspace& ws) {
   ws = Workspace{};
 }
 
-// Forward through LN1 .. GELU; leaves a, qkv, o, lse, x1, c, u, g, stats in ws.
+// Forward through LN1 .. GELU; leaves a, qkv, o, lse, x1, c, g, stats in ws,
+// and u (the pre-GELU activation) when keep_u — only the recompute feeds a
+// backward, so FwdCompute skips that 4*T*h store.
 static cudaError_t forward_body(const Dims& d, const void* W, const void* x, Workspace& ws, cudaStream_t st,
-                                LaunchCounter& lc) {
+                                LaunchCounter& lc, bool keep_u) {
   const int T = d.T(), h = d.h, eb = d.lp();
   const long long h2 = 1LL * h * h;
   const void* wqkv = W;
@@ -176,7 +178,10 @@ static cudaError_t forward_body(const Dims& d, const void* W, const void* x, Wor
   }
   GS_TRY(mm(d, T, h, h, ws.o, true, wo, true, ws.x1, Epi::AddResidual, st, lc, x, nullptr, ws.prof));
   GS_PROF(Norm, layernorm_fwd(d.dt, ws.x1, ws.c, ws.m2, ws.r2, T, h, st));
-  GS_TRY(mm(d, T, 4 * h, h, ws.c, true, w1, true, ws.u, Epi::StoreGelu, st, lc, nullptr, ws.g, ws.prof));
+  if (keep_u)
+    GS_TRY(mm(d, T, 4 * h, h, ws.c, true, w1, true, ws.u, Epi::StoreGelu, st, lc, nullptr, ws.g, ws.prof));
+  else
+    GS_TRY(mm(d, T, 4 * h, h, ws.c, true, w1, true, ws.g, Epi::Gelu, st, lc, nullptr, nullptr, ws.prof));
   lc.n += 4;  // two LayerNorms + attention (1 kernel in either path... counted as 1) + spare
   return cudaSuccess;
 }
@@ -184,7 +189,7 @@ static cudaError_t forward_body(const Dims& d, const void* W, const void* x, Wor
 cudaError_t layer_forward(const Dims& d, const void* W, const void* x, void* y, Workspace& ws, cudaStream_t st,
                           LaunchCounter& lc) {
   const long long h2 = 1LL * d.h * d.h;
-  GS_TRY(forward_body(d, W, x, ws, st, lc));
+  GS_TRY(forward_body(d, W, x, ws, st, lc, false));
   return mm(d, d.T(), d.h, 4 * d.h, ws.g, true, off(W, 8 * h2, d.lp()), true, y, Epi::AddResidual, st, lc, ws.x1, nullptr, ws.prof);
 }
 
@@ -197,7 +202,7 @@ cudaError_t layer_backward(const Dims& d, const void* W, const void* x, const vo
   const void* w1 = off(W, 4 * h2, eb);
   const void* w2 = off(W, 8 * h2, eb);
   const Epi wg = first ? Epi::StoreF32 : Epi::AccumF32;
-  GS_TRY(forward_body(d, W, x, ws, st, lc));  // recompute from the checkpoint
+  GS_TRY(forward_body(d, W, x, ws, st, lc, true));  // recompute from the checkpoint
 
   // Weight gradients run on ws.side once their inputs exist (fork), the
   // data-gradient chain stays on st; every input a wgrad reads is left intact

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(int M, int N, int K, con
       else if (EPI == (int)Epi::AccumF32) ((float*)C)[o] += v;
       else if (EPI == (int)Epi::StoreGelu) { st((T*)C + o, v); st(G + o, gelu_f(ld((T*)C + o))); }
       else if (EPI == (int)Epi::MulGeluGrad) { st((T*)C + o, v); st((T*)C + o, ld((T*)C + o) * gelu_grad_f(ld(R + o))); }
+      else if (EPI == (int)Epi::Gelu) { st((T*)C + o, v); st((T*)C + o, gelu_f(ld((T*)C + o))); }
       else ((float*)C)[o] = v;
     }
   }
@@ -90,6 +91,7 @@ cudaError_t launch_epi(const GemmArgs& g, cudaStream_t s) {
     case Epi::StoreGelu: simt_gemm_kernel<T, AK, BKM, 3><<<grid, 256, 0, s>>>(g.M, g.N, g.K, A, B, g.C, (const T*)g.R, (T*)g.G, ldc); break;
     case Epi::StoreF32: simt_gemm_kernel<T, AK, BKM, 4><<<grid, 256, 0, s>>>(g.M, g.N, g.K, A, B, g.C, (const T*)g.R, (T*)g.G, ldc); break;
     case Epi::MulGeluGrad: simt_gemm_kernel<T, AK, BKM, 5><<<grid, 256, 0, s>>>(g.M, g.N, g.K, A, B, g.C, (const T*)g.R, (T*)g.G, ldc); break;
+    case Epi::Gelu: simt_gemm_kernel<T, AK, BKM, 6><<<grid, 256, 0, s>>>(g.M, g.N, g.K, A, B, g.C, (const T*)g.R, (T*)g.G, ldc); break;
   }
   return cudaGetLastError();
 }

@@ -299,6 +299,10 @@ __device__ __forceinline__ void epilogue_store(const float (&v)[32], int lane, i
         }
       }
     }
+    if constexpr (EPI == (int)Epi::Gelu) {  // the G of StoreGelu, without storing u
+#pragma unroll
+      for (int i = 0; i < 32; ++i) w[i] = gelu_fast(__bfloat162float(__float2bfloat16_rn(w[i])));
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint32_t a = sa + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
@@ -734,6 +738,7 @@ cudaError_t launch_epi(const GemmArgs& g, cudaStream_t s) {
     case Epi::StoreGelu: return launch<BN, A_MN, B_MN, 3, CG>(g, s);
     case Epi::StoreF32: return launch<BN, A_MN, B_MN, 4, CG>(g, s);
     case Epi::MulGeluGrad: return launch<BN, A_MN, B_MN, 5, CG>(g, s);
+    case Epi::Gelu: return launch<BN, A_MN, B_MN, 6, CG>(g, s);
   }
   return cudaErrorInvalidValue;
 }

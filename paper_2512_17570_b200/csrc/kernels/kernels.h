@@ -22,6 +22,7 @@ enum class Epi {
   StoreGelu = 3,    // C(dt) = acc, G(dt) = gelu(acc)
   StoreF32 = 4,     // Cf32 = acc
   MulGeluGrad = 5,  // C(dt) = acc * gelu'(R(dt))   (dgrad of FC2 fused with GELU backward)
+  Gelu = 6,         // C(dt) = gelu(acc)   (StoreGelu's G alone: FwdCompute keeps no u)
 };
 struct GemmArgs {
   int M = 0, N = 0, K = 0;

@@ -117,6 +117,22 @@ def test_tcgen05_fused_epilogues():
     x = R.float().clone().requires_grad_(True)
     torch.nn.functional.gelu(x, approximate="tanh").backward(ref.bfloat16().float())
     assert rel(du.float(), x.grad) < 5e-3
+    # GELU-only epilogue (FwdCompute): bit-identical to StoreGelu's G, on the
+    # tcgen05 path (pair tiles and a half-empty last pair) and the SIMT path
+    for (m, n, k) in [(M, N, K), (384, 2048, 512)]:
+        a = torch.randn(m, k, device=d).bfloat16()
+        b_ = torch.randn(n, k, device=d).bfloat16()
+        u2 = torch.empty(m, n, device=d, dtype=torch.bfloat16)
+        g2 = torch.empty_like(u2)
+        only = torch.empty_like(u2)
+        gemm(BF16, a, True, b_, True, m, n, k, 3, u2, G=g2)
+        gemm(BF16, a, True, b_, True, m, n, k, 6, only)
+        assert torch.equal(only, g2)
+        ref_s = torch.empty_like(u2)
+        gemm(BF16, a, True, b_, True, m, n, k, 6, ref_s, simt=True)
+        assert rel(ref_s.float(), g2.float()) < 5e-3
+    with pytest.raises(RuntimeError):
+        gemm(BF16, A, True, B, True, M, N, K, 7, out)
 
 
 @pytest.mark.parametrize("M,N,K", [(64, 64, 64), (100, 70, 33), (256, 192, 128)])
