@@ -18,7 +18,10 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
+#include <climits>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -164,15 +167,36 @@ __device__ __forceinline__ uint32_t pack(float a, float b) {
 // except to rescale O (rare: lazy rescaling below).
 constexpr int kBK2 = 64;
 constexpr int kKV2 = kBK2 * kD * 2;  // 16 KB
+constexpr int kKS2 = 2;  // K ring depth (V: 2)
 struct FaSmem2 {
   uint8_t Q[kTile];          // [2 d-chunks][128 rows][128 B]
-  uint8_t K[2][kKV2];        // [2 d-chunks][64 rows][128 B]
+  uint8_t K[kKS2][kKV2];     // [2 d-chunks][64 rows][128 B]
   uint8_t V[2][kKV2];
-  // K and V slots are released separately: K(kb) right after S(kb), so the
-  // load of K(kb+2) overlaps softmax(kb) instead of waiting for PV(kb)
-  uint64_t q_full, k_full[2], v_full[2], k_empty[2], v_empty[2], s_full[2], p_full[2], o_done;
+  // K and V have their own producers and release points: K(kb) is freed
+  // right after S(kb), V(kb) after PV(kb), so the load of K(kb+2) overlaps
+  // softmax(kb).  (A third K slot, tried, changes nothing: the GS_ATTN_TRACE
+  // timeline shows the S / PV MMAs of the two CTAs on an SM, not the loads,
+  // pacing the blocks.)
+  uint64_t q_full, k_full[kKS2], v_full[2], k_empty[kKS2], v_empty[2], s_full[2], p_full[2], o_done;
   uint32_t tmem;
 };
+
+// GS_ATTN_TRACE grid schedule: {smid, start, end} of this CTA (see attn_trace_end)
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void cta_stamp(long long* tr, int slot) {
+  if (!tr || threadIdx.x != 0) return;
+  long long* c = tr + 8 * 64 + 4 * ((long long)blockIdx.y * gridDim.x + blockIdx.x);
+  if (slot == 1) {
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+    c[0] = sm;
+  }
+  c[slot] = gtimer();
+}
 
 template <int POLY>  // POLY: every 4th exponential on the FMA pipes instead of the SFU
 __global__ void __launch_bounds__(256, 2)
@@ -191,6 +215,7 @@ __global__ void __launch_bounds__(256, 2)
   // GS_ATTN_TRACE: clock64 stamps of CTA (0, 0) (the heaviest tile):
   // 0 MMA S(kb) issued, 1 MMA P(kb) seen, 2 softmax S(kb) seen, 3 softmax
   // math done, 4 softmax P(kb) published, 5 producer K(kb), 6 producer V(kb)
+  cta_stamp(tr, 1);
   long long* trc = (tr && blockIdx.x == 0 && blockIdx.y == 0) ? tr : nullptr;
 #define GS_TRF(ev, i)                                       \
   do {                                                      \
@@ -199,10 +224,12 @@ __global__ void __launch_bounds__(256, 2)
 
   if (threadIdx.x == 0) {
     bar_init(&sm.q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kKS2; ++i) {
       bar_init(&sm.k_full[i], 1);
-      bar_init(&sm.v_full[i], 1);
       bar_init(&sm.k_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&sm.v_full[i], 1);
       bar_init(&sm.v_empty[i], 1);
       bar_init(&sm.s_full[i], 1);
       bar_init(&sm.p_full[i], 128);
@@ -220,18 +247,24 @@ __global__ void __launch_bounds__(256, 2)
   const uint32_t tmem = sm.tmem;  // S0: 0-63, S1: 64-127, O: 128-255
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (lane == 0) {  // Q, then the K ring
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_q)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_kv)) : "memory");
       bar_expect(&sm.q_full, kTile);
       for (int c = 0; c < 2; ++c) tma2d(sm.Q + c * 16384, &map_q, &sm.q_full, j * kD + 64 * c, row0 + q0);
       for (int kb = 0; kb < nblk; ++kb) {
-        const int buf = kb & 1;
-        bar_wait(&sm.k_empty[buf], ((kb >> 1) & 1) ^ 1);
-        bar_expect(&sm.k_full[buf], kKV2);
+        const int sl = kb % kKS2;
+        bar_wait(&sm.k_empty[sl], ((kb / kKS2) & 1) ^ 1);
+        bar_expect(&sm.k_full[sl], kKV2);
         for (int c = 0; c < 2; ++c)
-          tma2d(sm.K[buf] + c * 8192, &map_kv, &sm.k_full[buf], h + j * kD + 64 * c, row0 + kb * kBK2);
+          tma2d(sm.K[sl] + c * 8192, &map_kv, &sm.k_full[sl], h + j * kD + 64 * c, row0 + kb * kBK2);
         GS_TRF(5, kb);
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {  // the V ring
+      for (int kb = 0; kb < nblk; ++kb) {
+        const int buf = kb & 1;
         bar_wait(&sm.v_empty[buf], ((kb >> 1) & 1) ^ 1);
         bar_expect(&sm.v_full[buf], kKV2);
         for (int c = 0; c < 2; ++c)
@@ -244,10 +277,11 @@ __global__ void __launch_bounds__(256, 2)
       const uint32_t qa = su32(sm.Q);
       bar_wait(&sm.q_full, 0);
       auto issue_s = [&](int kb) {
-        const int buf = kb & 1;
-        bar_wait(&sm.k_full[buf], (kb >> 1) & 1);
+        const int buf = kb & 1, sl = kb % kKS2;
+        GS_TRF(7, kb);
+        bar_wait(&sm.k_full[sl], (kb / kKS2) & 1);
         fence_after();
-        const uint32_t ka = su32(sm.K[buf]);
+        const uint32_t ka = su32(sm.K[sl]);
 #pragma unroll
         for (int ks = 0; ks < kD / 16; ++ks)
           mma(tmem + buf * 64, sdesc(qa + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024),
@@ -255,7 +289,7 @@ __global__ void __launch_bounds__(256, 2)
               (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24),
               ks != 0);
         commit(&sm.s_full[buf]);
-        commit(&sm.k_empty[buf]);
+        commit(&sm.k_empty[sl]);
         GS_TRF(0, kb);
       };
       issue_s(0);
@@ -286,23 +320,29 @@ __global__ void __launch_bounds__(256, 2)
       if (r == 0) GS_TRF(2, kb);
       fence_after();
       float sv[kBK2];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t rr[32];
-        tld32(tmem + lane_base + buf * 64 + c * 32, rr);
+      {  // both TMEM loads in flight before one wait (raw scores)
+        uint32_t rr[2][32];
+        tld32(tmem + lane_base + buf * 64, rr[0]);
+        tld32(tmem + lane_base + buf * 64 + 32, rr[1]);
         tld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(rr[i]);  // raw scores
+        for (int i = 0; i < kBK2; ++i) sv[i] = __uint_as_float(rr[i >> 5][i & 31]);
       }
       const bool mask = (kb + 1) * kBK2 > q0;  // blocks crossing the diagonal
       // max over the raw scores (scale > 0 keeps the order); the log2-domain
-      // scale folds into the exponent's FFMA below
-      float mraw = -INFINITY;
+      // scale folds into the exponent's FFMA below.  Eight independent partial
+      // maxima / sums: a single 64-long dependent chain would leave the two
+      // softmax warps of an SMSP stalled on ALU latency.
+      float mp[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mp[k] = -INFINITY;
 #pragma unroll
       for (int i = 0; i < kBK2; ++i) {
         if (mask && kb * kBK2 + i > qrow) sv[i] = -INFINITY;
-        mraw = fmaxf(mraw, sv[i]);
+        mp[i & 7] = fmaxf(mp[i & 7], sv[i]);
       }
+      const float mraw = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
+                               fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
       const float mx = fmaxf(m_run, mraw * scale_log2);
       // Lazy rescaling: the running max only moves when the block max exceeds
       // it by more than 2^8 (P <= 256 stays exact in bf16 / fp32); O and l
@@ -312,14 +352,15 @@ __global__ void __launch_bounds__(256, 2)
       const bool bump = mx > m_run + 8.0f;
       const float m_new = bump ? mx : m_run;
       const float corr = bump ? ex2(m_run - mx) : 1.0f;
-      float rs = 0.0f;
+      float ps[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
       const float nm = -m_new;
 #pragma unroll
       for (int i = 0; i < kBK2; ++i) {
         const float x = fmaf(sv[i], scale_log2, nm);
         sv[i] = (POLY && (i & 3) == 3) ? ex2_poly(x) : ex2(x);
-        rs += sv[i];
+        ps[i & 7] += sv[i];
       }
+      const float rs = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       l_run = l_run * corr + rs;
       m_run = m_new;
       if (r == 0) GS_TRF(3, kb);
@@ -376,6 +417,7 @@ __global__ void __launch_bounds__(256, 2)
   }
   fence_before();
   __syncthreads();
+  cta_stamp(tr, 2);
   if (warp == 2) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
@@ -741,6 +783,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   // tr[ev * 64 + i]: 0 mma ps_full(i) seen, 1 mma S(i) issued, 2 softmax
   // s_full(i) seen, 3 softmax math done, 4 softmax P/dS written, 5 drain
   // dq_full(i) seen, 6 drain dq_empty(i) arrived, 7 producer Q(i) issued
+  cta_stamp(tr, 1);
   long long* trc = (tr && blockIdx.x == 0 && blockIdx.y == 0) ? tr : nullptr;
 #define GS_TR4(ev, i)                                            \
   do {                                                           \
@@ -975,6 +1018,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   }
   fence_before();
   __syncthreads();
+  cta_stamp(tr, 2);
   if (warp == 2) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -1009,23 +1053,46 @@ bool attention_tc_supported(DType dt, int s, int h, int H) {
 
 
 // GS_ATTN_TRACE=1: clock64 timeline of CTA (0,0) of the backward (stderr)
-static long long* attn_trace_begin(cudaStream_t st) {
+// Past the 8 x 64 event stamps, every CTA writes {smid, start, end}
+// (%globaltimer ns) at tr[512 + 4 * cta]: the whole-grid schedule.
+static long long* attn_trace_begin(cudaStream_t st, int ncta) {
   static const bool on = getenv("GS_ATTN_TRACE") != nullptr;
   if (!on) return nullptr;
   long long* tr = nullptr;
-  cudaMalloc(&tr, 8 * 64 * sizeof(long long));
-  cudaMemsetAsync(tr, 0, 8 * 64 * sizeof(long long), st);
+  const size_t n = 8 * 64 + 4 * (size_t)ncta;
+  cudaMalloc(&tr, n * sizeof(long long));
+  cudaMemsetAsync(tr, 0, n * sizeof(long long), st);
   return tr;
 }
-static void attn_trace_end(long long* tr, cudaStream_t st,
+static void attn_trace_end(long long* tr, cudaStream_t st, int ncta, int ny,
                            const char* legend = "0 mma_ps_full 1 mma_S_issue 2 sm_s_full 3 sm_math 4 sm_written "
                                                 "5 dq_full 6 dq_empty 7 prod_Q",
                            int t0_event = 7) {
   if (!tr) return;
   long long hbuf[8 * 64];
+  std::vector<long long> cta(4 * (size_t)ncta);
   cudaMemcpyAsync(hbuf, tr, sizeof(hbuf), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(cta.data(), tr + 8 * 64, cta.size() * sizeof(long long), cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
   cudaFree(tr);
+  {  // grid schedule: span, SM occupancy, CTA durations per blockIdx.y
+    long long t_lo = LLONG_MAX, t_hi = 0, last_start = 0, busy = 0;
+    std::vector<double> dur_y(ny, 0.0);
+    std::vector<int> n_y(ny, 0);
+    for (int c = 0; c < ncta; ++c) {
+      const long long a = cta[4 * c + 1], e = cta[4 * c + 2];
+      t_lo = std::min(t_lo, a);
+      t_hi = std::max(t_hi, e);
+      last_start = std::max(last_start, a);
+      busy += e - a;
+      dur_y[c / (ncta / ny)] += (double)(e - a);
+      n_y[c / (ncta / ny)] += 1;
+    }
+    fprintf(stderr, "[attn grid] ctas %d span %.1f us, last CTA starts at %.1f us, sum CTA time / (span x 148 SMs) = %.2f CTAs per SM\n",
+            ncta, (t_hi - t_lo) / 1e3, (last_start - t_lo) / 1e3, (double)busy / ((double)(t_hi - t_lo) * 148));
+    for (int y = 0; y < ny; ++y)
+      fprintf(stderr, "[attn grid] blockIdx.y %2d: mean CTA %.1f us\n", y, n_y[y] ? dur_y[y] / n_y[y] / 1e3 : 0.0);
+  }
   const long long t0 = hbuf[t0_event * 64];
   fprintf(stderr, "[attn trace] ev: %s\n", legend);
   for (int i = 0; i < 32; ++i) {
@@ -1062,10 +1129,11 @@ cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s,
     init2 = true;
   }
   count_launch();
-  long long* tr = attn_trace_begin(st);
+  long long* tr = attn_trace_begin(st, b * H * (s / kBQ));
   kern<<<dim3(b * H, s / kBQ), 256, smem, st>>>(mq, mkv, (bf16*)o, lse, s, h, H,
                                                              1.4426950408889634f / sqrtf((float)kD), tr);
-  attn_trace_end(tr, st, "0 mma_S_issue 1 mma_P_seen 2 sm_S_seen 3 sm_math 4 sm_P_pub 5 prod_K 6 prod_V", 5);
+  attn_trace_end(tr, st, b * H * (s / kBQ), s / kBQ,
+                 "0 mma_S_issue 1 mma_P_seen 2 sm_S_seen 3 sm_math 4 sm_P_pub 5 prod_K 6 prod_V 7 mma_S_enter", 5);
   return cudaGetLastError();
 }
 
@@ -1117,10 +1185,10 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
       init4 = true;
     }
     count_launch();
-    long long* tr = attn_trace_begin(st);
+    long long* tr = attn_trace_begin(st, b * H * (s / kBK));
     fa_bwd_tc4_kernel<<<dim3(b * H, s / kBK), kThreadsBwd, smem4, st>>>(mq, mq64, md, mdq, lse2, D, (bf16*)dqkv, s,
                                                                           h, H, 1.0f / sqrtf((float)kD), tr);
-    attn_trace_end(tr, st);
+    attn_trace_end(tr, st, b * H * (s / kBK), s / kBK);
     return cudaGetLastError();
   }
   if (variant == 3) {
@@ -1132,11 +1200,11 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
       init3 = true;
     }
     count_launch();
-    long long* tr = attn_trace_begin(st);
+    long long* tr = attn_trace_begin(st, 0);
     // v3 takes the log2-domain lse (lse2 = lse * log2 e, from fa_prep)
     fa_bwd_tc3_kernel<<<dim3(b * H, s / kBK), kThreadsBwd, smem3, st>>>(mq, mq64, md, mdq, lse2, D, (bf16*)dqkv, s,
                                                                           h, H, 1.0f / sqrtf((float)kD), tr);
-    attn_trace_end(tr, st);
+    attn_trace_end(tr, st, 0, 1);
     return cudaGetLastError();
   }
   return cudaErrorInvalidValue;  // GS_ATTN_BWD must be 3 or 4

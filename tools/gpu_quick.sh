@@ -1,7 +1,4 @@
 mkdir -p gpurun_out
-rm -f gpurun_out/ab.txt
-for r in 1 2 3; do for v in new old; do
-  if [ $v = old ]; then export GS_AB_KEEP_U=1; else unset GS_AB_KEEP_U; fi
-  timeout 600 python bench.py > gpurun_out/b.log 2>&1
-  echo "$v $(grep '^{' gpurun_out/b.log | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"], d["clocks"]["sm_mhz"])')" >> gpurun_out/ab.txt
-done; done
+timeout 300 python tools/attn_grid_trace.py > gpurun_out/attn_grid.txt 2>&1
+timeout 300 python tools/attn_accuracy.py > gpurun_out/attn_acc.txt 2>&1
+timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q -k "attention or fused" > gpurun_out/t_attn.log 2>&1; echo "rc=$?" >> gpurun_out/t_attn.log
