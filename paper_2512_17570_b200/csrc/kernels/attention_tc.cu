@@ -424,6 +424,234 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
+// ------------------------------------------------------------ forward v3
+// Two 128-query tiles per CTA and 128-key blocks, one CTA per SM (all 512
+// TMEM columns: S0 | S1 | O0 | O1).  The S MMAs run at N = 128, where the
+// SMEM operand stream (Q and K rows, 8 KB per 64-cycle MMA) keeps up with the
+// tensor pipe — the N = 64 S MMAs of v2 run SMEM-bound — and the two tiles
+// ping-pong: while softmax WG t works on S_t(kb+1), the pipe runs
+// PV_{1-t}(kb) and S_{1-t}(kb+1).  P_t (bf16) is tcgen05.st-ed over S_t and
+// O_t += P_t V is a TS-MMA.  Since each tile's S(kb) is issued after its
+// PV(kb-1), seeing S_t(kb) means O_t is final for a rescale — no wait.
+constexpr int kThreadsF3 = 352;  // w0 Q+K, w1 MMA + TMEM, w2-5 / w6-9 softmax tiles 0 / 1, w10 V
+struct FaSmem3 {
+  uint8_t Q[2][kTile];  // per tile: [2 d-chunks][128 rows][128 B]
+  uint8_t K[2][kTile];  // 2-slot ring of 128-key blocks
+  uint8_t V[2][kTile];
+  uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], o_done[2];
+  uint32_t tmem;
+};
+
+template <int POLY>  // exponentials on the FMA pipes: 0 none, 1 one in four, 2 one in two
+__global__ void __launch_bounds__(kThreadsF3, 1)
+    fa_fwd_tc3_kernel(const __grid_constant__ CUtensorMap map_t, bf16* __restrict__ o, float* __restrict__ lse, int s,
+                      int h, int H, float scale_log2, long long* __restrict__ tr) {
+  extern __shared__ __align__(1024) uint8_t raw3[];
+  FaSmem3& sm = *reinterpret_cast<FaSmem3*>(raw3);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qp = gridDim.y - 1 - blockIdx.y;  // heaviest tile pairs first (LPT)
+  const int bh = blockIdx.x, bi = bh / H, j = bh % H;
+  const int row0 = bi * s, q0 = qp * 2 * kBQ;
+  const int nblk0 = (q0 + kBQ) / kBK, nblk1 = nblk0 + 1;  // causal: tile t sees keys < q0 + 128 (t + 1)
+  cta_stamp(tr, 1);
+  if (threadIdx.x == 0) {
+    bar_init(&sm.q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&sm.k_full[i], 1);
+      bar_init(&sm.k_empty[i], 1);
+      bar_init(&sm.v_full[i], 1);
+      bar_init(&sm.v_empty[i], 1);
+      bar_init(&sm.s_full[i], 1);
+      bar_init(&sm.p_full[i], 128);
+      bar_init(&sm.o_done[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = sm.tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {  // Q of both tiles, then the K ring
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_t)) : "memory");
+      bar_expect(&sm.q_full, 2 * kTile);
+      for (int t = 0; t < 2; ++t)
+        for (int c = 0; c < 2; ++c)
+          tma2d(sm.Q[t] + c * 16384, &map_t, &sm.q_full, j * kD + 64 * c, row0 + q0 + t * kBQ);
+      for (int kb = 0; kb < nblk1; ++kb) {
+        const int sl = kb & 1;
+        bar_wait(&sm.k_empty[sl], ((kb >> 1) & 1) ^ 1);
+        bar_expect(&sm.k_full[sl], kTile);
+        for (int c = 0; c < 2; ++c)
+          tma2d(sm.K[sl] + c * 16384, &map_t, &sm.k_full[sl], h + j * kD + 64 * c, row0 + kb * kBK);
+      }
+    }
+  } else if (warp == 10) {
+    if (lane == 0) {  // the V ring
+      for (int kb = 0; kb < nblk1; ++kb) {
+        const int sl = kb & 1;
+        bar_wait(&sm.v_empty[sl], ((kb >> 1) & 1) ^ 1);
+        bar_expect(&sm.v_full[sl], kTile);
+        for (int c = 0; c < 2; ++c)
+          tma2d(sm.V[sl] + c * 16384, &map_t, &sm.v_full[sl], 2 * h + j * kD + 64 * c, row0 + kb * kBK);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      bar_wait(&sm.q_full, 0);
+      auto issue_s = [&](int t, int kb) {  // S_t = Q_t K(kb)^T into columns [128 t, 128 t + 128)
+        const uint32_t qa = su32(sm.Q[t]), ka = su32(sm.K[kb & 1]);
+#pragma unroll
+        for (int ks = 0; ks < kD / 16; ++ks)
+          mma(tmem + t * 128, desc_kmajor(qa, ks), desc_kmajor(ka, ks), idesc(false), ks != 0);
+        commit(&sm.s_full[t]);
+      };
+      auto wait_k = [&](int kb) {
+        bar_wait(&sm.k_full[kb & 1], (kb >> 1) & 1);
+        fence_after();
+      };
+      auto issue_pv = [&](int t, int kb) {  // O_t += P_t V(kb), P_t from TMEM (8 columns per 16 keys)
+        const uint32_t va = su32(sm.V[kb & 1]);
+#pragma unroll
+        for (int ks = 0; ks < kBK / 16; ++ks)
+          mma_ts(tmem + 256 + t * 128, tmem + t * 128 + ks * 8, desc_mnmajor(va, ks), idesc(true), (kb | ks) != 0);
+        commit(&sm.o_done[t]);
+      };
+      wait_k(0);
+      issue_s(0, 0);
+      issue_s(1, 0);
+      commit(&sm.k_empty[0]);
+      for (int kb = 0; kb < nblk1; ++kb) {
+        bar_wait(&sm.v_full[kb & 1], (kb >> 1) & 1);
+        bool k_ready = false;
+        if (kb < nblk0) {
+          bar_wait(&sm.p_full[0], kb & 1);
+          fence_after();
+          issue_pv(0, kb);
+          if (kb + 1 < nblk0) {
+            wait_k(kb + 1);
+            k_ready = true;
+            issue_s(0, kb + 1);
+          }
+        }
+        bar_wait(&sm.p_full[1], kb & 1);
+        fence_after();
+        issue_pv(1, kb);
+        commit(&sm.v_empty[kb & 1]);
+        if (kb + 1 < nblk1) {
+          if (!k_ready) wait_k(kb + 1);
+          issue_s(1, kb + 1);
+          commit(&sm.k_empty[(kb + 1) & 1]);
+        }
+      }
+    }
+  } else if (warp >= 2 && warp < 10) {
+    const int t = (warp - 2) >> 2;
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int r = quarter * 32 + lane;
+    const int q0t = q0 + t * kBQ, qrow = q0t + r;
+    const int nb = t ? nblk1 : nblk0;
+    const uint32_t lb = (uint32_t)(quarter * 32) << 16;
+    const uint32_t St = tmem + lb + t * 128, Ot = tmem + lb + 256 + t * 128;
+    float m_run = -INFINITY, l_run = 0.0f;
+    for (int kb = 0; kb < nb; ++kb) {
+      bar_wait(&sm.s_full[t], kb & 1);
+      fence_after();
+      float sv[kBK];
+      {
+        uint32_t rr[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tld32(St + c * 32, rr[c]);
+        tld_wait();
+#pragma unroll
+        for (int i = 0; i < kBK; ++i) sv[i] = __uint_as_float(rr[i >> 5][i & 31]);
+      }
+      if ((kb + 1) * kBK > q0t) {  // the diagonal block: keys past the row masked
+        const int lim = qrow - kb * kBK;
+#pragma unroll
+        for (int i = 0; i < kBK; ++i)
+          if (i > lim) sv[i] = -INFINITY;
+      }
+      float mp[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mp[k] = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < kBK; ++i) mp[i & 7] = fmaxf(mp[i & 7], sv[i]);
+      const float mraw = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
+                               fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+      const float mx = fmaxf(m_run, mraw * scale_log2);
+      const bool bump = mx > m_run + 8.0f;  // lazy rescaling, as in v2
+      const float m_new = bump ? mx : m_run;
+      const float corr = bump ? ex2(m_run - mx) : 1.0f;
+      const float nm = -m_new;
+      float ps[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int i = 0; i < kBK; ++i) {
+        const float x = fmaf(sv[i], scale_log2, nm);
+        sv[i] = ((POLY == 1 && (i & 3) == 3) || (POLY == 2 && (i & 1))) ? ex2_poly(x) : ex2(x);
+        ps[i & 7] += sv[i];
+      }
+      l_run = l_run * corr + (((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7])));
+      m_run = m_new;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {  // P_t -> TMEM over S_t (64 columns of bf16 pairs)
+        uint32_t pk[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) pk[k] = pack(sv[64 * half + 2 * k], sv[64 * half + 2 * k + 1]);
+        tst32(St + half * 32, pk);
+      }
+      if (kb > 0 && __any_sync(0xffffffffu, bump)) {  // PV_t(kb-1) is complete (see above)
+#pragma unroll
+        for (int c = 0; c < kD / 32; ++c) {
+          uint32_t rr[32];
+          tld32(Ot + c * 32, rr);
+          tld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * corr);
+          tst32(Ot + c * 32, rr);
+        }
+      }
+      tst_wait();
+      fence_before();
+      bar_arrive(&sm.p_full[t]);
+    }
+    // After the last arrive o_done[t] is in phase nb-1 (PV_t(nb-1) pending)
+    // or nb; earlier phases completed before S_t(nb-1) did.
+    bar_wait(&sm.o_done[t], (nb - 1) & 1);
+    fence_after();
+    const float inv = 1.0f / l_run;
+    bf16* orow = o + (long long)(row0 + qrow) * h + j * kD;
+#pragma unroll
+    for (int c = 0; c < kD / 32; ++c) {
+      uint32_t rr[32];
+      tld32(Ot + c * 32, rr);
+      tld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack(__uint_as_float(rr[8 * q]) * inv, __uint_as_float(rr[8 * q + 1]) * inv);
+        w.y = pack(__uint_as_float(rr[8 * q + 2]) * inv, __uint_as_float(rr[8 * q + 3]) * inv);
+        w.z = pack(__uint_as_float(rr[8 * q + 4]) * inv, __uint_as_float(rr[8 * q + 5]) * inv);
+        w.w = pack(__uint_as_float(rr[8 * q + 6]) * inv, __uint_as_float(rr[8 * q + 7]) * inv);
+        *reinterpret_cast<uint4*>(orow + c * 32 + 8 * q) = w;
+      }
+    }
+    lse[(long long)bh * s + qrow] = (m_run + log2f(l_run)) * 0.6931471805599453f;
+  }
+  fence_before();
+  __syncthreads();
+  cta_stamp(tr, 2);
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 // ============================================================== backward
 // One CTA per (128-key block, batch x head); loop over 64-query blocks from
 // the diagonal down.  Per block (TMEM columns in brackets):
@@ -1113,6 +1341,33 @@ cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s,
                   strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
+  }
+  static const int fwd_variant = [] {  // GS_ATTN_FWD=2 keeps the 64-key two-CTA kernel
+    const char* e = getenv("GS_ATTN_FWD");
+    return e ? atoi(e) : 3;
+  }();
+  if (fwd_variant == 3 && s % (2 * kBQ) == 0) {
+    const int smem3 = (int)sizeof(FaSmem3);
+    static const int poly3 = [] {
+      const char* e = getenv("GS_ATTN_POLY");
+      return e ? atoi(e) : 0;
+    }();
+    auto kern3 = poly3 == 2 ? fa_fwd_tc3_kernel<2> : poly3 == 1 ? fa_fwd_tc3_kernel<1> : fa_fwd_tc3_kernel<0>;
+    static bool init3 = false;
+    if (!init3) {
+      for (auto k : {fa_fwd_tc3_kernel<0>, fa_fwd_tc3_kernel<1>, fa_fwd_tc3_kernel<2>}) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+        if (e != cudaSuccess) return e;
+      }
+      init3 = true;
+    }
+    count_launch();
+    const int ny = s / (2 * kBQ);
+    long long* tr = attn_trace_begin(st, b * H * ny);
+    kern3<<<dim3(b * H, ny), kThreadsF3, smem3, st>>>(mq, (bf16*)o, lse, s, h, H,
+                                                                   1.4426950408889634f / sqrtf((float)kD), tr);
+    attn_trace_end(tr, st, b * H * ny, ny, "(v3: grid schedule only)", 0);
+    return cudaGetLastError();
   }
   const int smem = (int)sizeof(FaSmem2);
   static const int poly = [] {  // GS_ATTN_POLY=1: FMA-pipe exp2 for 1 in 4 elements
