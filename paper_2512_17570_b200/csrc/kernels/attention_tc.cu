@@ -987,7 +987,7 @@ struct FaBwdSmem4 {
   uint8_t K[kTile], V[kTile];
   uint8_t Q[kQS4][kHalf], dO[kQS4][kHalf];
   uint8_t dST[kPT];
-  float dq_stage[kDqRows4][kD];
+  float dq_stage[2][kDqRows4][kD];  // double-buffered: piece p+1 is written while piece p's reduce reads
   float L[kQS4][kBQb], D[kQS4][kBQb];
   uint64_t kv_full, q_full[kQS4], q_empty[kQS4], s_full[2], ps_full, pds_empty, dq_full[2], dq_empty[2], mma_done;
   uint32_t tmem;
@@ -1207,10 +1207,12 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       if (r == 0) GS_TR4(6, i);
 #pragma unroll
       for (int half = 0; half < kBQb / kDqRows4; ++half) {
-        if (r == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
+        const int sb = half & 1;  // pieces per block is even: piece parity == half parity
+        // the reduce that last read this buffer (two pieces back) is done
+        if (r == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         asm volatile("bar.sync 3, 128;" ::: "memory");
 #pragma unroll
-        for (int q = 0; q < kDqRows4; ++q) sm.dq_stage[q][r] = __uint_as_float(rr[half * kDqRows4 + q]) * scale;
+        for (int q = 0; q < kDqRows4; ++q) sm.dq_stage[sb][q][r] = __uint_as_float(rr[half * kDqRows4 + q]) * scale;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync 3, 128;" ::: "memory");
         if (r == 0) {
@@ -1218,7 +1220,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
           asm volatile(
               "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                   reinterpret_cast<uint64_t>(&map_dq)),
-              "r"(su32(&sm.dq_stage[0][0])), "r"(j * kD), "r"(row0 + q0)
+              "r"(su32(&sm.dq_stage[sb][0][0])), "r"(j * kD), "r"(row0 + q0)
               : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
