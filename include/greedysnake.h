@@ -111,6 +111,12 @@ int gs_find_optimal_config(const gs_model_spec* model, const gs_machine_spec* ma
 /* grid_search_config(model, machine, M, alpha, steps)  planner.hpp:38-40 */
 int gs_grid_search_config(const gs_model_spec* model, const gs_machine_spec* machine, int num_microbatches,
                           double alpha, int steps, gs_planner_solution* out);
+/* io_roofline(model, machine, batch_samples, x_opt) -> samples/s    roofline.hpp:12-13
+   (+inf when no optimizer state is SSD-resident);
+   compute_roofline(model, machine) -> samples/s                      roofline.hpp:17 */
+int gs_io_roofline(const gs_model_spec* model, const gs_machine_spec* machine, unsigned long long batch_samples,
+                   double x_opt, double* out);
+int gs_compute_roofline(const gs_model_spec* model, const gs_machine_spec* machine, double* out);
 /* solve_lp(A, b, c) over dense row-major A [m][n]; x[n]  simplex.hpp:17 */
 int gs_solve_lp(int m, int n, const double* A, const double* b, const double* c, int* feasible, int* bounded,
                 double* objective, double* x);
@@ -179,6 +185,15 @@ int gs_engine_set_profiling(gs_engine* engine, int stride);
 int gs_engine_set_trace(gs_engine* engine, int on);
 /* trace of the last run (last <= 3 iterations when record_trace was set) */
 int gs_engine_trace(gs_engine* engine, gs_trace_record* out, int cap, int* n);
+
+/* --------------------------------------------------------------- context */
+/* One context per device: selects the device and owns a non-blocking stream
+   the kernel entry points below can be given (gs_ctx_stream). */
+typedef struct gs_ctx gs_ctx;
+int gs_ctx_create(int device, gs_ctx** out);
+void* gs_ctx_stream(const gs_ctx* ctx);
+int gs_ctx_sync(gs_ctx* ctx);
+void gs_ctx_destroy(gs_ctx* ctx);
 
 /* --------------------------------------------------------------- kernels */
 /* dtype: 0 = fp32, 1 = bf16.  stream: cudaStream_t (NULL = legacy default). */

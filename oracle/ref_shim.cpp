@@ -10,6 +10,7 @@
 
 #include "offsim/json_io.hpp"
 #include "offsim/planner.hpp"
+#include "offsim/roofline.hpp"
 #include "offsim/simplex.hpp"
 #include "offsim/schedule.hpp"
 #include "offsim/simulator.hpp"
@@ -89,6 +90,13 @@ int ref_planner(int mode, const int* model, const double* machine, int mbs, doub
                           s.split.x_param, s.split.x_opt, s.t_fwd_stage, s.t_bwd_stage, s.iteration_estimate,
                           s.throughput_estimate};
     std::memcpy(out, v, sizeof(v));
+  });
+}
+// out = {io_roofline(model, machine, batch, x_opt), compute_roofline(model, machine)}  (roofline.cpp:8-33)
+int ref_rooflines(const int* model, const double* machine, unsigned long long batch, double x_opt, double* out) {
+  return guard([&] {
+    out[0] = io_roofline(model_of(model), machine_of(machine), batch, x_opt);
+    out[1] = compute_roofline(model_of(model), machine_of(machine));
   });
 }
 // solve_lp over a dense row-major A [m x n]: out = {feasible, bounded, objective, x...}

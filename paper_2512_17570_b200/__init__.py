@@ -130,6 +130,15 @@ def lib() -> C.CDLL:
                                              C.POINTER(C.c_void_p)]
         L.gs_adam_step_packed.argtypes = [C.c_float] * 5 + [C.c_int, C.c_float, C.c_void_p, C.c_void_p, C.c_void_p,
                                                             C.c_int, C.c_int64, C.c_void_p]
+        L.gs_io_roofline.argtypes = [C.POINTER(_ModelSpec), C.POINTER(_Machine), C.c_ulonglong, C.c_double,
+                                     C.POINTER(C.c_double)]
+        L.gs_compute_roofline.argtypes = [C.POINTER(_ModelSpec), C.POINTER(_Machine), C.POINTER(C.c_double)]
+        L.gs_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+        L.gs_ctx_stream.argtypes = [C.c_void_p]
+        L.gs_ctx_stream.restype = C.c_void_p
+        L.gs_ctx_sync.argtypes = [C.c_void_p]
+        L.gs_ctx_destroy.argtypes = [C.c_void_p]
+        L.gs_ctx_destroy.restype = None
         _lib = L
     return _lib
 
@@ -352,6 +361,55 @@ def grid_search_config(model: ModelSpec, machine: MachineSpec, num_microbatches:
     check(lib().gs_grid_search_config(C.byref(model._c()), C.byref(machine._c()), num_microbatches,
                                       C.c_double(alpha), steps, C.byref(out)))
     return _solution(out)
+
+
+def io_roofline(model: ModelSpec, machine: MachineSpec, batch_samples: int, x_opt: float = 0.0) -> float:
+    """Samples/s bound from the SSD optimizer-state round trip (roofline.hpp:12-13); inf without SSD bytes."""
+    out = C.c_double()
+    check(lib().gs_io_roofline(C.byref(model._c()), C.byref(machine._c()), batch_samples, C.c_double(x_opt),
+                               C.byref(out)))
+    return out.value
+
+
+def compute_roofline(model: ModelSpec, machine: MachineSpec) -> float:
+    """Samples/s bound from the calibrated per-layer compute times (roofline.hpp:17)."""
+    out = C.c_double()
+    check(lib().gs_compute_roofline(C.byref(model._c()), C.byref(machine._c()), C.byref(out)))
+    return out.value
+
+
+class Context:
+    """One per device (gs_ctx_create): selects the device, owns a non-blocking
+    stream for the kernel entry points."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().gs_ctx_create(device, C.byref(h)))
+        self.handle = h
+
+    @property
+    def stream(self) -> C.c_void_p:
+        return C.c_void_p(lib().gs_ctx_stream(self.handle))
+
+    def sync(self) -> None:
+        check(lib().gs_ctx_sync(self.handle))
+
+    def close(self) -> None:
+        if self.handle:
+            lib().gs_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def solve_lp(A, b, c):

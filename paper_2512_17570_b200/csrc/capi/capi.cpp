@@ -56,6 +56,11 @@ int guarded(F&& f) {
   }
 }
 
+int fail(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+
 int cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return GS_OK;
   g_error = std::string("CUDA: ") + cudaGetErrorString(e);
@@ -237,6 +242,13 @@ int gs_grid_search_config(const gs_model_spec* model, const gs_machine_spec* mac
                  out);
   });
 }
+int gs_io_roofline(const gs_model_spec* model, const gs_machine_spec* machine, unsigned long long batch_samples,
+                   double x_opt, double* out) {
+  return guarded([&] { *out = offsim::io_roofline(model_of(model), machine_of(machine), batch_samples, x_opt); });
+}
+int gs_compute_roofline(const gs_model_spec* model, const gs_machine_spec* machine, double* out) {
+  return guarded([&] { *out = offsim::compute_roofline(model_of(model), machine_of(machine)); });
+}
 int gs_solve_lp(int m, int n, const double* A, const double* b, const double* c, int* feasible, int* bounded,
                 double* objective, double* x) {
   return guarded([&] {
@@ -333,6 +345,39 @@ int gs_engine_trace(gs_engine* engine, gs_trace_record* out, int cap, int* n) {
       out[i] = {r.iteration, r.task, static_cast<int>(r.resource), r.t_start_ms, r.t_end_ms, r.bytes, r.physical_bytes};
     }
   });
+}
+
+// ----------------------------------------------------------------- context
+struct gs_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+};
+int gs_ctx_create(int device, gs_ctx** out) {
+  if (!out) return fail(GS_ERR_VALIDATION, "gs_ctx_create: out is null");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+    (void)cudaGetLastError();
+    return fail(GS_ERR_CUDA, "gs_ctx_create: no CUDA device " + std::to_string(device));
+  }
+  auto c = std::make_unique<gs_ctx>();
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(GS_ERR_CUDA, std::string("gs_ctx_create: ") + cudaGetErrorString(cudaGetLastError()));
+  *out = c.release();
+  return GS_OK;
+}
+void* gs_ctx_stream(const gs_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+int gs_ctx_sync(gs_ctx* ctx) {
+  if (!ctx) return fail(GS_ERR_VALIDATION, "gs_ctx_sync: null context");
+  return cuda_status(cudaStreamSynchronize(ctx->stream));
+}
+void gs_ctx_destroy(gs_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->stream) {
+    cudaSetDevice(ctx->device);
+    cudaStreamDestroy(ctx->stream);
+  }
+  delete ctx;
 }
 
 // ----------------------------------------------------------------- kernels

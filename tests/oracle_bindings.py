@@ -216,6 +216,16 @@ def ref_planner(mode: str, model, machine, mbs=1, alpha=0.0, steps=100):
     return tuple(out)
 
 
+def ref_rooflines(model, machine, batch, x_opt):
+    """(io_roofline, compute_roofline) of the reference (oracle/_ref)."""
+    lib = ref()
+    out = (C.c_double * 2)()
+    rc = lib.ref_rooflines(model, (C.c_double * 13)(*machine), C.c_ulonglong(batch), C.c_double(x_opt), out)
+    if rc != 0:
+        raise RuntimeError(f"reference rc={rc}: {lib.ref_last_error().decode()}")
+    return out[0], out[1]
+
+
 def ref_solve_lp(A, b, c):
     lib = ref()
     m, n = len(A), len(c)

@@ -40,3 +40,25 @@ def test_version_and_error_channel():
 def test_product_library_does_not_link_the_oracle():
     so = open(gs.LIB_PATH, "rb").read()
     assert b"gso_train" not in so and b"liboracle" not in so and b"ref_plan_json" not in so
+
+
+def test_context_rejects_a_missing_device():
+    # no compute: device -1 never exists (CPU container or GPU box alike)
+    try:
+        gs.Context(-1)
+    except gs.OffsimError as e:
+        assert "no CUDA device" in str(e)
+    else:
+        raise AssertionError("gs_ctx_create(-1) succeeded")
+
+
+def test_io_roofline_is_infinite_without_ssd_state():
+    model = gs.ModelSpec(24, 2048, 16, 2048, 2, 2, 4, 3, 1)
+    m = gs.MachineSpec(gpu_mem_bytes=180 << 30, cpu_usable_dram_bytes=1 << 40, pcie_h2d_bw=5e10, pcie_d2h_bw=5e10,
+                       ssd_read_bw=2.5e9, ssd_write_bw=2.5e9, fwd_compute_time_per_layer_per_mb=4e-4,
+                       bwd_compute_time_per_layer_per_mb=1.2e-3, cpu_step_throughput=1e10, fixed_overhead_time=0.0,
+                       num_gpus=1, gpu_working_set_bytes=1 << 30, ssd_duplex=True)
+    assert gs.io_roofline(model, m, 32, 1.0) == float("inf")
+    finite = gs.io_roofline(model, m, 32, 0.0)
+    # 14.5 GB of optimizer state read and written (duplex) per 32 samples
+    assert abs(finite - 32 / (12 * 50331648 * 24 / 2.5e9)) / finite < 1e-6

@@ -313,3 +313,16 @@ def test_layer_bf16_tensor_core_path_tracks_fp32():
         out[dt] = (Y.float(), DX.float(), DW)
     for a, bb in zip(out[BF16], out[F32]):
         assert rel(a, bb) < 3e-2
+
+
+def test_context_stream_runs_kernels():
+    """gs_ctx_create / gs_ctx_stream: a GEMM enqueued on the context's stream."""
+    d = dev()
+    A = torch.randn(256, 128, device=d).bfloat16()
+    B = torch.randn(256, 128, device=d).bfloat16()
+    out = torch.empty(256, 256, device=d, dtype=torch.bfloat16)
+    with gs.Context(0) as ctx:
+        lib = gs.lib()
+        gs.check(lib.gs_gemm(BF16, 256, 256, 128, ptr(A), 1, ptr(B), 1, ptr(out), None, None, 0, ctx.stream))
+        ctx.sync()
+    assert rel(out.float(), A.float() @ B.float().t()) < 5e-3

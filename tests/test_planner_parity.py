@@ -119,3 +119,20 @@ def test_solve_lp_matches_reference():
                 for i in range(m):
                     assert sum(A[i][j] * x[j] for j in range(n)) <= b[i] + 1e-7
                 assert min(x) >= -1e-9
+
+
+@requires_reference
+@pytest.mark.parametrize("seed", range(20))
+def test_rooflines_match_reference(seed):
+    """io_roofline / compute_roofline (roofline.cpp:8-33) through the C-ABI."""
+    rng = random.Random(1000 + seed)
+    m, arr = machine(rng)
+    n, h, dp = rng.randint(2, 96), rng.choice([64, 2048, 8192]), rng.choice([1, 2, 8])
+    model = gs.ModelSpec(n, h, 4, 256, 2, 2, 4, 3, dp)
+    x_opt = rng.choice([0.0, 0.25, 0.5, 1.0])
+    batch = rng.choice([1, 4, 64])
+    io_ref, comp_ref = ob.ref_rooflines(ob.model_array(n, h, 4, 256, 2, dp=dp), arr, batch, x_opt)
+    io = gs.io_roofline(model, m, batch, x_opt)
+    comp = gs.compute_roofline(model, m)
+    assert (io == io_ref == float("inf")) or close(io, io_ref)
+    assert close(comp, comp_ref)
