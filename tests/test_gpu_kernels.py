@@ -162,7 +162,9 @@ def attn_reference(qkv, b, s, h, H):
                                                (BF16, 2, 2048, 2048, 16, 0.5), (F32, 2, 32, 64, 4, 0.5),
                                                (BF16, 2, 32, 64, 4, 0.5),
                                                # large scores: the running max jumps by >2^8 (lazy O rescale path)
-                                               (BF16, 1, 1024, 512, 4, 2.5), (BF16, 2, 512, 256, 2, "ramp")])
+                                               (BF16, 1, 1024, 512, 4, 2.5), (BF16, 2, 512, 256, 2, "ramp"),
+                                               # s % 256 == 128: the 64-key two-CTA forward (v2)
+                                               (BF16, 2, 384, 512, 4, 0.5), (BF16, 1, 640, 256, 2, 2.5)])
 def test_attention_fwd_bwd(dtype, b, s, h, H, amp):
     d = dev()
     tdt = torch.bfloat16 if dtype == BF16 else torch.float32
