@@ -157,20 +157,6 @@ __device__ __forceinline__ uint32_t pack(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
 }
-// Blackwell paired fp32 ops (FFMA2 / FADD2): two lanes' worth of work per
-// issue slot, each lane rounded exactly as FFMA / FADD.
-__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0, float c1) {
-  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n}"
-      : "=f"(d0), "=f"(d1)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
-}
-__device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
-  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n}"
-      : "=f"(d0), "=f"(d1)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
 
 // ------------------------------------------------------------ forward v2
 // 64-key blocks: 96 KB of shared memory and 256 TMEM columns per CTA, so two
@@ -447,7 +433,7 @@ __global__ void __launch_bounds__(256, 2)
 // PV_{1-t}(kb) and S_{1-t}(kb+1).  P_t (bf16) is tcgen05.st-ed over S_t and
 // O_t += P_t V is a TS-MMA.  Since each tile's S(kb) is issued after its
 // PV(kb-1), seeing S_t(kb) means O_t is final for a rescale — no wait.
-constexpr int kThreadsF3 = 320;  // w0 loads, w1 MMA + TMEM, w2-5 / w6-9 softmax tiles 0 / 1 (<= 200 registers)
+constexpr int kThreadsF3 = 352;  // w0 Q+K, w1 MMA + TMEM, w2-5 / w6-9 softmax tiles 0 / 1, w10 V
 struct FaSmem3 {
   uint8_t Q[2][kTile];  // per tile: [2 d-chunks][128 rows][128 B]
   uint8_t K[2][kTile];  // 2-slot ring of 128-key blocks
@@ -491,7 +477,7 @@ __global__ void __launch_bounds__(kThreadsF3, 1)
   const uint32_t tmem = sm.tmem;
 
   if (warp == 0) {
-    if (lane == 0) {  // Q of both tiles, then K(kb), V(kb) through their 2-slot rings
+    if (lane == 0) {  // Q of both tiles, then the K ring
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_t)) : "memory");
       bar_expect(&sm.q_full, 2 * kTile);
       for (int t = 0; t < 2; ++t)
@@ -503,6 +489,12 @@ __global__ void __launch_bounds__(kThreadsF3, 1)
         bar_expect(&sm.k_full[sl], kTile);
         for (int c = 0; c < 2; ++c)
           tma2d(sm.K[sl] + c * 16384, &map_t, &sm.k_full[sl], h + j * kD + 64 * c, row0 + kb * kBK);
+      }
+    }
+  } else if (warp == 10) {
+    if (lane == 0) {  // the V ring
+      for (int kb = 0; kb < nblk1; ++kb) {
+        const int sl = kb & 1;
         bar_wait(&sm.v_empty[sl], ((kb >> 1) & 1) ^ 1);
         bar_expect(&sm.v_full[sl], kTile);
         for (int c = 0; c < 2; ++c)
@@ -598,26 +590,21 @@ __global__ void __launch_bounds__(kThreadsF3, 1)
       const float corr = bump ? ex2(m_run - mx) : 1.0f;
       const float nm = -m_new;
       float ps[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
-      // exponentials in pairs (FFMA2 for the argument, FADD2 into the eight
-      // partial sums: element i still lands in partial i % 8); each 64-key
-      // half of P goes to TMEM as soon as it exists
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
+      for (int i = 0; i < kBK; ++i) {
+        const float x = fmaf(sv[i], scale_log2, nm);
+        sv[i] = ((POLY == 1 && (i & 3) == 3) || (POLY == 2 && (i & 1))) ? ex2_poly(x) : ex2(x);
+        ps[i & 7] += sv[i];
+      }
+      l_run = l_run * corr + (((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7])));
+      m_run = m_new;
 #pragma unroll
-        for (int i = 64 * half; i < 64 * half + 64; i += 2) {
-          float x0, x1;
-          ffma2(x0, x1, sv[i], sv[i + 1], scale_log2, scale_log2, nm, nm);
-          sv[i] = ex2(x0);
-          sv[i + 1] = ((POLY == 1 && (i & 3) == 2) || POLY == 2) ? ex2_poly(x1) : ex2(x1);
-          fadd2(ps[i & 7], ps[(i & 7) + 1], ps[i & 7], ps[(i & 7) + 1], sv[i], sv[i + 1]);
-        }
-        uint32_t pk[32];  // P_t -> TMEM over S_t (32 columns of bf16 pairs per half)
+      for (int half = 0; half < 2; ++half) {  // P_t -> TMEM over S_t (64 columns of bf16 pairs)
+        uint32_t pk[32];
 #pragma unroll
         for (int k = 0; k < 32; ++k) pk[k] = pack(sv[64 * half + 2 * k], sv[64 * half + 2 * k + 1]);
         tst32(St + half * 32, pk);
       }
-      l_run = l_run * corr + (((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7])));
-      m_run = m_new;
       if (kb > 0 && __any_sync(0xffffffffu, bump)) {  // PV_t(kb-1) is complete (see above)
 #pragma unroll
         for (int c = 0; c < kD / 32; ++c) {
