@@ -1,11 +1,10 @@
 mkdir -p gpurun_out
-L=paper_2512_17570_b200/libgreedysnake.so
-cp $L /tmp/lib_new.so
-rm -f gpurun_out/attn_ab.txt
-for r in 1 2 3; do
-  cp /tmp/lib_new.so $L; echo "new $(timeout 120 python tools/gemm_probe.py 2>&1 | head -1)" >> gpurun_out/attn_ab.txt
-  cp paper_2512_17570_b200/libgreedysnake_prev.so $L; echo "prev $(timeout 120 python tools/gemm_probe.py 2>&1 | head -1)" >> gpurun_out/attn_ab.txt
-done
-cp /tmp/lib_new.so $L
-timeout 120 python tools/attn_accuracy.py > gpurun_out/attn_acc.txt 2>&1
-timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q -k "attention or context" > gpurun_out/t_attn.log 2>&1; echo "rc=$?" >> gpurun_out/t_attn.log
+rm -f gpurun_out/bn_ab.txt
+for r in 1 2 3; do for v in 1 0; do
+  echo "bn192=$v $(GS_GEMM_BN192=$v timeout 120 python tools/gemm_probe.py 2>&1 | grep fwd_qkv)" >> gpurun_out/bn_ab.txt
+done; done
+timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q -k "gemm" > gpurun_out/t_gemm.log 2>&1; echo "rc=$?" >> gpurun_out/t_gemm.log
+for r in 1 2; do for v in 1 0; do
+  GS_GEMM_BN192=$v timeout 600 python bench.py --no-cpu-baseline > gpurun_out/b.log 2>&1
+  echo "bench bn192=$v $(grep '^{' gpurun_out/b.log | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"], d["clocks"]["sm_mhz"])')" >> gpurun_out/bn_ab.txt
+done; done
