@@ -155,6 +155,19 @@ def pcie_bandwidth(torch, nbytes=1 << 30):
     return out
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (/proc/cpuinfo) and nproc, reported next to CPU numbers."""
+    name = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                name = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{name}, nproc {os.cpu_count()}"
+
+
 def cpu_sample(cfg_name: str, budget_s: float = 20.0):
     """Time the oracle port (fp32 C, OpenMP, all host threads) on one layer's
     forward + recompute-and-backward at the workload's micro-batch geometry.
@@ -201,7 +214,8 @@ def run_reference(args):
             "ms_per_step": t_layer * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": config_dict(args),
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": desc},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": desc,
+                             "cpu": cpu_model()},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -438,7 +452,7 @@ def run_ours(args):
     if not args.no_cpu_baseline:
         dt, toks, threads, desc = cpu_sample(args.config)
         line["cpu_baseline"] = {"value": toks / (N * dt), "unit": "tokens/s", "cores": threads, "kind": "port",
-                                "sample": desc}
+                                "sample": desc, "cpu": cpu_model()}
     print(json.dumps(line), flush=True)
 
 
