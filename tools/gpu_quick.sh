@@ -1,10 +1,5 @@
 mkdir -p gpurun_out
-rm -f gpurun_out/bn_ab.txt
-for r in 1 2 3; do for v in 1 0; do
-  echo "bn192=$v $(GS_GEMM_BN192=$v timeout 120 python tools/gemm_probe.py 2>&1 | grep fwd_qkv)" >> gpurun_out/bn_ab.txt
-done; done
-timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q -k "gemm" > gpurun_out/t_gemm.log 2>&1; echo "rc=$?" >> gpurun_out/t_gemm.log
-for r in 1 2; do for v in 1 0; do
-  GS_GEMM_BN192=$v timeout 600 python bench.py --no-cpu-baseline > gpurun_out/b.log 2>&1
-  echo "bench bn192=$v $(grep '^{' gpurun_out/b.log | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"], d["clocks"]["sm_mhz"])')" >> gpurun_out/bn_ab.txt
-done; done
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
