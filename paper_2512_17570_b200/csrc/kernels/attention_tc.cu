@@ -438,7 +438,9 @@ struct FaSmem3 {
   uint8_t Q[2][kTile];  // per tile: [2 d-chunks][128 rows][128 B]
   uint8_t K[2][kTile];  // 2-slot ring of 128-key blocks
   uint8_t V[2][kTile];
-  uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], o_done[2];
+  // P_t is published in two halves (keys 0-63: p_lo, 64-127: p_hi) so the
+  // first half of PV_t overlaps the softmax's second half
+  uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_lo[2], p_hi[2], o_done[2];
   uint32_t tmem;
 };
 
@@ -462,7 +464,8 @@ __global__ void __launch_bounds__(kThreadsF3, 1)
       bar_init(&sm.v_full[i], 1);
       bar_init(&sm.v_empty[i], 1);
       bar_init(&sm.s_full[i], 1);
-      bar_init(&sm.p_full[i], 128);
+      bar_init(&sm.p_lo[i], 128);
+      bar_init(&sm.p_hi[i], 128);
       bar_init(&sm.o_done[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -517,9 +520,16 @@ __global__ void __launch_bounds__(kThreadsF3, 1)
       };
       auto issue_pv = [&](int t, int kb) {  // O_t += P_t V(kb), P_t from TMEM (8 columns per 16 keys)
         const uint32_t va = su32(sm.V[kb & 1]);
+        bar_wait(&sm.p_lo[t], kb & 1);
+        fence_after();
 #pragma unroll
-        for (int ks = 0; ks < kBK / 16; ++ks)
+        for (int ks = 0; ks < kBK / 32; ++ks)
           mma_ts(tmem + 256 + t * 128, tmem + t * 128 + ks * 8, desc_mnmajor(va, ks), idesc(true), (kb | ks) != 0);
+        bar_wait(&sm.p_hi[t], kb & 1);
+        fence_after();
+#pragma unroll
+        for (int ks = kBK / 32; ks < kBK / 16; ++ks)
+          mma_ts(tmem + 256 + t * 128, tmem + t * 128 + ks * 8, desc_mnmajor(va, ks), idesc(true), 1u);
         commit(&sm.o_done[t]);
       };
       wait_k(0);
@@ -530,8 +540,6 @@ __global__ void __launch_bounds__(kThreadsF3, 1)
         bar_wait(&sm.v_full[kb & 1], (kb >> 1) & 1);
         bool k_ready = false;
         if (kb < nblk0) {
-          bar_wait(&sm.p_full[0], kb & 1);
-          fence_after();
           issue_pv(0, kb);
           if (kb + 1 < nblk0) {
             wait_k(kb + 1);
@@ -539,8 +547,6 @@ __global__ void __launch_bounds__(kThreadsF3, 1)
             issue_s(0, kb + 1);
           }
         }
-        bar_wait(&sm.p_full[1], kb & 1);
-        fence_after();
         issue_pv(1, kb);
         commit(&sm.v_empty[kb & 1]);
         if (kb + 1 < nblk1) {
@@ -591,34 +597,36 @@ __global__ void __launch_bounds__(kThreadsF3, 1)
       const float nm = -m_new;
       float ps[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-      for (int i = 0; i < kBK; ++i) {
-        const float x = fmaf(sv[i], scale_log2, nm);
-        sv[i] = ((POLY == 1 && (i & 3) == 3) || (POLY == 2 && (i & 1))) ? ex2_poly(x) : ex2(x);
-        ps[i & 7] += sv[i];
-      }
-      l_run = l_run * corr + (((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7])));
-      m_run = m_new;
+      for (int half = 0; half < 2; ++half) {
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {  // P_t -> TMEM over S_t (64 columns of bf16 pairs)
-        uint32_t pk[32];
+        for (int i = 64 * half; i < 64 * half + 64; ++i) {
+          const float x = fmaf(sv[i], scale_log2, nm);
+          sv[i] = ((POLY == 1 && (i & 3) == 3) || (POLY == 2 && (i & 1))) ? ex2_poly(x) : ex2(x);
+          ps[i & 7] += sv[i];
+        }
+        uint32_t pk[32];  // this half of P_t -> TMEM over S_t (32 columns of bf16 pairs)
 #pragma unroll
         for (int k = 0; k < 32; ++k) pk[k] = pack(sv[64 * half + 2 * k], sv[64 * half + 2 * k + 1]);
         tst32(St + half * 32, pk);
-      }
-      if (kb > 0 && __any_sync(0xffffffffu, bump)) {  // PV_t(kb-1) is complete (see above)
+        // O is rescaled before the first half of PV(kb) may accumulate into
+        // it (after the first half's P is packed, so its registers are free)
+        if (half == 0 && kb > 0 && __any_sync(0xffffffffu, bump)) {  // PV_t(kb-1) is complete (see above)
 #pragma unroll
-        for (int c = 0; c < kD / 32; ++c) {
-          uint32_t rr[32];
-          tld32(Ot + c * 32, rr);
-          tld_wait();
+          for (int c = 0; c < kD / 32; ++c) {
+            uint32_t rr[32];
+            tld32(Ot + c * 32, rr);
+            tld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * corr);
-          tst32(Ot + c * 32, rr);
+            for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * corr);
+            tst32(Ot + c * 32, rr);
+          }
         }
+        tst_wait();
+        fence_before();
+        bar_arrive(half ? &sm.p_hi[t] : &sm.p_lo[t]);
       }
-      tst_wait();
-      fence_before();
-      bar_arrive(&sm.p_full[t]);
+      l_run = l_run * corr + (((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7])));
+      m_run = m_new;
     }
     // After the last arrive o_done[t] is in phase nb-1 (PV_t(nb-1) pending)
     // or nb; earlier phases completed before S_t(nb-1) did.
