@@ -1,5 +1,2 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 900 python bench.py --config gpt65b-4layer --no-cpu-baseline > gpurun_out/bench65.log 2>&1; echo "rc=$?" >> gpurun_out/bench65.log
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "rc=$?" >> gpurun_out/bench.log
+timeout 900 python -m pytest tests/test_gpu_kernels.py -q -k "repeatable" > gpurun_out/t_rep.log 2>&1; echo "rc=$?" >> gpurun_out/t_rep.log
