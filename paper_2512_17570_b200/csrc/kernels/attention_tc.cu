@@ -1001,9 +1001,45 @@ struct FaBwdSmem4 {
   uint32_t tmem;
 };
 
+// 128 rows x 128 fp32 TMEM columns (lane = row, this warp's quarter) -> bf16
+// (x scale) in shared memory as two SWIZZLE_128B boxes [2][128 rows][128 B],
+// ready for store_tile_128.  Row-per-thread 16-byte stores, conflict-free
+// under the swizzle.
+__device__ __forceinline__ void stage_rows_bf16(uint32_t taddr, float scale, uint8_t* stg, int r) {
+#pragma unroll
+  for (int c = 0; c < kD / 32; ++c) {
+    uint32_t rr[32];
+    tld32(taddr + c * 32, rr);
+    tld_wait();
+    uint8_t* line = stg + (c >> 1) * 16384 + r * 128;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 w;
+      w.x = pack(__uint_as_float(rr[8 * q]) * scale, __uint_as_float(rr[8 * q + 1]) * scale);
+      w.y = pack(__uint_as_float(rr[8 * q + 2]) * scale, __uint_as_float(rr[8 * q + 3]) * scale);
+      w.z = pack(__uint_as_float(rr[8 * q + 4]) * scale, __uint_as_float(rr[8 * q + 5]) * scale);
+      w.w = pack(__uint_as_float(rr[8 * q + 6]) * scale, __uint_as_float(rr[8 * q + 7]) * scale);
+      *reinterpret_cast<uint4*>(line + ((((c & 1) * 4 + q) ^ (r & 7)) << 4)) = w;
+    }
+  }
+}
+// Two TMA stores (64 columns each) of a staged 128 x 128 bf16 tile at
+// (col, row); waits until they are complete (the CTA may exit right after).
+__device__ __forceinline__ void store_tile_128(const CUtensorMap* m, const uint8_t* stg, int col, int row) {
+#pragma unroll
+  for (int half = 0; half < 2; ++half)
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(su32(stg + half * 16384)), "r"(col + 64 * half), "r"(row)
+                 : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     fa_bwd_tc4_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_q,
                       const __grid_constant__ CUtensorMap map_do, const __grid_constant__ CUtensorMap map_dq,
+                      const __grid_constant__ CUtensorMap map_out,
                       const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv, int s,
                       int h, int H, float scale, long long* __restrict__ tr) {
   extern __shared__ __align__(1024) uint8_t rawb4[];
@@ -1182,22 +1218,13 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     }
     bar_wait(&sm.mma_done, 0);
     fence_after();
-    bf16* out = dqkv + (long long)(row0 + key) * 3 * h + h + j * kD;
-#pragma unroll
-    for (int c = 0; c < kD / 32; ++c) {
-      uint32_t rr[32];
-      tld32(tmem + lb + kDK + c * 32, rr);
-      tld_wait();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 w;
-        w.x = pack(__uint_as_float(rr[8 * q]) * scale, __uint_as_float(rr[8 * q + 1]) * scale);
-        w.y = pack(__uint_as_float(rr[8 * q + 2]) * scale, __uint_as_float(rr[8 * q + 3]) * scale);
-        w.z = pack(__uint_as_float(rr[8 * q + 4]) * scale, __uint_as_float(rr[8 * q + 5]) * scale);
-        w.w = pack(__uint_as_float(rr[8 * q + 6]) * scale, __uint_as_float(rr[8 * q + 7]) * scale);
-        *reinterpret_cast<uint4*>(out + c * 32 + 8 * q) = w;
-      }
-    }
+    // dK leaves through shared memory and two TMA stores (full 128-B lines):
+    // per-thread row stores of 16 B into 12 KB-strided rows took ~4.5k
+    // cycles.  The Q ring is free once every MMA has completed.
+    stage_rows_bf16(tmem + lb + kDK, scale, sm.Q[0], r);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 4, 128;" ::: "memory");
+    if (r == 0) store_tile_128(&map_out, sm.Q[0], h + j * kD, row0 + k0);
   } else if (warp >= 8) {
     const int r = (warp - 8) * 32 + lane;  // d row of dQ^T; key row for dV
     const uint32_t lb = ((uint32_t)((warp & 3) * 32)) << 16;
@@ -1237,22 +1264,10 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     bar_wait(&sm.mma_done, 0);
     fence_after();
-    bf16* out = dqkv + (long long)(row0 + k0 + r) * 3 * h + 2 * h + j * kD;
-#pragma unroll
-    for (int c = 0; c < kD / 32; ++c) {
-      uint32_t rr2[32];
-      tld32(tmem + lb + kDV + c * 32, rr2);
-      tld_wait();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 w;
-        w.x = pack(__uint_as_float(rr2[8 * q]), __uint_as_float(rr2[8 * q + 1]));
-        w.y = pack(__uint_as_float(rr2[8 * q + 2]), __uint_as_float(rr2[8 * q + 3]));
-        w.z = pack(__uint_as_float(rr2[8 * q + 4]), __uint_as_float(rr2[8 * q + 5]));
-        w.w = pack(__uint_as_float(rr2[8 * q + 6]), __uint_as_float(rr2[8 * q + 7]));
-        *reinterpret_cast<uint4*>(out + c * 32 + 8 * q) = w;
-      }
-    }
+    stage_rows_bf16(tmem + lb + kDV, 1.0f, sm.dO[0], r);  // dV, same path as dK (dO ring)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 3, 128;" ::: "memory");
+    if (r == 0) store_tile_128(&map_out, sm.dO[0], 2 * h + j * kD, row0 + k0);
   }
   fence_before();
   __syncthreads();
@@ -1451,8 +1466,18 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
     }
     count_launch();
     long long* tr = attn_trace_begin(st, b * H * (s / kBK));
-    fa_bwd_tc4_kernel<<<dim3(b * H, s / kBK), kThreadsBwd, smem4, st>>>(mq, mq64, md, mdq, lse2, D, (bf16*)dqkv, s,
-                                                                          h, H, 1.0f / sqrtf((float)kD), tr);
+    CUtensorMap mout;  // dqkv, bf16, 64-column x 128-row boxes (dK / dV TMA stores)
+    {
+      const cuuint64_t dims[2] = {(cuuint64_t)3 * h, (cuuint64_t)b * s};
+      const cuuint64_t strides[1] = {(cuuint64_t)3 * h * 2};
+      const cuuint32_t box[2] = {64, 128};
+      if (encoder()(&mout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dqkv, dims, strides, box, elem,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
+    fa_bwd_tc4_kernel<<<dim3(b * H, s / kBK), kThreadsBwd, smem4, st>>>(mq, mq64, md, mdq, mout, lse2, D, (bf16*)dqkv,
+                                                                          s, h, H, 1.0f / sqrtf((float)kD), tr);
     attn_trace_end(tr, st, b * H * (s / kBK), s / kBK);
     return cudaGetLastError();
   }
