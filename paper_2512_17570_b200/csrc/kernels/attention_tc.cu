@@ -433,6 +433,41 @@ __global__ void __launch_bounds__(256, 2)
 // PV_{1-t}(kb) and S_{1-t}(kb+1).  P_t (bf16) is tcgen05.st-ed over S_t and
 // O_t += P_t V is a TS-MMA.  Since each tile's S(kb) is issued after its
 // PV(kb-1), seeing S_t(kb) means O_t is final for a rescale — no wait.
+// 128 rows x 128 fp32 TMEM columns (lane = row, this warp's quarter) -> bf16
+// (x scale) in shared memory as two SWIZZLE_128B boxes [2][128 rows][128 B],
+// ready for store_tile_128.  Row-per-thread 16-byte stores, conflict-free
+// under the swizzle.
+__device__ __forceinline__ void stage_rows_bf16(uint32_t taddr, float scale, uint8_t* stg, int r) {
+#pragma unroll
+  for (int c = 0; c < kD / 32; ++c) {
+    uint32_t rr[32];
+    tld32(taddr + c * 32, rr);
+    tld_wait();
+    uint8_t* line = stg + (c >> 1) * 16384 + r * 128;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 w;
+      w.x = pack(__uint_as_float(rr[8 * q]) * scale, __uint_as_float(rr[8 * q + 1]) * scale);
+      w.y = pack(__uint_as_float(rr[8 * q + 2]) * scale, __uint_as_float(rr[8 * q + 3]) * scale);
+      w.z = pack(__uint_as_float(rr[8 * q + 4]) * scale, __uint_as_float(rr[8 * q + 5]) * scale);
+      w.w = pack(__uint_as_float(rr[8 * q + 6]) * scale, __uint_as_float(rr[8 * q + 7]) * scale);
+      *reinterpret_cast<uint4*>(line + ((((c & 1) * 4 + q) ^ (r & 7)) << 4)) = w;
+    }
+  }
+}
+// Two TMA stores (64 columns each) of a staged 128 x 128 bf16 tile at
+// (col, row); waits until they are complete (the CTA may exit right after).
+__device__ __forceinline__ void store_tile_128(const CUtensorMap* m, const uint8_t* stg, int col, int row) {
+#pragma unroll
+  for (int half = 0; half < 2; ++half)
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(su32(stg + half * 16384)), "r"(col + 64 * half), "r"(row)
+                 : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 constexpr int kThreadsF3 = 352;  // w0 Q+K, w1 MMA + TMEM, w2-5 / w6-9 softmax tiles 0 / 1, w10 V
 struct FaSmem3 {
   uint8_t Q[2][kTile];  // per tile: [2 d-chunks][128 rows][128 B]
@@ -446,8 +481,9 @@ struct FaSmem3 {
 
 template <int POLY>  // exponentials on the FMA pipes: 0 none, 1 one in four, 2 one in two
 __global__ void __launch_bounds__(kThreadsF3, 1)
-    fa_fwd_tc3_kernel(const __grid_constant__ CUtensorMap map_t, bf16* __restrict__ o, float* __restrict__ lse, int s,
-                      int h, int H, float scale_log2, long long* __restrict__ tr) {
+    fa_fwd_tc3_kernel(const __grid_constant__ CUtensorMap map_t, const __grid_constant__ CUtensorMap map_o,
+                      bf16* __restrict__ o, float* __restrict__ lse, int s, int h, int H, float scale_log2,
+                      long long* __restrict__ tr) {
   extern __shared__ __align__(1024) uint8_t raw3[];
   FaSmem3& sm = *reinterpret_cast<FaSmem3*>(raw3);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -632,23 +668,13 @@ __global__ void __launch_bounds__(kThreadsF3, 1)
     // or nb; earlier phases completed before S_t(nb-1) did.
     bar_wait(&sm.o_done[t], (nb - 1) & 1);
     fence_after();
-    const float inv = 1.0f / l_run;
-    bf16* orow = o + (long long)(row0 + qrow) * h + j * kD;
-#pragma unroll
-    for (int c = 0; c < kD / 32; ++c) {
-      uint32_t rr[32];
-      tld32(Ot + c * 32, rr);
-      tld_wait();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 w;
-        w.x = pack(__uint_as_float(rr[8 * q]) * inv, __uint_as_float(rr[8 * q + 1]) * inv);
-        w.y = pack(__uint_as_float(rr[8 * q + 2]) * inv, __uint_as_float(rr[8 * q + 3]) * inv);
-        w.z = pack(__uint_as_float(rr[8 * q + 4]) * inv, __uint_as_float(rr[8 * q + 5]) * inv);
-        w.w = pack(__uint_as_float(rr[8 * q + 6]) * inv, __uint_as_float(rr[8 * q + 7]) * inv);
-        *reinterpret_cast<uint4*>(orow + c * 32 + 8 * q) = w;
-      }
-    }
+    // O_t / l -> bf16 through shared memory (Q_t: every MMA reading it has
+    // completed once o_done[t] has) and two TMA stores of full lines
+    stage_rows_bf16(Ot, 1.0f / l_run, sm.Q[t], r);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (t == 0) asm volatile("bar.sync 5, 128;" ::: "memory");  // this warpgroup only
+    else asm volatile("bar.sync 6, 128;" ::: "memory");
+    if (r == 0) store_tile_128(&map_o, sm.Q[t], j * kD, row0 + q0t);
     lse[(long long)bh * s + qrow] = (m_run + log2f(l_run)) * 0.6931471805599453f;
   }
   fence_before();
@@ -1000,41 +1026,6 @@ struct FaBwdSmem4 {
   uint64_t kv_full, q_full[kQS4], q_empty[kQS4], s_full[2], ps_full, pds_empty, dq_full[2], dq_empty[2], mma_done;
   uint32_t tmem;
 };
-
-// 128 rows x 128 fp32 TMEM columns (lane = row, this warp's quarter) -> bf16
-// (x scale) in shared memory as two SWIZZLE_128B boxes [2][128 rows][128 B],
-// ready for store_tile_128.  Row-per-thread 16-byte stores, conflict-free
-// under the swizzle.
-__device__ __forceinline__ void stage_rows_bf16(uint32_t taddr, float scale, uint8_t* stg, int r) {
-#pragma unroll
-  for (int c = 0; c < kD / 32; ++c) {
-    uint32_t rr[32];
-    tld32(taddr + c * 32, rr);
-    tld_wait();
-    uint8_t* line = stg + (c >> 1) * 16384 + r * 128;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint4 w;
-      w.x = pack(__uint_as_float(rr[8 * q]) * scale, __uint_as_float(rr[8 * q + 1]) * scale);
-      w.y = pack(__uint_as_float(rr[8 * q + 2]) * scale, __uint_as_float(rr[8 * q + 3]) * scale);
-      w.z = pack(__uint_as_float(rr[8 * q + 4]) * scale, __uint_as_float(rr[8 * q + 5]) * scale);
-      w.w = pack(__uint_as_float(rr[8 * q + 6]) * scale, __uint_as_float(rr[8 * q + 7]) * scale);
-      *reinterpret_cast<uint4*>(line + ((((c & 1) * 4 + q) ^ (r & 7)) << 4)) = w;
-    }
-  }
-}
-// Two TMA stores (64 columns each) of a staged 128 x 128 bf16 tile at
-// (col, row); waits until they are complete (the CTA may exit right after).
-__device__ __forceinline__ void store_tile_128(const CUtensorMap* m, const uint8_t* stg, int col, int row) {
-#pragma unroll
-  for (int half = 0; half < 2; ++half)
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                     reinterpret_cast<uint64_t>(m)),
-                 "r"(su32(stg + half * 16384)), "r"(col + 64 * half), "r"(row)
-                 : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
 
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     fa_bwd_tc4_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_q,
@@ -1389,7 +1380,17 @@ cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s,
     count_launch();
     const int ny = s / (2 * kBQ);
     long long* tr = attn_trace_begin(st, b * H * ny);
-    kern3<<<dim3(b * H, ny), kThreadsF3, smem3, st>>>(mq, (bf16*)o, lse, s, h, H,
+    CUtensorMap mo;  // o, bf16, 64-column x 128-row boxes (TMA stores of O)
+    {
+      const cuuint64_t dims[2] = {(cuuint64_t)h, (cuuint64_t)b * s};
+      const cuuint64_t strides[1] = {(cuuint64_t)h * 2};
+      const cuuint32_t box[2] = {64, 128};
+      if (encoder()(&mo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, o, dims, strides, box, elem,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
+    kern3<<<dim3(b * H, ny), kThreadsF3, smem3, st>>>(mq, mo, (bf16*)o, lse, s, h, H,
                                                                    1.4426950408889634f / sqrtf((float)kD), tr);
     attn_trace_end(tr, st, b * H * ny, ny, "(v3: grid schedule only)", 0);
     return cudaGetLastError();
