@@ -506,6 +506,32 @@ __global__ void __launch_bounds__(kThreadsF3, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // Thread 0 is the producer: Q of both tiles and the first K / V slots go
+  // out before the CTA-wide sync, overlapping the TMEM allocation.
+  auto load_k = [&](int kb) {
+    const int sl = kb & 1;
+    bar_expect(&sm.k_full[sl], kTile);
+    for (int c = 0; c < 2; ++c)
+      tma2d(sm.K[sl] + c * 16384, &map_t, &sm.k_full[sl], h + j * kD + 64 * c, row0 + kb * kBK);
+  };
+  auto load_v = [&](int kb) {
+    const int sl = kb & 1;
+    bar_expect(&sm.v_full[sl], kTile);
+    for (int c = 0; c < 2; ++c)
+      tma2d(sm.V[sl] + c * 16384, &map_t, &sm.v_full[sl], 2 * h + j * kD + 64 * c, row0 + kb * kBK);
+  };
+  const int n_early = nblk1 < 2 ? nblk1 : 2;  // ring slots that start empty
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_t)) : "memory");
+    bar_expect(&sm.q_full, 2 * kTile);
+    for (int t = 0; t < 2; ++t)
+      for (int c = 0; c < 2; ++c)
+        tma2d(sm.Q[t] + c * 16384, &map_t, &sm.q_full, j * kD + 64 * c, row0 + q0 + t * kBQ);
+    for (int kb = 0; kb < n_early; ++kb) {
+      load_k(kb);
+      load_v(kb);
+    }
+  }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -516,28 +542,13 @@ __global__ void __launch_bounds__(kThreadsF3, 1)
   const uint32_t tmem = sm.tmem;
 
   if (warp == 0) {
-    if (lane == 0) {  // Q of both tiles, then the K ring
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_t)) : "memory");
-      bar_expect(&sm.q_full, 2 * kTile);
-      for (int t = 0; t < 2; ++t)
-        for (int c = 0; c < 2; ++c)
-          tma2d(sm.Q[t] + c * 16384, &map_t, &sm.q_full, j * kD + 64 * c, row0 + q0 + t * kBQ);
-      for (int kb = 0; kb < nblk1; ++kb) {
+    if (lane == 0) {  // the rest of the K / V rings
+      for (int kb = n_early; kb < nblk1; ++kb) {
         const int sl = kb & 1;
-        bar_wait(&sm.k_empty[sl], ((kb >> 1) & 1) ^ 1);
-        bar_expect(&sm.k_full[sl], kTile);
-        for (int c = 0; c < 2; ++c)
-          tma2d(sm.K[sl] + c * 16384, &map_t, &sm.k_full[sl], h + j * kD + 64 * c, row0 + kb * kBK);
-      }
-    }
-  } else if (warp == 10) {
-    if (lane == 0) {  // the V ring
-      for (int kb = 0; kb < nblk1; ++kb) {
-        const int sl = kb & 1;
+        bar_wait(&sm.k_empty[sl], ((kb >> 1) & 1) ^ 1);  // K(kb) after S_1(kb-2), not behind V's slot
+        load_k(kb);
         bar_wait(&sm.v_empty[sl], ((kb >> 1) & 1) ^ 1);
-        bar_expect(&sm.v_full[sl], kTile);
-        for (int c = 0; c < 2; ++c)
-          tma2d(sm.V[sl] + c * 16384, &map_t, &sm.v_full[sl], 2 * h + j * kD + 64 * c, row0 + kb * kBK);
+        load_v(kb);
       }
     }
   } else if (warp == 1) {
@@ -1069,6 +1080,32 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     bar_init(&sm.mma_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // Thread 0 is also the producer: it starts the K / V tiles and the first
+  // ring slots before the CTA-wide sync, so their latency overlaps the TMEM
+  // allocation (the first tiles of a CTA were ~1.3k cycles late otherwise).
+  auto load_q = [&](int i) {
+    const int sl = i % kQS4, q0 = (qb0 + i) * kBQb;
+    bar_expect(&sm.q_full[sl], 2 * kHalf + 2 * kBQb * 4);
+    for (int c = 0; c < 2; ++c) {
+      tma2d(sm.Q[sl] + c * 8192, &map_q, &sm.q_full[sl], j * kD + 64 * c, row0 + q0);
+      tma2d(sm.dO[sl] + c * 8192, &map_do, &sm.q_full[sl], j * kD + 64 * c, row0 + q0);
+    }
+    bulk_g2s(sm.L[sl], lse + (long long)bh * s + q0, kBQb * 4, &sm.q_full[sl]);
+    bulk_g2s(sm.D[sl], Dg + (long long)bh * s + q0, kBQb * 4, &sm.q_full[sl]);
+    GS_TR4(7, i);
+  };
+  const int n_early = nq < kQS4 ? nq : kQS4;  // ring slots that start empty
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_do)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_q)) : "memory");
+    bar_expect(&sm.kv_full, 2 * kTile);
+    for (int c = 0; c < 2; ++c) {
+      tma2d(sm.K + c * 16384, &map_qkv, &sm.kv_full, h + j * kD + 64 * c, row0 + k0);
+      tma2d(sm.V + c * 16384, &map_qkv, &sm.kv_full, 2 * h + j * kD + 64 * c, row0 + k0);
+    }
+    for (int i = 0; i < n_early; ++i) load_q(i);
+  }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -1081,25 +1118,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_do)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_q)) : "memory");
-      bar_expect(&sm.kv_full, 2 * kTile);
-      for (int c = 0; c < 2; ++c) {
-        tma2d(sm.K + c * 16384, &map_qkv, &sm.kv_full, h + j * kD + 64 * c, row0 + k0);
-        tma2d(sm.V + c * 16384, &map_qkv, &sm.kv_full, 2 * h + j * kD + 64 * c, row0 + k0);
-      }
-      for (int i = 0; i < nq; ++i) {
-        const int sl = i % kQS4, q0 = (qb0 + i) * kBQb;
-        bar_wait(&sm.q_empty[sl], ((i / kQS4) & 1) ^ 1);
-        bar_expect(&sm.q_full[sl], 2 * kHalf + 2 * kBQb * 4);
-        for (int c = 0; c < 2; ++c) {
-          tma2d(sm.Q[sl] + c * 8192, &map_q, &sm.q_full[sl], j * kD + 64 * c, row0 + q0);
-          tma2d(sm.dO[sl] + c * 8192, &map_do, &sm.q_full[sl], j * kD + 64 * c, row0 + q0);
-        }
-        bulk_g2s(sm.L[sl], lse + (long long)bh * s + q0, kBQb * 4, &sm.q_full[sl]);
-        bulk_g2s(sm.D[sl], Dg + (long long)bh * s + q0, kBQb * 4, &sm.q_full[sl]);
-        GS_TR4(7, i);
+      for (int i = n_early; i < nq; ++i) {
+        bar_wait(&sm.q_empty[i % kQS4], ((i / kQS4) & 1) ^ 1);
+        load_q(i);
       }
     }
   } else if (warp == 1) {

@@ -3,8 +3,8 @@ L=paper_2512_17570_b200/libgreedysnake.so
 cp $L /tmp/lib_new.so
 rm -f gpurun_out/attn_ab.txt
 for r in 1 2 3; do
-  cp /tmp/lib_new.so $L; echo "new $(timeout 120 python tools/gemm_probe.py 2>&1 | sed -n 1p)" >> gpurun_out/attn_ab.txt
-  cp paper_2512_17570_b200/libgreedysnake_prev.so $L; echo "prev $(timeout 120 python tools/gemm_probe.py 2>&1 | sed -n 1p)" >> gpurun_out/attn_ab.txt
+  cp /tmp/lib_new.so $L; echo "new $(timeout 120 python tools/gemm_probe.py 2>&1 | sed -n 1,2p | tr "\n" " ")" >> gpurun_out/attn_ab.txt
+  cp paper_2512_17570_b200/libgreedysnake_prev.so $L; echo "prev $(timeout 120 python tools/gemm_probe.py 2>&1 | sed -n 1,2p | tr "\n" " ")" >> gpurun_out/attn_ab.txt
 done
 cp /tmp/lib_new.so $L
 timeout 120 python tools/attn_grid_trace.py > gpurun_out/attn_grid.txt 2>&1
