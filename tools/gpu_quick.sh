@@ -1,11 +1,5 @@
 mkdir -p gpurun_out
-L=paper_2512_17570_b200/libgreedysnake.so
-cp $L /tmp/lib_new.so
-rm -f gpurun_out/attn_ab.txt
-for r in 1 2 3; do
-  cp /tmp/lib_new.so $L; echo "new $(timeout 120 python tools/gemm_probe.py 2>&1 | sed -n 1,2p | tr "\n" " ")" >> gpurun_out/attn_ab.txt
-  cp paper_2512_17570_b200/libgreedysnake_prev.so $L; echo "prev $(timeout 120 python tools/gemm_probe.py 2>&1 | sed -n 1,2p | tr "\n" " ")" >> gpurun_out/attn_ab.txt
-done
-cp /tmp/lib_new.so $L
-timeout 120 python tools/attn_grid_trace.py > gpurun_out/attn_grid.txt 2>&1
-timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q -k "attention" > gpurun_out/t_attn.log 2>&1; echo "rc=$?" >> gpurun_out/t_attn.log
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 300 python tools/gemm_probe.py > gpurun_out/probe.jsonl 2>&1
