@@ -468,7 +468,7 @@ __device__ __forceinline__ void store_tile_128(const CUtensorMap* m, const uint8
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-constexpr int kThreadsF3 = 352;  // w0 Q+K, w1 MMA + TMEM, w2-5 / w6-9 softmax tiles 0 / 1, w10 V
+constexpr int kThreadsF3 = 320;  // w0 loads (thread 0), w1 MMA + TMEM, w2-5 / w6-9 softmax tiles 0 / 1
 struct FaSmem3 {
   uint8_t Q[2][kTile];  // per tile: [2 d-chunks][128 rows][128 B]
   uint8_t K[2][kTile];  // 2-slot ring of 128-key blocks
