@@ -1,10 +1,9 @@
-mkdir -p gpurun_out
-L=paper_2512_17570_b200/libgreedysnake.so
-cp $L /tmp/lib_new.so
-rm -f gpurun_out/attn_ab.txt
-for r in 1 2 3; do
-  cp /tmp/lib_new.so $L; echo "new $(timeout 120 python tools/gemm_probe.py 2>&1 | sed -n 1p)" >> gpurun_out/attn_ab.txt
-  cp paper_2512_17570_b200/libgreedysnake_prev.so $L; echo "prev $(timeout 120 python tools/gemm_probe.py 2>&1 | sed -n 1p)" >> gpurun_out/attn_ab.txt
+out=gpurun_out
+mkdir -p $out
+for k in "fa_fwd_tc3:attn_fwd" "fa_bwd_tc4:attn_bwd"; do
+  IFS=: read -r name tag <<< "$k"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$name -s 2 -c 1 \
+    -o $out/final_prof_$tag -f python tools/ncu_targets.py $tag > $out/final_ncu_$tag.log 2>&1
+  ncu -i $out/final_prof_$tag.ncu-rep --page raw --csv > $out/final_raw_$tag.csv 2>/dev/null
+  rm -f $out/final_prof_$tag.ncu-rep
 done
-cp /tmp/lib_new.so $L
-timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q -k "attention" > gpurun_out/t_attn.log 2>&1; echo "rc=$?" >> gpurun_out/t_attn.log
