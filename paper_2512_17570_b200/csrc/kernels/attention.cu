@@ -549,6 +549,7 @@ __global__ void dq_store_kernel(const float* __restrict__ dq, bf16* __restrict__
 __global__ void fa_prep_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout, const float* __restrict__ lse,
                                float* __restrict__ D, float* __restrict__ L2, float* __restrict__ dq, int b, int s,
                                int h, int H) {
+  pdl_trigger_and_wait();
   const long long rows = (long long)b * H * s;
   const int sub = threadIdx.x & 15;
   for (long long gr = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 4; gr < rows;
@@ -579,6 +580,7 @@ __global__ void fa_prep_kernel(const bf16* __restrict__ o, const bf16* __restric
 
 // dQ fp32 [b*s][h] -> bf16 q-columns of dqkv [b*s][3h], 8 columns per thread.
 __global__ void dq_store_vec_kernel(const float* __restrict__ dq, bf16* __restrict__ dqkv, long long rows, int h) {
+  pdl_trigger_and_wait();
   const long long n8 = rows * h / 8;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
     const long long e = i * 8, r = e / h, c = e % h;
@@ -629,12 +631,14 @@ cudaError_t fa_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16*
   cudaError_t e = cudaSuccess;
   if (HD == 128 && attention_tc_supported(DType::BF16, s, h, H)) {
     count_launch();
-    fa_prep_kernel<<<grid_for(rows * 16, 256), 256, 0, st>>>(o, dout, lse, D, L2, dq, b, s, h, H);
+    e = launch_pdl(fa_prep_kernel, dim3(grid_for(rows * 16, 256)), dim3(256), 0, st, (const bf16*)o,
+                   (const bf16*)dout, lse, D, L2, dq, b, s, h, H);
+    if (e != cudaSuccess) return e;
     e = attention_bwd_tc(qkv, dout, lse, L2, D, dqkv, dq, b, s, h, H, st);
     if (e != cudaSuccess) return e;
     count_launch();
-    dq_store_vec_kernel<<<grid_for((long long)b * s * h / 8, 256), 256, 0, st>>>(dq, dqkv, (long long)b * s, h);
-    return cudaGetLastError();
+    return launch_pdl(dq_store_vec_kernel, dim3(grid_for((long long)b * s * h / 8, 256)), dim3(256), 0, st,
+                      (const float*)dq, (bf16*)dqkv, (long long)b * s, h);
   }
   e = cudaMemsetAsync(dq, 0, sizeof(float) * (size_t)b * s * h, st);
   if (e != cudaSuccess) return e;

@@ -484,6 +484,7 @@ __global__ void __launch_bounds__(kThreadsF3, 1)
     fa_fwd_tc3_kernel(const __grid_constant__ CUtensorMap map_t, const __grid_constant__ CUtensorMap map_o,
                       bf16* __restrict__ o, float* __restrict__ lse, int s, int h, int H, float scale_log2,
                       long long* __restrict__ tr) {
+  pdl_trigger_and_wait();
   extern __shared__ __align__(1024) uint8_t raw3[];
   FaSmem3& sm = *reinterpret_cast<FaSmem3*>(raw3);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1044,6 +1045,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
                       const __grid_constant__ CUtensorMap map_out,
                       const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv, int s,
                       int h, int H, float scale, long long* __restrict__ tr) {
+  pdl_trigger_and_wait();
   extern __shared__ __align__(1024) uint8_t rawb4[];
   FaBwdSmem4& sm = *reinterpret_cast<FaBwdSmem4*>(rawb4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1411,8 +1413,9 @@ cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
     }
-    kern3<<<dim3(b * H, ny), kThreadsF3, smem3, st>>>(mq, mo, (bf16*)o, lse, s, h, H,
-                                                                   1.4426950408889634f / sqrtf((float)kD), tr);
+    cudaError_t le = launch_pdl(kern3, dim3(b * H, ny), dim3(kThreadsF3), smem3, st, mq, mo, (bf16*)o, lse, s, h, H,
+                                1.4426950408889634f / sqrtf((float)kD), tr);
+    if (le != cudaSuccess) return le;
     attn_trace_end(tr, st, b * H * ny, ny, "(v3: grid schedule only)", 0);
     return cudaGetLastError();
   }
@@ -1498,8 +1501,9 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
     }
-    fa_bwd_tc4_kernel<<<dim3(b * H, s / kBK), kThreadsBwd, smem4, st>>>(mq, mq64, md, mdq, mout, lse2, D, (bf16*)dqkv,
-                                                                          s, h, H, 1.0f / sqrtf((float)kD), tr);
+    cudaError_t le = launch_pdl(fa_bwd_tc4_kernel, dim3(b * H, s / kBK), dim3(kThreadsBwd), smem4, st, mq, mq64, md,
+                                mdq, mout, lse2, D, (bf16*)dqkv, s, h, H, 1.0f / sqrtf((float)kD), tr);
+    if (le != cudaSuccess) return le;
     attn_trace_end(tr, st, b * H * (s / kBK), s / kBK);
     return cudaGetLastError();
   }

@@ -1,6 +1,9 @@
 // Shared device helpers for the sm_100a kernels.
 #pragma once
 
+#include <cstdlib>
+#include <utility>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -72,6 +75,40 @@ inline int num_sms() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+// Programmatic dependent launch (PDL): kernels on the layer chain are
+// launched with programmatic stream serialisation and open with
+// pdl_trigger_and_wait(): the next kernel's CTAs may be scheduled while this
+// grid's last CTAs run, but no CTA touches memory before its predecessor grid
+// has completed (griddepcontrol.wait), so stream order semantics are kept.
+// griddepcontrol.* are no-ops for a kernel launched without the attribute.
+// GS_PDL=0 launches without it.
+__device__ __forceinline__ void pdl_trigger_and_wait() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("GS_PDL");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 inline unsigned grid_for(long long n, int block, int per_thread = 1) {

@@ -158,6 +158,7 @@ template <typename T, int C>
 __global__ void __launch_bounds__(256) ln_fwd_vec_kernel(const T* __restrict__ x, T* __restrict__ y,
                                                          float* __restrict__ mean, float* __restrict__ rstd,
                                                          int rows, int h, int nw) {
+  pdl_trigger_and_wait();
   using VT = Vec<T>;
   constexpr int N = VT::N;
   __shared__ float red[8];
@@ -213,6 +214,7 @@ template <typename T, int C>
 __global__ void __launch_bounds__(256) ln_bwd_vec_kernel(const T* __restrict__ x, const float* __restrict__ mean,
                                                          const float* __restrict__ rstd, const T* __restrict__ dy,
                                                          const T* res, T* dx, int rows, int h, int nw) {
+  pdl_trigger_and_wait();
   using VT = Vec<T>;
   constexpr int N = VT::N;
   __shared__ float red[8];
@@ -274,6 +276,12 @@ inline RowShape row_shape(int h, int n) {
   r.c = (nv + 32 * r.nw - 1) / (32 * r.nw);
   return r;
 }
+#define GS_TRY_E(expr)                      \
+  do {                                      \
+    const cudaError_t e_ = (expr);          \
+    if (e_ != cudaSuccess) return e_;       \
+  } while (0)
+
 #define GS_ROW_C(c, ...)                                       \
   do {                                                         \
     if ((c) <= 1) { constexpr int C = 1; __VA_ARGS__; }        \
@@ -514,8 +522,8 @@ cudaError_t layernorm_fwd(DType dt, const void* x, void* y, float* mean, float* 
   GS_DISPATCH(dt, {
     if (h % Vec<T>::N == 0) {
       const RowShape r = row_shape(h, Vec<T>::N);
-      GS_ROW_C(r.c, ln_fwd_vec_kernel<T, C><<<(rows + r.rpb - 1) / r.rpb, 32 * r.nw * r.rpb, 0, s>>>(
-                        (const T*)x, (T*)y, mean, rstd, rows, h, r.nw));
+      GS_ROW_C(r.c, GS_TRY_E(launch_pdl(ln_fwd_vec_kernel<T, C>, dim3((rows + r.rpb - 1) / r.rpb),
+                                        dim3(32 * r.nw * r.rpb), 0, s, (const T*)x, (T*)y, mean, rstd, rows, h, r.nw)));
     } else {
       GS_ROW_E(h, ln_fwd_kernel<T, E><<<rows, kRowThreads, 0, s>>>((const T*)x, (T*)y, mean, rstd, h));
     }
@@ -531,8 +539,9 @@ cudaError_t layernorm_bwd(DType dt, const void* x, const float* mean, const floa
   GS_DISPATCH(dt, {
     if (h % Vec<T>::N == 0) {
       const RowShape r = row_shape(h, Vec<T>::N);
-      GS_ROW_C(r.c, ln_bwd_vec_kernel<T, C><<<(rows + r.rpb - 1) / r.rpb, 32 * r.nw * r.rpb, 0, s>>>(
-                        (const T*)x, mean, rstd, (const T*)dy, (const T*)res, (T*)dx, rows, h, r.nw));
+      GS_ROW_C(r.c, GS_TRY_E(launch_pdl(ln_bwd_vec_kernel<T, C>, dim3((rows + r.rpb - 1) / r.rpb),
+                                        dim3(32 * r.nw * r.rpb), 0, s, (const T*)x, mean, rstd, (const T*)dy,
+                                        (const T*)res, (T*)dx, rows, h, r.nw)));
     } else {
       if (res && res != dx) {
         cudaError_t e = cudaMemcpyAsync(dx, res, (size_t)rows * h * sizeof(T), cudaMemcpyDeviceToDevice, s);

@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_g, int M,
                    int N, int K, void* C, const bf16* R, bf16* G, int ldc, int sk_rem, float4* __restrict__ sk_ws,
                    int* __restrict__ sk_flags, int sk_epoch) {
+  pdl_trigger_and_wait();
   using Cfg = TileCfg<BN, CG>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -717,13 +718,15 @@ cudaError_t launch(const GemmArgs& g, cudaStream_t s) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = Cfg::kSmemBytes;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see pdl_trigger_and_wait
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   count_launch();
   return cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mg, g.M, g.N, g.K, g.C, (const bf16*)g.R, (bf16*)g.G,
                             g.ldc ? g.ldc : g.N, rem, sk ? sk->ws : nullptr, sk ? sk->flags : nullptr, epoch);
