@@ -83,6 +83,10 @@ inline int num_sms() {
 // grid's last CTAs run, but no CTA touches memory before its predecessor grid
 // has completed (griddepcontrol.wait), so stream order semantics are kept.
 // griddepcontrol.* are no-ops for a kernel launched without the attribute.
+// The wait comes first in every kernel, before TMEM allocation too: a
+// dependent CTA that allocated TMEM before its wait could starve a primary
+// CTA that has triggered but not yet allocated (measured: an 85k-token/s
+// outlier run with the wait moved after the allocation).
 // GS_PDL=0 launches without it.
 __device__ __forceinline__ void pdl_trigger_and_wait() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
