@@ -1,6 +1,2 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-timeout 900 python bench.py > gpurun_out/bench2.log 2>&1
-timeout 300 python tools/gemm_probe.py > gpurun_out/probe.jsonl 2>&1
+timeout 1500 python bench.py --config gpt13b-nvme --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench13.log 2>&1; echo "rc=$?" >> gpurun_out/bench13.log
