@@ -157,6 +157,20 @@ def test_bf16_engine_tracks_oracle():
     assert np.array_equal(reps[-1].ledger, gs.plan_traffic(plan))
 
 
+def test_bf16_engine_tcgen05_attention_tracks_oracle():
+    """The production kernels end to end: head_dim 128 and s % 256 == 0 put
+    the layers on the tcgen05 GEMMs, the two-tile attention forward (v3) and
+    the tcgen05 backward, with programmatic dependent launch between them."""
+    need_gpu()
+    g = ob.Geometry(n_layers=2, hidden=256, heads=2, seq=256, mb_size=2, vocab=512)
+    M, iters = 2, 3
+    plan, reps, losses, layers, fixed, tokens = run_engine(g, M, (1, 1, 1), 0.25, iters, lp=2)
+    ref_loss, ref_layers, _ = oracle_run(g, M, plan, tokens)
+    assert np.max(np.abs(losses - ref_loss) / ref_loss) < 2e-2
+    assert rel(layers, ref_layers) < 5e-2
+    assert np.array_equal(reps[-1].ledger, gs.plan_traffic(plan))
+
+
 @pytest.mark.parametrize("split,tier", [((1, 1, 1), 0), ((0, 0, 0), 0), ((0.3, 0.7, 0.5), 2)])
 def test_fp32_horizontal_engine_matches_oracle(split, tier):
     """The ablation baseline (build_horizontal, schedule.cpp:127-258) executes

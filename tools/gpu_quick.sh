@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 1500 python bench.py --config gpt13b-nvme --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench13.log 2>&1; echo "rc=$?" >> gpurun_out/bench13.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 600 python -m pytest tests/test_gpu_engine.py -q -k "bf16" > gpurun_out/t_bf16.log 2>&1; echo "rc=$?" >> gpurun_out/t_bf16.log
