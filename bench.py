@@ -3,25 +3,33 @@
 A step is one training iteration of the vertical (snake) plan with the
 alpha-delayed optimizer step, executed by the B200 executor through the
 C-ABI (gs_engine_run): every plan task runs for real (tcgen05 GEMMs, flash
-attention, fused Adam, PCIe DMA of params / checkpoints / gradients, NVMe I/O
-when the split puts data on SSD).
+attention, fused Adam, PCIe DMA of params / checkpoints / gradients /
+optimizer state, NVMe I/O when the split puts data on SSD).
 
-Workload (BASELINE.json configs[1]; GPT-65B, the metric's headline model, does
-not fit this box's 196 GB DRAM / 80 GB disk): GPT-1.3B (N=24, h=2048, 16 heads,
-s=2048, b=2, vocab 50304), M=16 micro-batches per iteration, split (1,1,1)
-(all params / checkpoints / optimizer state CPU-resident), alpha=0.2, bf16.
+Workload (BASELINE.json configs[1], as written): GPT-1.3B (N=24, h=2048, 16
+heads, s=2048, b=2, vocab 50304), M=16 micro-batches per iteration, split
+(1,1,1): params, checkpoints and the fp32 optimizer state (master, m, v) live
+in pinned host DRAM; every optimizer step streams its state slice through
+HBM (opt_tier 2) and the updated bf16 params back; alpha=0.2, bf16.  The
+optimizer-state streaming (24 B/element) is outside the reference's ledger
+and is counted in e2e's PCIe bytes and in the iteration roofline.  GPT-65B,
+the metric's headline model, does not fit this box (196 GB DRAM / 80 GB
+disk); `--config gpt65b-8layer` runs its layer geometry on an 8-layer slice
+with the optimizer state split between pinned DRAM and the NVMe file.
 
 --impl reference times the reference CPU path on the host cores: the
 reference's offsim carries no training arithmetic, so the timed CPU
-implementation is the C oracle port (oracle/gs_oracle.c, fp32, OpenMP) on a
-bounded sample (one layer's forward + recompute + backward at the workload's
-b*s tokens... see `cpu_sample`), extrapolated to the model.
+implementation is the C oracle port (oracle/gs_oracle.c, fp32, OpenMP) —
+each step one layer's forward + recompute + backward at b=1, s=2048, plus the
+tied LM head timed once — extrapolated to one training step of the workload.
 
-Multi-GPU: one process per GPU (torchrun).  ZeRO-3 data parallelism inside
-the executor: each rank runs its own M micro-batches (global batch grows with
-N: scaling "weak"), owns 1/N of every layer's params / grads / optimizer state,
-all-gathers layer shards (NCCL) before each stage and reduce-scatters the fp32
-layer gradient after it; rank 0 reports max-over-ranks time.
+Multi-GPU: one process per GPU (torchrun; `--gpus N` without torchrun
+re-launches itself under torch.distributed.run).  ZeRO-3 data parallelism
+inside the executor: each rank runs its own M micro-batches (global batch
+grows with N: scaling "weak"), owns 1/N of every layer's params / grads /
+optimizer state, all-gathers layer shards before each stage and
+reduce-scatters the fp32 layer gradient after it; rank 0 reports
+max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -43,20 +51,30 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 # one metric string for both arms (the driver computes the ours/reference ratio)
 METRIC = "tokens/sec (GPT-1.3B training, vertical schedule + alpha-delayed optimizer step, BASELINE configs[1])"
 
+OPT_TIERS = {0: "auto", 1: "HBM", 2: "pinned host DRAM, streamed through HBM per step"}
+
 CONFIGS = {
-    # name: (N, h, heads, s, b, vocab, M, split, alpha)
-    "gpt1.3b": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2),
-    "gpt1.3b-ssd-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 0.0), 0.2),
+    # name: (N, h, heads, s, b, vocab, M, split, alpha, opt_tier, ssd_ring_layers)
+    # BASELINE configs[1] as written: everything CPU-resident in pinned DRAM
+    "gpt1.3b": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2, 2, 8),
+    # the same with the CPU-resident optimizer fraction held in HBM instead
+    "gpt1.3b-hbm-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2, 1, 8),
+    "gpt1.3b-ssd-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 0.0), 0.2, 2, 8),
     # BASELINE configs[2] shape on this box (196 GB DRAM, 80 GB disk): half of
-    # the optimizer state (75.5 GB) on the NVMe tier, the other half in HBM
-    "gpt13b-nvme": (40, 5120, 40, 2048, 2, 50304, 16, (1.0, 1.0, 0.5), 0.2),
-    # GPT-65B layer geometry (h = 8192, 64 heads, b = 2) on a 4-layer slice of
-    # the vertical plan (M = 32, BASELINE configs[3] per-rank batch): the full
-    # 80-layer model needs 258 GB of CPU-resident fp32 grads (> this box's
-    # DRAM); per-stage work is per layer, so tokens/s x 4/80 projects it
-    "gpt65b-4layer": (4, 8192, 64, 2048, 2, 50304, 32, (1.0, 1.0, 1.0), 0.2),
-    "tiny": (4, 64, 4, 32, 2, 128, 4, (0.0, 0.0, 0.0), 0.25),
+    # the optimizer state (75.5 GB) on the NVMe tier, the other half in DRAM
+    "gpt13b-nvme": (40, 5120, 40, 2048, 2, 50304, 16, (1.0, 1.0, 0.5), 0.2, 2, 2),
+    # GPT-65B layer geometry (h = 8192, 64 heads, b = 2, M = 32: BASELINE
+    # configs[3] per rank, split (1,1,0.5)) on an 8-layer slice: the optimizer
+    # state half in pinned DRAM, half on the NVMe file (38.7 GB), never in HBM.
+    # The full 80-layer model needs 773 GB of optimizer state (> this box)
+    "gpt65b-8layer": (8, 8192, 64, 2048, 2, 50304, 32, (1.0, 1.0, 0.5), 0.2, 2, 2),
+    "tiny": (4, 64, 4, 32, 2, 128, 4, (0.0, 0.0, 0.0), 0.25, 2, 8),
 }
+
+
+def make_tokens(V, iters, M, b, s, seed):
+    """Synthetic token ids, uniform in [0, V), [iters][M][b][s+1]."""
+    return np.random.default_rng(seed).integers(0, V, size=(iters, M, b, s + 1), dtype=np.int32)
 
 
 def peaks():
@@ -168,50 +186,72 @@ def cpu_model() -> str:
     return f"{name}, nproc {os.cpu_count()}"
 
 
-def cpu_sample(cfg_name: str, budget_s: float = 20.0):
+_HEAD_S = {}
+
+
+def cpu_sample(cfg_name: str, head: bool = False):
     """Time the oracle port (fp32 C, OpenMP, all host threads) on one layer's
-    forward + recompute-and-backward at the workload's micro-batch geometry.
-    Returns (seconds per layer-microbatch, tokens, threads, description)."""
+    forward + recompute-and-backward at b=1 and the workload's full sequence
+    (or, head=True, the tied LM head: final LN, logits, CE, both grads).
+    Returns (seconds, threads)."""
     import oracle_bindings as ob
-    N, h, H, s, b, V, M, split, alpha = CONFIGS[cfg_name]
-    # bounded: b=1 and a shorter sequence keep one sample ~10 s on 16 cores
-    sb, ss = 1, min(s, 1024)
-    g = ob.Geometry(n_layers=N, hidden=h, heads=H, seq=ss, mb_size=sb, vocab=V)
+    N, h, H, s, b, V = CONFIGS[cfg_name][:6]
+    g = ob.Geometry(n_layers=N, hidden=h, heads=H, seq=s, mb_size=1, vocab=V)
     cfg = g.cfg()
     lib = ob.oracle()
     rng = np.random.default_rng(0)
-    w = (rng.standard_normal(12 * h * h) * 0.02).astype(np.float32)
-    x = rng.standard_normal(sb * ss * h).astype(np.float32)
-    dy = rng.standard_normal(sb * ss * h).astype(np.float32) * 0.01
-    y = np.empty_like(x)
-    dx = np.empty_like(x)
-    dw = np.zeros_like(w)
     f = lambda a: a.ctypes.data_as(C.POINTER(C.c_float))  # noqa: E731
+    x = rng.standard_normal(s * h).astype(np.float32)
+    dx = np.empty_like(x)
+    if head:
+        wte = (rng.standard_normal(V * h) * 0.02).astype(np.float32)
+        dwte = np.zeros_like(wte)
+        tok = rng.integers(0, V, s + 1, dtype=np.int32)
+        t0 = time.perf_counter()
+        lib.gso_head(C.byref(cfg), f(wte), f(x), tok.ctypes.data_as(C.POINTER(C.c_int32)), C.c_float(1.0 / s),
+                     f(dx), f(dwte))
+        return time.perf_counter() - t0, lib.gso_num_threads()
+    w = (rng.standard_normal(12 * h * h) * 0.02).astype(np.float32)
+    dy = rng.standard_normal(s * h).astype(np.float32) * 0.01
+    y = np.empty_like(x)
+    dw = np.zeros_like(w)
     t0 = time.perf_counter()
     lib.gso_layer_fwd(C.byref(cfg), f(w), f(x), f(y))
     lib.gso_layer_bwd(C.byref(cfg), f(w), f(x), f(dy), f(dx), f(dw))
-    dt = time.perf_counter() - t0
-    desc = (f"oracle C fp32 port, {lib.gso_num_threads()} threads: 1 layer fwd + recompute+bwd at b={sb}, s={ss} "
-            f"(h={h}); tokens/s = b*s / (N * t_layer); head, embedding and Adam not included")
-    return dt, sb * ss, lib.gso_num_threads(), desc
+    return time.perf_counter() - t0, lib.gso_num_threads()
+
+
+def cpu_step_estimate(cfg_name: str, t_layer: float):
+    """Extrapolate one training step of the workload from a layer sample and
+    the (cached) head sample: M*b sequences x (N layers + head)."""
+    N, h, H, s, b, V, M = CONFIGS[cfg_name][:7]
+    if cfg_name not in _HEAD_S:
+        _HEAD_S[cfg_name] = cpu_sample(cfg_name, head=True)[0]
+    t_step = M * b * (N * t_layer + _HEAD_S[cfg_name])
+    desc = (f"oracle C fp32 port: per step 1 layer fwd + recompute + bwd at b=1, s={s}, h={h} timed, the tied LM "
+            f"head (V={V}) timed once ({_HEAD_S[cfg_name]:.2f} s); step = M*b*(N*t_layer + t_head) with M={M}, b={b}, "
+            f"N={N}; embedding and the Adam step (< 0.1%) excluded")
+    return t_step, M * b * s, desc
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    N, h, H, s, b, V, M, split, alpha = CONFIGS[args.config]
     for _ in range(args.warmup if args.config == "tiny" else 0):
         cpu_sample(args.config)
-    times = []
+    steps, threads = [], 1
     for _ in range(args.steps):
-        dt, toks, threads, desc = cpu_sample(args.config)
-        times.append(dt)
-    t_layer = float(np.mean(times))
-    value = toks / (N * t_layer)
+        dt, threads = cpu_sample(args.config)
+        steps.append(cpu_step_estimate(args.config, dt))
+    t_step = float(np.mean([t for t, _, _ in steps]))
+    toks, desc = steps[0][1], steps[0][2]
+    value = toks / t_step
     line = {"impl": "reference", "metric": metric(args),
             "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_layer * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": t_step * 1e3,
+            "ms_per_step_note": "extrapolated CPU time of one training step of the workload (not the sample's)",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": config_dict(args),
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": desc,
@@ -227,16 +267,18 @@ def metric(args):
 
 
 def config_dict(args):
-    N, h, H, s, b, V, M, split, alpha = CONFIGS[args.config]
+    N, h, H, s, b, V, M, split, alpha, tier, ring = CONFIGS[args.config]
     M = args.microbatches or M
     alpha = args.alpha if args.alpha >= 0 else alpha
     alpha = alpha if args.schedule == "vertical" else 0.0
+    place = (f"CPU-resident fractions (split) in pinned host DRAM, the rest on the NVMe file; "
+             f"CPU-resident optimizer state: {OPT_TIERS[tier]}")
     return {"workload": f"{args.config}: GPT N={N} h={h} heads={H} s={s} b={b} vocab={V}, {args.schedule} schedule, "
-                        f"M={M} micro-batches/iteration, split(x_ckpt,x_param,x_opt)={split}, alpha={alpha}",
-            "schedule": args.schedule,
+                        f"M={M} micro-batches/iteration, split(x_ckpt,x_param,x_opt)={split}, alpha={alpha}; {place}",
+            "schedule": args.schedule, "opt_tier": OPT_TIERS[tier],
             "global_batch": M * b * max(args.gpus, 1), "seq_len": s, "microbatches": M, "alpha": alpha,
             "split": list(split), "parallelism": f"zero3-dp{args.gpus}" if args.gpus > 1 else "single",
-            "l2": "working set (2.4 GB params/iteration streamed) >> 126 MB L2; no flush needed"}
+            "l2": "working set (params / optimizer state streamed, GBs per iteration) >> 126 MB L2; no flush needed"}
 
 
 def calibrate_and_simulate(gs, eng, plan, model, tokens, K, dev_ms):
@@ -305,8 +347,9 @@ def run_ours(args):
     else:
         torch.cuda.set_device(0)
     import paper_2512_17570_b200 as gs
-    import oracle_bindings as ob
-    N, h, H, s, b, V, M, split, alpha = CONFIGS[args.config]
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world} ranks")
+    N, h, H, s, b, V, M, split, alpha, tier, ring = CONFIGS[args.config]
     M = args.microbatches or M
     alpha = args.alpha if args.alpha >= 0 else alpha
     model = gs.ModelSpec(N, h, H, s, b, 2, 4, 3, world)  # ZeRO-3 over the ranks
@@ -324,11 +367,10 @@ def run_ours(args):
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().numpy().tobytes())
     eng = gs.Engine(plan, model, V, gs.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0), seed=1234,
-                    device=torch.cuda.current_device(), nvme_dir=nvme, opt_tier=0, profile=True, rank=rank,
-                    world=world, nccl_id=nccl_id)
-    g = ob.Geometry(n_layers=N, hidden=h, heads=H, seq=s, mb_size=b, vocab=V)
+                    device=torch.cuda.current_device(), nvme_dir=nvme, opt_tier=tier, profile=True, rank=rank,
+                    world=world, nccl_id=nccl_id, ssd_ring_layers=ring)
     K, W = args.steps, args.warmup
-    tokens = ob.make_tokens(g, W + 2 * K, M, seed=7 + rank)
+    tokens = make_tokens(V, W + 2 * K, M, b, s, seed=7 + rank)
     # warm-up (untimed)
     eng.set_profiling(0)
     eng.run(tokens[:W])
@@ -384,11 +426,12 @@ def run_ours(args):
             "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)"}
     # iteration roofline (north star): max of compute at peak and ledger bytes over measured links
     bw = pcie_bandwidth(torch)
-    led = rep.ledger
+    led, ext = rep.ledger, rep.extension
     flops_iter = N * 4 * (24 * h * h + 2 * s * h) * tokens_per_step
     t_comp = flops_iter / (tf_sust * 1e12)
-    t_h2d = float(led[0].sum()) / bw["h2d"]
-    t_d2h = float(led[1].sum()) / bw["d2h"]
+    # PCIe: the plan's ledger plus the GPU optimizer's state streaming
+    t_h2d = float(led[0].sum() + ext[0].sum()) / bw["h2d"]
+    t_d2h = float(led[1].sum() + ext[1].sum()) / bw["d2h"]
     t_ssd, nvme = 0.0, None
     if float(led[2].sum() + led[3].sum()) > 0:
         # the NVMe tier's own bandwidth (O_DIRECT, 8 x 8 MiB in flight), both
@@ -419,13 +462,15 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "tokens/s", "wall_s": e2e_wall,
                     "h2d_bytes_per_step": int(M * b * (s + 1) * 4 + led[0].sum() + rep.extension[0].sum()),
                     "d2h_bytes_per_step": int(8 + led[1].sum() + rep.extension[1].sum()),
-                    "note": "tokens from pageable host memory copied per step; PCIe bytes are the plan's offload "
-                            "traffic + GPU-optimizer extension, all inside the timed region"},
+                    "note": "host token ids copied to pinned memory and read by the GPU every step, losses read "
+                            "back; PCIe bytes = the plan's offload ledger + the GPU optimizer's state / param "
+                            "streaming (extension ledger), all inside the timed region"},
             "gpu_launches": rep.gpu_launches,
             "roofline": roof,
             "iteration_roofline": {"t_roof_ms": t_roof * 1e3, "t_measured_ms": ms_step, "frac": t_roof / (ms_step / 1e3),
                                    "t_compute_ms": t_comp * 1e3, "t_pcie_h2d_ms": t_h2d * 1e3,
                                    "t_pcie_d2h_ms": t_d2h * 1e3, "t_ssd_ms": t_ssd * 1e3, "nvme": nvme,
+                                   "pcie_bytes": "ledger + extension (optimizer-state streaming) per direction",
                                    "pcie_h2d_gbs": bw["h2d"] / 1e9,
                                    "pcie_d2h_gbs": bw["d2h"] / 1e9, "flops_per_iteration": flops_iter,
                                    "compute_roofline_tokens_s": tokens_per_step / t_comp,
@@ -444,14 +489,10 @@ def run_ours(args):
             "losses": rep.losses,
             "model_vs_measured": calib,
             "clocks": clk.summary()}
-    if args.config == "gpt65b-4layer":
-        line["projection_80_layers"] = {
-            "tokens_s": value * N / 80.0, "method": "4-layer slice tokens/s x 4/80: every stage's compute and "
-            "transfers are per layer, so an 80-layer iteration takes 20x the slice's (pipeline fill ignored)",
-            "compute_roofline_tokens_s_80_layers": tokens_per_step / (t_comp * 80.0 / N)}
     if not args.no_cpu_baseline:
-        dt, toks, threads, desc = cpu_sample(args.config)
-        line["cpu_baseline"] = {"value": toks / (N * dt), "unit": "tokens/s", "cores": threads, "kind": "port",
+        dt, threads = cpu_sample(args.config)
+        t_step, toks, desc = cpu_step_estimate(args.config, dt)
+        line["cpu_baseline"] = {"value": toks / t_step, "unit": "tokens/s", "cores": threads, "kind": "port",
                                 "sample": desc, "cpu": cpu_model()}
     print(json.dumps(line), flush=True)
 
@@ -470,6 +511,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--calibrate", type=int, default=1, help="calibrate offsim::simulate from the trace")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -79,6 +79,9 @@ int gs_plan_build_horizontal(const gs_model_spec* model, int num_microbatches, c
 int gs_plan_from_json(const char* json, gs_plan** out);
 void gs_plan_free(gs_plan* plan);
 int gs_plan_num_tasks(const gs_plan* plan);
+/* SchedulePlan header fields (schedule.hpp:58-71): variant (0 single-fb,
+   1 horizontal, 2 vertical), delay ratio, micro-batches, layers */
+int gs_plan_info(const gs_plan* plan, int* variant, double* alpha, int* num_microbatches, int* num_layers);
 int gs_plan_task(const gs_plan* plan, int index, gs_task* out);
 /* deps of task `index` into out[0..cap) ; *n = number of deps */
 int gs_plan_task_deps(const gs_plan* plan, int index, int* out, int cap, int* n);
@@ -174,6 +177,8 @@ int gs_engine_flush(gs_engine* engine);
 /* fp32 master weights: layers [N][12 h^2], fixed [(V + s) h]; either may be NULL */
 int gs_engine_read_params(gs_engine* engine, float* layers, float* fixed);
 int gs_engine_read_moments(gs_engine* engine, float* layer_m, float* layer_v);
+/* fp32 Adam moments of the embedding / position table [(V+s)*h] (either may be NULL) */
+int gs_engine_read_fixed_moments(gs_engine* engine, float* m, float* v);
 /* per kernel class of the last run: 0 gemm, 1 attention_fwd, 2 attention_bwd,
    3 layernorm, 4 other — algorithmic flops, CUDA-event ms and count of the
    sampled launches, and all launches of the class */

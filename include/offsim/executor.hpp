@@ -103,8 +103,9 @@ class Executor {
   void flush();
   // fp32 master weights: layers [N][12h^2], fixed [(V+s)*h] (wte then wpe).
   void read_params(float* layers, float* fixed);
-  // fp32 optimizer moments, same layout as read_params.
-  void read_moments(float* layer_m, float* layer_v);
+  // fp32 optimizer moments, same layout as read_params (fixed_m / fixed_v:
+  // the embedding / position table's, [(V+s)*h]; may be null).
+  void read_moments(float* layer_m, float* layer_v, float* fixed_m = nullptr, float* fixed_v = nullptr);
   // Per kernel class of the last run (profile_kernels): algorithmic flops,
   // summed CUDA-event milliseconds and launches.  Classes: gemm,
   // attention_fwd, attention_bwd, layernorm, other.

@@ -67,17 +67,43 @@ void gso_make_tokens(const gso_cfg* c, uint64_t seed, int iteration, int microba
 }
 
 /* --------------------------------------------------------------- GEMMs */
-/* C[M,N] (+)= A[M,K] * B[K,N] */
+/* C[M,N] (+)= A[M,K] * B[K,N].  Rows go in blocks of four so each B row
+ * loaded from memory feeds four accumulator rows; every C element still sums
+ * over k in increasing order (the per-element arithmetic is unchanged). */
 static void gemm_nn(const float* A, const float* B, float* C, int M, int N, int K, int accumulate) {
+  const int nb = (M + 3) / 4;
 #pragma omp parallel for schedule(static)
-  for (int i = 0; i < M; ++i) {
-    float* c = C + (long long)i * N;
-    if (!accumulate) memset(c, 0, sizeof(float) * (size_t)N);
-    const float* a = A + (long long)i * K;
-    for (int k = 0; k < K; ++k) {
-      const float av = a[k];
-      const float* b = B + (long long)k * N;
-      for (int j = 0; j < N; ++j) c[j] += av * b[j];
+  for (int ib = 0; ib < nb; ++ib) {
+    const int i0 = 4 * ib, rows = M - i0 < 4 ? M - i0 : 4;
+    float* c[4];
+    const float* a[4];
+    for (int r = 0; r < 4; ++r) {
+      const int i = i0 + (r < rows ? r : 0);
+      c[r] = C + (long long)i * N;
+      a[r] = A + (long long)i * K;
+    }
+    for (int r = 0; r < rows; ++r)
+      if (!accumulate) memset(c[r], 0, sizeof(float) * (size_t)N);
+    if (rows == 4) {
+      float *c0 = c[0], *c1 = c[1], *c2 = c[2], *c3 = c[3];
+      for (int k = 0; k < K; ++k) {
+        const float a0 = a[0][k], a1 = a[1][k], a2 = a[2][k], a3 = a[3][k];
+        const float* b = B + (long long)k * N;
+        for (int j = 0; j < N; ++j) {
+          const float bj = b[j];
+          c0[j] += a0 * bj;
+          c1[j] += a1 * bj;
+          c2[j] += a2 * bj;
+          c3[j] += a3 * bj;
+        }
+      }
+    } else {
+      for (int r = 0; r < rows; ++r)
+        for (int k = 0; k < K; ++k) {
+          const float av = a[r][k];
+          const float* b = B + (long long)k * N;
+          for (int j = 0; j < N; ++j) c[r][j] += av * b[j];
+        }
     }
   }
 }
@@ -92,15 +118,36 @@ static void gemm_nt(const float* A, const float* B, float* C, int M, int N, int 
   free(bt);
 }
 
-/* C[M,N] += A[K,M]^T * B[K,N]  (weight gradient: A = dY, B = X) */
+/* C[M,N] += A[K,M]^T * B[K,N]  (weight gradient: A = dY, B = X); four
+ * output rows per B row load, per-element order over k unchanged. */
 static void gemm_tn_acc(const float* A, const float* B, float* C, int M, int N, int K) {
+  const int nb = (M + 3) / 4;
 #pragma omp parallel for schedule(static)
-  for (int i = 0; i < M; ++i) {
-    float* c = C + (long long)i * N;
-    for (int k = 0; k < K; ++k) {
-      const float av = A[(long long)k * M + i];
-      const float* b = B + (long long)k * N;
-      for (int j = 0; j < N; ++j) c[j] += av * b[j];
+  for (int ib = 0; ib < nb; ++ib) {
+    const int i0 = 4 * ib, rows = M - i0 < 4 ? M - i0 : 4;
+    if (rows == 4) {
+      float *c0 = C + (long long)i0 * N, *c1 = c0 + N, *c2 = c1 + N, *c3 = c2 + N;
+      for (int k = 0; k < K; ++k) {
+        const float* ar = A + (long long)k * M + i0;
+        const float a0 = ar[0], a1 = ar[1], a2 = ar[2], a3 = ar[3];
+        const float* b = B + (long long)k * N;
+        for (int j = 0; j < N; ++j) {
+          const float bj = b[j];
+          c0[j] += a0 * bj;
+          c1[j] += a1 * bj;
+          c2[j] += a2 * bj;
+          c3[j] += a3 * bj;
+        }
+      }
+    } else {
+      for (int r = 0; r < rows; ++r) {
+        float* c = C + (long long)(i0 + r) * N;
+        for (int k = 0; k < K; ++k) {
+          const float av = A[(long long)k * M + i0 + r];
+          const float* b = B + (long long)k * N;
+          for (int j = 0; j < N; ++j) c[j] += av * b[j];
+        }
+      }
     }
   }
 }
@@ -150,6 +197,7 @@ static void ln_bwd(const float* x, const float* mean, const float* rstd, const f
 static void attn_fwd(const gso_cfg* c, const float* qkv, float* o, float* lse) {
   const int s = c->seq, h = c->hidden, H = c->heads, d = h / H, b = c->mb_size;
   const float scale = 1.0f / sqrtf((float)d);
+  if (d > 128) abort(); /* head_dim <= 128, as the executor requires */
 #pragma omp parallel for collapse(2) schedule(dynamic)
   for (int bh = 0; bh < b * H; ++bh)
     for (int t = 0; t < s; ++t) {
@@ -166,13 +214,15 @@ static void attn_fwd(const gso_cfg* c, const float* qkv, float* o, float* lse) {
       }
       double z = 0;
       for (int u = 0; u <= t; ++u) z += exp(p[u] - mx);
-      float* out = o + ((long long)(bi * s + t)) * h + j * d;
-      for (int e = 0; e < d; ++e) {
-        double acc = 0;
-        for (int u = 0; u <= t; ++u)
-          acc += exp(p[u] - mx) / z * qkv[((long long)(bi * s + u)) * 3 * h + 2 * h + j * d + e];
-        out[e] = (float)acc;
+      for (int u = 0; u <= t; ++u) p[u] = exp(p[u] - mx) / z; /* probabilities */
+      double acc[128];
+      for (int e = 0; e < d; ++e) acc[e] = 0;
+      for (int u = 0; u <= t; ++u) { /* each output element sums over u in increasing order */
+        const float* v = qkv + ((long long)(bi * s + u)) * 3 * h + 2 * h + j * d;
+        for (int e = 0; e < d; ++e) acc[e] += p[u] * v[e];
       }
+      float* out = o + ((long long)(bi * s + t)) * h + j * d;
+      for (int e = 0; e < d; ++e) out[e] = (float)acc[e];
       lse[(long long)bh * s + t] = (float)(mx + log(z));
       free(p);
     }

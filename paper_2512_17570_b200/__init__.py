@@ -230,6 +230,13 @@ class SchedulePlan:
     def __len__(self) -> int:
         return lib().gs_plan_num_tasks(self._h)
 
+    def info(self) -> dict:
+        """Header fields: variant, alpha (delay ratio), microbatches, layers."""
+        v, a, m, n = C.c_int(), C.c_double(), C.c_int(), C.c_int()
+        check(lib().gs_plan_info(self._h, C.byref(v), C.byref(a), C.byref(m), C.byref(n)))
+        return dict(variant=("single-fb", "horizontal", "vertical")[v.value], alpha=a.value, microbatches=m.value,
+                    layers=n.value)
+
     def task(self, i: int) -> dict:
         t = _Task()
         check(lib().gs_plan_task(self._h, i, C.byref(t)))
@@ -467,7 +474,7 @@ class Engine:
         self.model = model
         self.vocab_size = vocab_size
         self.plan = plan
-        self.microbatches = plan.as_dict()["microbatches"] if len(plan) < 20000 else None
+        self.microbatches = plan.info()["microbatches"]
         self._nvme = nvme_dir.encode()
         self._id = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         cfg = _EngineConfig(model._c(), vocab_size, adam.lr, adam.beta1, adam.beta2, adam.eps, adam.weight_decay,
@@ -491,11 +498,20 @@ class Engine:
             device_ptr: int | None = None) -> RunReport:
         """tokens: int32 array [iterations][M][b][s+1] (host); or pass
         device_ptr (an int address) with tokens_on_device=True."""
+        m = self.model
+        shape = (self.microbatches, m.microbatch_size, m.seq_len + 1)
         if device_ptr is None:
             tok = np.ascontiguousarray(tokens, dtype=np.int32)
             iterations = tok.shape[0] if iterations is None else iterations
+            if tok.shape != (iterations,) + shape:
+                raise ValidationError(f"tokens must have shape {(iterations,) + shape} "
+                                      f"[iterations][M][b][s+1], got {tok.shape}")
+            if tok.size and (int(tok.min()) < 0 or int(tok.max()) >= self.vocab_size):
+                raise ValidationError(f"token ids must lie in [0, {self.vocab_size})")
             ptr = tok.ctypes.data_as(C.c_void_p)
         else:
+            if iterations is None or iterations < 1:
+                raise ValidationError("device tokens need iterations >= 1")
             ptr = C.c_void_p(device_ptr)
         losses = (C.c_double * iterations)()
         rep = _RunReport()
@@ -541,4 +557,10 @@ class Engine:
         m = np.empty((self.model.num_layers, P), np.float32)
         v = np.empty_like(m)
         check(lib().gs_engine_read_moments(self._h, m.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p)))
+        return m, v
+
+    def read_fixed_moments(self):
+        n = (self.vocab_size + self.model.seq_len) * self.model.hidden_dim
+        m, v = np.empty(n, np.float32), np.empty(n, np.float32)
+        check(lib().gs_engine_read_fixed_moments(self._h, m.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p)))
         return m, v

@@ -144,6 +144,15 @@ int gs_plan_from_json(const char* json, gs_plan** out) {
 }
 void gs_plan_free(gs_plan* plan) { delete plan; }
 int gs_plan_num_tasks(const gs_plan* plan) { return plan ? static_cast<int>(plan->plan.tasks.size()) : -1; }
+int gs_plan_info(const gs_plan* plan, int* variant, double* alpha, int* num_microbatches, int* num_layers) {
+  return guarded([&] {
+    if (!plan) throw offsim::ValidationError("plan is NULL");
+    if (variant) *variant = static_cast<int>(plan->plan.kind.variant);
+    if (alpha) *alpha = plan->plan.kind.delay_ratio;
+    if (num_microbatches) *num_microbatches = plan->plan.num_microbatches;
+    if (num_layers) *num_layers = plan->plan.num_layers;
+  });
+}
 int gs_plan_task(const gs_plan* plan, int index, gs_task* out) {
   return guarded([&] {
     if (!plan || index < 0 || index >= static_cast<int>(plan->plan.tasks.size()))
@@ -318,6 +327,12 @@ int gs_engine_read_params(gs_engine* engine, float* layers, float* fixed) {
 }
 int gs_engine_read_moments(gs_engine* engine, float* m, float* v) {
   return guarded([&] { engine->ex->read_moments(m, v); });
+}
+int gs_engine_read_fixed_moments(gs_engine* engine, float* m, float* v) {
+  return guarded([&] {
+    if (!engine) throw offsim::ValidationError("engine is NULL");
+    engine->ex->read_moments(nullptr, nullptr, m, v);
+  });
 }
 int gs_engine_kernel_profile(gs_engine* engine, double flops[5], double ms[5], int launches[5],
                              int64_t total_launches[5]) {

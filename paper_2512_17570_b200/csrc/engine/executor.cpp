@@ -165,6 +165,7 @@ struct Executor::Impl {
   std::vector<void*> in_x, out_y, in_g, out_g;  // [2*M] each, index p*M+m
   int32_t* dev_tok[2] = {nullptr, nullptr};
   double* dev_loss = nullptr;  // [loss_cap] per run iteration
+  int* dev_bad_tokens = nullptr;  // count of out-of-vocabulary token ids seen by the run
   int loss_cap = 0;
   float* opt_stage = nullptr;  // 12 * chunk floats
   void* lp_stage = nullptr;    // chunk lp elements
@@ -178,7 +179,8 @@ struct Executor::Impl {
   bool ssd_param = false, ssd_opt = false, ssd_ckpt = false;
   std::vector<Blob> param_blob, opt_blob;  // [N]
   std::vector<Blob> ckpt_blob;             // [N*M]
-  std::vector<uint8_t*> host_grad;         // [N]
+  std::vector<uint8_t*> host_grad;         // [host_grad_ring], slot = layer % ring
+  int host_grad_ring = 1;
   std::vector<uint8_t*> host_ilg;          // [2*M]
   int32_t* tok_pinned = nullptr;
   long long tok_capacity = 0;
@@ -278,6 +280,27 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
     throw ValidationError("executor: data-parallel execution covers the vertical schedule");
   if (plan.num_layers != ms.num_layers) throw ValidationError("executor: plan and model disagree on num_layers");
   if (cfg.vocab_size < 2) throw ValidationError("executor: vocab_size must be >= 2");
+  if (cfg.world > 1 && (12ull * ms.hidden_dim * ms.hidden_dim) % static_cast<u64>(cfg.world) != 0)
+    throw ValidationError("executor: 12*hidden^2 must divide by the number of ranks (equal ZeRO-3 shards)");
+  {
+    // Buffers are sized from cfg.model, transfers from the plan's task bytes:
+    // the plan must be the one the builder produces for this model (a plan
+    // built for another width / dp degree / precision would overrun them).
+    // A reference-dumped plan passes: the builders are byte-identical.
+    const SchedulePlan want = horizontal ? build_horizontal(ms, plan.num_microbatches, plan.split)
+                                         : build_vertical(ms, plan.num_microbatches, plan.split, plan.kind.delay_ratio);
+    if (want.tasks.size() != plan.tasks.size())
+      throw ValidationError("executor: plan does not match the model (" + std::to_string(plan.tasks.size()) +
+                            " tasks, the model's plan has " + std::to_string(want.tasks.size()) + ")");
+    for (size_t i = 0; i < want.tasks.size(); ++i) {
+      const Task &a = plan.tasks[i], &b = want.tasks[i];
+      if (a.kind != b.kind || a.layer != b.layer || a.microbatch != b.microbatch || a.stage != b.stage ||
+          a.data != b.data || a.link != b.link || a.bytes != b.bytes || a.elements != b.elements ||
+          a.deps != b.deps || a.cross_iter_dep != b.cross_iter_dep)
+        throw ValidationError("executor: plan task " + std::to_string(i) +
+                              " does not match the model's plan (bytes / geometry / dp degree differ)");
+    }
+  }
 
   N = ms.num_layers;
   M = plan.num_microbatches;
@@ -364,6 +387,8 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   }
   const u64 tok_bytes = 4ull * M * d.b * (d.s + 1);
   for (int i = 0; i < 2; ++i) dev_tok[i] = static_cast<int32_t*>(dmalloc(tok_bytes));
+  dev_bad_tokens = static_cast<int*>(dmalloc(sizeof(int)));
+  cuda_check(cudaMemset(dev_bad_tokens, 0, sizeof(int)), "memset");
   chunk = static_cast<long long>(std::min<u64>(P, 32ull << 20));
   chunk = (chunk + 3) / 4 * 4;
   opt_stage = static_cast<float*>(dmalloc(12ull * chunk));
@@ -384,8 +409,14 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
     param_blob.push_back(
         make_blob(lp * Ps, {lp * loc_now}, cpu_portion(lp * Ps, plan.split.x_param), false, ring_param, l % ring_k));
     opt_blob.push_back(make_blob(opt_bytes, {12 * loc_now}, cpu_opt, opt_hbm, ring_opt, l % ring_k));
-    host_grad.push_back(arena.alloc(4 * Ps));
   }
+  // GradAccum D2H landing buffers.  The horizontal schedule reads a layer's
+  // partial sum back for the next micro-batch, so it keeps one per layer;
+  // in the vertical schedule the optimizer consumes the gradient in HBM and
+  // the plan's D2H (schedule.cpp:489-494) only has to land somewhere: a
+  // two-slot ring (N x 4P of pinned DRAM would be 258 GB at GPT-65B).
+  host_grad_ring = horizontal ? N : std::min(N, 2);
+  for (int i = 0; i < host_grad_ring; ++i) host_grad.push_back(arena.alloc(4 * Ps));
   for (int l = 0; l < N; ++l)
     for (int m = 0; m < M; ++m)
       ckpt_blob.push_back(
@@ -743,9 +774,9 @@ void Executor::Impl::hazards() {
           case DataKind::GradAccum:
             if (t.link == LinkKind::PCIe_D2H) {
               R(slot_id(kGrad, l % grad_ring));
-              W(slot_id(kHostGrad, l));
+              W(slot_id(kHostGrad, l % host_grad_ring));
             } else {  // horizontal accumulation fetch
-              R(slot_id(kHostGrad, l));
+              R(slot_id(kHostGrad, l % host_grad_ring));
               W(slot_id(kGrad, l % grad_ring));
             }
             break;
@@ -970,13 +1001,13 @@ void Executor::Impl::compute_task(const Task& t, int it) {
     // pinned buffer by an SM copy kernel (a cudaMemcpy would queue on the
     // copy engines behind the plan's bulk parameter / checkpoint DMA)
     const int32_t* src = run_tokens + static_cast<long long>(it) * tok_n;
-    const uint32_t* from = reinterpret_cast<const uint32_t*>(src);
+    const int32_t* from = src;
     if (!run_tokens_dev) {
       void* dp = nullptr;
       cuda_check(cudaHostGetDevicePointer(&dp, const_cast<int32_t*>(src), 0), "token device pointer");
-      from = static_cast<const uint32_t*>(dp);
+      from = static_cast<const int32_t*>(dp);
     }
-    cuda_check(gs::copy_words(reinterpret_cast<uint32_t*>(dev_tok[slot]), from, tok_n, s_gpu), "tokens");
+    cuda_check(gs::copy_tokens(dev_tok[slot], from, tok_n, d.V, dev_bad_tokens, s_gpu), "tokens");
     lc.n += 1;
     cuda_check(cudaMemsetAsync(dev_loss + it, 0, sizeof(double), s_gpu), "loss");
     if (fixed_done < git) {  // embedding / head step with the previous iteration's grads
@@ -1196,9 +1227,13 @@ void Executor::Impl::xfer_task(const Task& t, int it, u64& phys) {
     case DataKind::GradAccum: {
       float* g = grad_shard[static_cast<size_t>(l % grad_ring)];
       if (t.link == LinkKind::PCIe_D2H) {
-        cuda_check(cudaMemcpyAsync(host_grad[static_cast<size_t>(l)], g, t.bytes, cudaMemcpyDeviceToHost, s_d2h), "grad");
+        cuda_check(cudaMemcpyAsync(host_grad[static_cast<size_t>(l % host_grad_ring)], g, t.bytes,
+                                   cudaMemcpyDeviceToHost, s_d2h),
+                   "grad");
       } else {
-        cuda_check(cudaMemcpyAsync(g, host_grad[static_cast<size_t>(l)], t.bytes, cudaMemcpyHostToDevice, s_h2d), "grad");
+        cuda_check(cudaMemcpyAsync(g, host_grad[static_cast<size_t>(l % host_grad_ring)], t.bytes,
+                                   cudaMemcpyHostToDevice, s_h2d),
+                   "grad");
       }
       phys = t.bytes;
       break;
@@ -1271,6 +1306,12 @@ ExecReport Executor::run(int iterations, const int32_t* tokens, bool tokens_on_d
   if (!tokens) throw ValidationError("run: tokens required");
   const long long tok_n = 1LL * I.M * I.d.b * (I.d.s + 1);
   if (!tokens_on_device) {
+    // ids index wte / dwte: reject out-of-vocabulary ids before any copy
+    const long long n = tok_n * iterations;
+    for (long long i = 0; i < n; ++i)
+      if (tokens[i] < 0 || tokens[i] >= I.d.V)
+        throw ValidationError("run: token id " + std::to_string(tokens[i]) + " at index " + std::to_string(i) +
+                              " is outside [0, vocab_size)");
     if (I.tok_capacity < tok_n * iterations) {
       I.tok_pinned = reinterpret_cast<int32_t*>(I.arena.alloc(4ull * tok_n * iterations));
       I.tok_capacity = tok_n * iterations;
@@ -1339,6 +1380,13 @@ ExecReport Executor::run(int iterations, const int32_t* tokens, bool tokens_on_d
             iterations, ms, 1e3 * I.host_enqueue_s, 1e3 * I.host_wait_s);
   cuda_check(cudaMemcpy(loss.data(), I.dev_loss, sizeof(double) * loss.size(), cudaMemcpyDeviceToHost), "loss");
   cudaEventDestroy(ev_end);
+  int bad = 0;
+  cuda_check(cudaMemcpy(&bad, I.dev_bad_tokens, sizeof(int), cudaMemcpyDeviceToHost), "token check");
+  if (bad) {
+    cuda_check(cudaMemset(I.dev_bad_tokens, 0, sizeof(int)), "memset");
+    throw ValidationError("run: " + std::to_string(bad) +
+                          " device token ids were outside [0, vocab_size) (replaced by 0; the run is invalid)");
+  }
   const double denom = static_cast<double>(I.d.T()) * I.M;
   for (int it = 0; it < iterations; ++it) rep.losses.push_back(loss[static_cast<size_t>(it)] / denom);
   if (I.cfg.record_trace) {
@@ -1414,13 +1462,15 @@ void Executor::read_params(float* layers, float* fixed) {
   if (fixed) cuda_check(cudaMemcpy(fixed, I.fx_master, 4 * I.n_fixed, cudaMemcpyDeviceToHost), "read fixed");
 }
 
-void Executor::read_moments(float* layer_m, float* layer_v) {
+void Executor::read_moments(float* layer_m, float* layer_v, float* fixed_m, float* fixed_v) {
   Impl& I = *impl_;
   cuda_check(cudaDeviceSynchronize(), "sync");
   for (int l = 0; l < I.N; ++l) {
     if (layer_m) read_field(I, l, 1, layer_m + static_cast<size_t>(l) * I.P);
     if (layer_v) read_field(I, l, 2, layer_v + static_cast<size_t>(l) * I.P);
   }
+  if (fixed_m) cuda_check(cudaMemcpy(fixed_m, I.fx_m, 4 * I.n_fixed, cudaMemcpyDeviceToHost), "read fixed m");
+  if (fixed_v) cuda_check(cudaMemcpy(fixed_v, I.fx_v, 4 * I.n_fixed, cudaMemcpyDeviceToHost), "read fixed v");
 }
 
 namespace {

@@ -124,13 +124,46 @@ std::string Uring::transfer(int file_fd, bool write, uint64_t off, uint8_t* buf,
   std::vector<Req> todo;
   for (uint64_t pos = 0; pos < bytes; pos += piece) todo.push_back({pos, std::min(piece, bytes - pos)});
   size_t next = 0;
-  unsigned inflight = 0;
+  // Accounting from the rings themselves: the kernel advances the SQ head as
+  // it consumes entries, so `queued - consumed` entries wait in the SQ and
+  // `consumed - completed` requests are in flight, whatever io_uring_enter
+  // returned.
+  const unsigned head0 = __atomic_load_n(sq_head_, __ATOMIC_ACQUIRE);
+  unsigned tail = __atomic_load_n(sq_tail_, __ATOMIC_RELAXED);
+  unsigned completed = 0;
+  std::string err;
   io_uring_sqe* sqes = static_cast<io_uring_sqe*>(sqes_);
   io_uring_cqe* cqes = static_cast<io_uring_cqe*>(cqes_);
-  while (next < todo.size() || inflight > 0) {
-    unsigned queued = 0;
-    unsigned tail = __atomic_load_n(sq_tail_, __ATOMIC_RELAXED);
-    while (next < todo.size() && inflight + queued < depth_) {
+  auto reap = [&] {
+    unsigned head = __atomic_load_n(cq_head_, __ATOMIC_RELAXED);
+    const unsigned ctail = __atomic_load_n(cq_tail_, __ATOMIC_ACQUIRE);
+    for (; head != ctail; ++head) {
+      const io_uring_cqe& c = cqes[head & *cq_mask_];
+      ++completed;
+      if (!err.empty()) continue;  // draining after an error
+      const Req q = todo[static_cast<size_t>(c.user_data)];
+      if (c.res < 0) err = std::string(write ? "write: " : "read: ") + std::strerror(-c.res);
+      else if (c.res == 0) err = std::string(write ? "write" : "read") + ": unexpected EOF";
+      else if (static_cast<uint64_t>(c.res) < q.len)  // short transfer: queue the rest
+        todo.push_back({q.pos + static_cast<uint64_t>(c.res), q.len - static_cast<uint64_t>(c.res)});
+    }
+    __atomic_store_n(cq_head_, head, __ATOMIC_RELEASE);
+  };
+  for (;;) {
+    const unsigned consumed = __atomic_load_n(sq_head_, __ATOMIC_ACQUIRE) - head0;
+    const unsigned queued = tail - head0;
+    const unsigned inflight = consumed - completed, waiting = queued - consumed;
+    if (!err.empty()) {
+      // stop issuing: withdraw entries the kernel has not consumed, then
+      // drain the in-flight requests so no CQE outlives this call
+      if (waiting) __atomic_store_n(sq_tail_, tail -= waiting, __ATOMIC_RELEASE);
+      if (inflight == 0) return err;
+      syscall(__NR_io_uring_enter, fd_, 0, 1, IORING_ENTER_GETEVENTS, nullptr, 0);
+      reap();
+      continue;
+    }
+    if (next >= todo.size() && inflight == 0 && waiting == 0) return {};
+    while (next < todo.size() && (tail - head0) - completed < depth_) {
       const unsigned idx = tail & *sq_mask_;
       io_uring_sqe& e = sqes[idx];
       std::memset(&e, 0, sizeof(e));
@@ -143,27 +176,14 @@ std::string Uring::transfer(int file_fd, bool write, uint64_t off, uint8_t* buf,
       sq_array_[idx] = idx;
       ++tail;
       ++next;
-      ++queued;
     }
     __atomic_store_n(sq_tail_, tail, __ATOMIC_RELEASE);
-    const long r = syscall(__NR_io_uring_enter, fd_, queued, 1, IORING_ENTER_GETEVENTS, nullptr, 0);
-    if (r < 0 && errno != EINTR) return std::string("io_uring_enter: ") + std::strerror(errno);
-    inflight += queued;
-    unsigned head = __atomic_load_n(cq_head_, __ATOMIC_RELAXED);
-    const unsigned ctail = __atomic_load_n(cq_tail_, __ATOMIC_ACQUIRE);
-    for (; head != ctail; ++head) {
-      const io_uring_cqe& c = cqes[head & *cq_mask_];
-      --inflight;
-      Req& q = todo[static_cast<size_t>(c.user_data)];
-      if (c.res < 0) return std::string(write ? "write: " : "read: ") + std::strerror(-c.res);
-      if (c.res == 0) return std::string(write ? "write" : "read") + ": unexpected EOF";
-      if (static_cast<uint64_t>(c.res) < q.len) {  // short transfer: queue the rest
-        todo.push_back({q.pos + static_cast<uint64_t>(c.res), q.len - static_cast<uint64_t>(c.res)});
-      }
-    }
-    __atomic_store_n(cq_head_, head, __ATOMIC_RELEASE);
+    const unsigned to_submit = tail - __atomic_load_n(sq_head_, __ATOMIC_ACQUIRE);
+    const long r = syscall(__NR_io_uring_enter, fd_, to_submit, 1, IORING_ENTER_GETEVENTS, nullptr, 0);
+    if (r < 0 && errno != EINTR && errno != EAGAIN && errno != EBUSY)
+      err = std::string("io_uring_enter: ") + std::strerror(errno);
+    reap();
   }
-  return {};
 }
 
 NvmeFile::NvmeFile(const std::string& dir, bool odirect, int threads) : read_pool_(threads), write_pool_(threads) {

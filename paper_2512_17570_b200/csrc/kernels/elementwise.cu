@@ -583,6 +583,30 @@ cudaError_t copy_words(uint32_t* dst, const uint32_t* src, long long n, cudaStre
   return cudaGetLastError();
 }
 
+// Token ids of an iteration: copied (src may be mapped pinned host memory),
+// range-checked against the vocabulary.  An id outside [0, V) would index
+// past wte / dwte in the embedding, head and loss kernels: it is replaced by
+// 0 and counted in *bad, which the executor checks after the run.
+__global__ void copy_tokens_kernel(int32_t* __restrict__ dst, const int32_t* __restrict__ src, long long n, int V,
+                                   int* __restrict__ bad) {
+  int nbad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    int32_t t = src[i];
+    if (t < 0 || t >= V) {
+      t = 0;
+      ++nbad;
+    }
+    dst[i] = t;
+  }
+  if (nbad) atomicAdd(bad, nbad);
+}
+cudaError_t copy_tokens(int32_t* dst, const int32_t* src, long long n, int vocab, int* bad, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  copy_tokens_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, src, n, vocab, bad);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t embed_fwd(DType dt, const void* wte, const void* wpe, const int32_t* tok, void* x0, int b, int s,
                       int h, cudaStream_t st) {
   GS_DISPATCH(dt, embed_fwd_kernel<T><<<b * s, 256, 0, st>>>((const T*)wte, (const T*)wpe, tok, (T*)x0, s, h));

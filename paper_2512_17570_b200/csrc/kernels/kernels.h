@@ -77,6 +77,9 @@ cudaError_t fill_zero(void* p, size_t bytes, cudaStream_t s);
 // dst[i] = src[i] by SM threads (src may be mapped pinned host memory): a
 // small copy that does not queue behind bulk DMA on the copy engines.
 cudaError_t copy_words(uint32_t* dst, const uint32_t* src, long long n, cudaStream_t s);
+// dst[i] = src[i] for token ids, with ids outside [0, vocab) replaced by 0
+// and counted into *bad (device int).
+cudaError_t copy_tokens(int32_t* dst, const int32_t* src, long long n, int vocab, int* bad, cudaStream_t s);
 
 // ----------------------------------------------------- embedding / head
 // x0[bi*s+t] = wte[tok[bi*(s+1)+t]] + wpe[t]   (tokens laid out [b][s+1])
