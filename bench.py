@@ -9,10 +9,15 @@ optimizer state, NVMe I/O when the split puts data on SSD).
 Workload (BASELINE.json configs[1], as written): GPT-1.3B (N=24, h=2048, 16
 heads, s=2048, b=2, vocab 50304), M=16 micro-batches per iteration, split
 (1,1,1): params, checkpoints and the fp32 optimizer state (master, m, v) live
-in pinned host DRAM; every optimizer step streams its state slice through
-HBM (opt_tier 2) and the updated bf16 params back; alpha=0.2, bf16.  The
-optimizer-state streaming (24 B/element) is outside the reference's ledger
-and is counted in e2e's PCIe bytes and in the iteration roofline.  GPT-65B,
+in pinned host DRAM, and the plan's CpuStep runs where the state lives — on
+the host cores (opt_tier 3, the reference's resource model,
+proj/src/simulator.cpp:24-43): the GradAccum D2H lands the fp32 gradient in
+DRAM, the AVX2 Adam writes the bf16 params straight into their host copy;
+alpha=0.2, bf16.  The iteration roofline adds the host-DRAM term (30 B per
+stepped element over the measured host copy bandwidth).  Variants:
+`gpt1.3b-stream-opt` (state streamed through HBM and stepped by the fused
+GPU kernel, 26 B/element of extra PCIe, counted in e2e and the roofline) and
+`gpt1.3b-hbm-opt` (state resident in HBM).  GPT-65B,
 the metric's headline model, does not fit this box (196 GB DRAM / 80 GB
 disk); `--config gpt65b-8layer` runs its layer geometry on an 8-layer slice
 with the optimizer state split between pinned DRAM and the NVMe file.
@@ -51,14 +56,17 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 # one metric string for both arms (the driver computes the ours/reference ratio)
 METRIC = "tokens/sec (GPT-1.3B training, vertical schedule + alpha-delayed optimizer step, BASELINE configs[1])"
 
-OPT_TIERS = {0: "auto", 1: "HBM", 2: "pinned host DRAM, streamed through HBM per step"}
+OPT_TIERS = {0: "auto", 1: "HBM", 2: "pinned host DRAM, streamed through HBM per step",
+             3: "pinned host DRAM, stepped by the host cores (the reference's CpuStep)"}
 
 CONFIGS = {
     # name: (N, h, heads, s, b, vocab, M, split, alpha, opt_tier, ssd_ring_layers)
     # BASELINE configs[1] as written: everything CPU-resident in pinned DRAM
-    "gpt1.3b": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2, 2, 8),
+    "gpt1.3b": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2, 3, 8),
     # the same with the CPU-resident optimizer fraction held in HBM instead
     "gpt1.3b-hbm-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2, 1, 8),
+    "gpt1.3b-stream-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2, 2, 8),
+    "gpt1.3b-host-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2, 3, 8),
     "gpt1.3b-ssd-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 0.0), 0.2, 2, 8),
     # BASELINE configs[2] shape on this box (196 GB DRAM, 80 GB disk): half of
     # the optimizer state (75.5 GB) on the NVMe tier, the other half in DRAM
@@ -440,7 +448,15 @@ def run_ours(args):
         gs.check(gs.lib().gs_nvme_probe(os.environ.get("GS_NVME_DIR", "/tmp").encode(), C.c_uint64(4 << 30), out))
         nvme = {"write_gbs": out[0], "read_gbs": out[1], "concurrent_gbs_per_direction": out[2]}
         t_ssd = max(float(led[2].sum()), float(led[3].sum())) / (out[2] * 1e9)
-    t_roof = max(t_comp, t_h2d, t_d2h, t_ssd)
+    # host DRAM (OPT_HOST): the CpuStep bytes of the iteration — every layer's
+    # P elements at 30 B (12 state in + 4 grad in + 12 state out + 2 bf16
+    # param out) — over the measured multi-threaded host copy bandwidth
+    t_host, host = 0.0, None
+    if tier == 3:
+        host = gs.host_probe()
+        host["bytes_per_iteration"] = 30 * N * 12 * h * h // world
+        t_host = host["bytes_per_iteration"] / (host["copy_gbs"] * 1e9)
+    t_roof = max(t_comp, t_h2d, t_d2h, t_ssd, t_host)
     # the paper's narrower line-through-origin bound (roofline.cpp:8-22): only
     # the SSD-resident optimizer state's round trip, at the measured NVMe rate
     io_roof = None
@@ -470,6 +486,7 @@ def run_ours(args):
             "iteration_roofline": {"t_roof_ms": t_roof * 1e3, "t_measured_ms": ms_step, "frac": t_roof / (ms_step / 1e3),
                                    "t_compute_ms": t_comp * 1e3, "t_pcie_h2d_ms": t_h2d * 1e3,
                                    "t_pcie_d2h_ms": t_d2h * 1e3, "t_ssd_ms": t_ssd * 1e3, "nvme": nvme,
+                                   "t_host_dram_ms": t_host * 1e3, "host_dram": host,
                                    "pcie_bytes": "ledger + extension (optimizer-state streaming) per direction",
                                    "pcie_h2d_gbs": bw["h2d"] / 1e9,
                                    "pcie_d2h_gbs": bw["d2h"] / 1e9, "flops_per_iteration": flops_iter,

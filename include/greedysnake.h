@@ -133,13 +133,14 @@ typedef struct gs_engine_config {
   int device;
   const char* nvme_dir;    /* directory for the NVMe tier file (NULL -> "/tmp") */
   int odirect;             /* 1: O_DIRECT on the NVMe tier */
-  int opt_tier;            /* 0 auto, 1 HBM, 2 pinned host */
+  int opt_tier;            /* 0 auto, 1 HBM, 2 pinned DRAM streamed through HBM, 3 pinned DRAM stepped by host cores */
   int record_trace;
   int profile_kernels;     /* CUDA-event timing per kernel class (gs_engine_kernel_profile) */
   int rank, world;         /* ZeRO-3 data parallelism: model.data_parallel_degree == world */
   const uint8_t* nccl_id;  /* 128-byte ncclUniqueId from gs_nccl_unique_id() on rank 0 (world > 1) */
   int force_collectives;   /* run the sharded / NCCL path even at world == 1 */
   int ssd_ring_layers;     /* pinned staging slots per SSD-resident data kind (0 -> 8) */
+  int host_threads;        /* opt_tier 3: host optimizer threads (0 -> hardware threads - 4) */
 } gs_engine_config;
 
 /* ncclGetUniqueId() for rank 0 of a data-parallel job */
@@ -159,6 +160,7 @@ typedef struct gs_trace_record {
   int iteration, task, resource;
   double t_start_ms, t_end_ms;
   uint64_t bytes, physical_bytes;
+  double t_host_ms;  /* host time the dispatcher began enqueueing the task (its dependencies dispatched) */
 } gs_trace_record;
 
 typedef struct gs_engine gs_engine; /* opaque offsim::Executor */
@@ -234,6 +236,11 @@ int gs_layer_bench(int dtype, int b, int s, int h, int heads, int iters, double 
  * (`bytes` moved per direction): out = {write GB/s, read GB/s, per-direction
  * GB/s with reads and writes concurrent} */
 int gs_nvme_probe(const char* dir, uint64_t bytes, double out[3]);
+/* diagnostics: host DRAM as the host-core optimizer step sees it, on
+ * `threads` workers (0 -> hardware threads - 4) over `elements` fp32 Adam
+ * elements of pinned memory: out = {copy GB/s (read + write bytes), host
+ * Adam Gelem/s (bf16 output, 30 B/element), threads used} */
+int gs_host_probe(int threads, uint64_t elements, double out[3]);
 /* number of device kernels launched through this library so far */
 int64_t gs_launch_count(void);
 

@@ -9,8 +9,9 @@
 //   GPU    FwdCompute / RecomputeAndBwd / FixedOps -> compute CUDA stream
 //   H2D    Xfer PCIe_H2D                           -> copy stream (pinned DRAM -> HBM)
 //   D2H    Xfer PCIe_D2H                           -> copy stream (HBM -> pinned DRAM)
-//   CPU    CpuStep                                 -> optimizer stream: fused Adam on
-//                                                     the GPU, state streamed through HBM
+//   CPU    CpuStep                                 -> host cores (OptTier::Host), or the
+//                                                     optimizer stream: fused Adam on the GPU,
+//                                                     state in HBM or streamed through it
 //   SSD_R  Xfer SSD_Read                           -> NVMe file reads (O_DIRECT, thread pool)
 //   SSD_W  Xfer SSD_Write                          -> NVMe file writes
 //
@@ -31,10 +32,15 @@
 
 namespace offsim {
 
+// Where the plan's CPU-resident optimizer fraction (split.x_opt) lives and
+// which processor runs CpuStep on it.  SSD-resident bytes always round-trip
+// through the NVMe file and a pinned staging slot.
 enum class OptTier {
-  Auto = 0,  // CPU-resident optimizer fraction in HBM when it fits, else pinned DRAM
-  Hbm = 1,   // CPU-resident fraction kept in HBM (B200: 180 GB)
-  Host = 2,  // CPU-resident fraction in pinned DRAM, streamed through HBM per step
+  Auto = 0,    // HBM when it fits (< 60% of free HBM), else Stream
+  Hbm = 1,     // kept in HBM (B200: 180 GB); fused Adam kernel in place
+  Stream = 2,  // pinned DRAM, streamed through HBM per step (upload -> fused Adam -> download pipeline)
+  Host = 3,    // pinned DRAM, stepped by the host cores where it lives: the reference's CpuStep
+               // (simulator.cpp:24-43), gradients from the plan's GradAccum D2H, no extra PCIe bytes
 };
 
 struct AdamConfig {
@@ -61,6 +67,7 @@ struct ExecConfig {
   // them through a ring of this many per-layer pinned slots (slot = layer %
   // ring); reuse of a slot is ordered by the executor's hazard edges.
   int ssd_ring_layers = 8;
+  int host_threads = 0;  // OptTier::Host worker threads (0: hardware threads - 4, at least 1)
 };
 
 struct TraceRecord {
@@ -70,6 +77,7 @@ struct TraceRecord {
   double t_start_ms, t_end_ms;  // relative to the run start (GPU tasks: CUDA events)
   u64 bytes;                    // logical bytes (the plan's)
   u64 physical_bytes;           // bytes actually moved (NVMe rounds to 4 KiB)
+  double t_host_ms = 0.0;       // host time the dispatcher began enqueueing it (dependencies dispatched)
 };
 
 struct ExecReport {

@@ -25,6 +25,9 @@ LINKS = ("H2D", "D2H", "SSD_read", "SSD_write")
 DATA = ("param", "ckpt", "grad_accum", "interlayer_grad", "opt_state")
 TASK_KINDS = ("fwd", "bwd", "cpu_step", "xfer", "fixed_ops")
 RESOURCES = ("compute", "cpu_step", "pcie_h2d", "pcie_d2h", "ssd_read", "ssd_write")
+# Engine(opt_tier=...): where the CPU-resident optimizer fraction lives and
+# what steps it (include/offsim/executor.hpp OptTier)
+OPT_AUTO, OPT_HBM, OPT_STREAM, OPT_HOST = 0, 1, 2, 3
 
 OK, ERR_PLAN_BUG, ERR_VALIDATION, ERR_INFEASIBLE, ERR_CUDA, ERR_RUNTIME = range(6)
 
@@ -87,7 +90,8 @@ class _EngineConfig(C.Structure):
                 ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float), ("seed", C.c_uint64),
                 ("device", C.c_int), ("nvme_dir", C.c_char_p), ("odirect", C.c_int), ("opt_tier", C.c_int),
                 ("record_trace", C.c_int), ("profile_kernels", C.c_int), ("rank", C.c_int), ("world", C.c_int),
-                ("nccl_id", C.c_void_p), ("force_collectives", C.c_int), ("ssd_ring_layers", C.c_int)]
+                ("nccl_id", C.c_void_p), ("force_collectives", C.c_int), ("ssd_ring_layers", C.c_int),
+                ("host_threads", C.c_int)]
 
 
 class _RunReport(C.Structure):
@@ -98,7 +102,8 @@ class _RunReport(C.Structure):
 
 class _TraceRecord(C.Structure):
     _fields_ = [("iteration", C.c_int), ("task", C.c_int), ("resource", C.c_int), ("t_start_ms", C.c_double),
-                ("t_end_ms", C.c_double), ("bytes", C.c_uint64), ("physical_bytes", C.c_uint64)]
+                ("t_end_ms", C.c_double), ("bytes", C.c_uint64), ("physical_bytes", C.c_uint64),
+                ("t_host_ms", C.c_double)]
 
 
 # ------------------------------------------------------------------ loading
@@ -470,7 +475,8 @@ class Engine:
     def __init__(self, plan: SchedulePlan, model: ModelSpec, vocab_size: int, adam: AdamConfig = AdamConfig(),
                  seed: int = 42, device: int = 0, nvme_dir: str = "/tmp", odirect: bool = True, opt_tier: int = 0,
                  record_trace: bool = False, profile: bool = False, rank: int = 0, world: int = 1,
-                 nccl_id: bytes | None = None, force_collectives: bool = False, ssd_ring_layers: int = 0):
+                 nccl_id: bytes | None = None, force_collectives: bool = False, ssd_ring_layers: int = 0,
+                 host_threads: int = 0):
         self.model = model
         self.vocab_size = vocab_size
         self.plan = plan
@@ -480,7 +486,7 @@ class Engine:
         cfg = _EngineConfig(model._c(), vocab_size, adam.lr, adam.beta1, adam.beta2, adam.eps, adam.weight_decay,
                             seed, device, self._nvme, int(odirect), opt_tier, int(record_trace), int(profile),
                             rank, world, C.cast(self._id, C.c_void_p) if self._id is not None else None,
-                            int(force_collectives), int(ssd_ring_layers))
+                            int(force_collectives), int(ssd_ring_layers), int(host_threads))
         h = C.c_void_p()
         check(lib().gs_engine_create(plan.handle, C.byref(cfg), C.byref(h)))
         self._h = h
@@ -523,7 +529,8 @@ class Engine:
             arr = (_TraceRecord * n.value)()
             check(lib().gs_engine_trace(self._h, arr, n.value, C.byref(n)))
             trace = [dict(iteration=r.iteration, task=r.task, resource=RESOURCES[r.resource], t_start_ms=r.t_start_ms,
-                          t_end_ms=r.t_end_ms, bytes=r.bytes, physical_bytes=r.physical_bytes) for r in arr]
+                          t_end_ms=r.t_end_ms, bytes=r.bytes, physical_bytes=r.physical_bytes,
+                          t_host_ms=r.t_host_ms) for r in arr]
         return RunReport(rep.total_ms, rep.iterations, rep.gpu_launches, list(losses), _ledger(rep.ledger),
                          _ledger(rep.extension), _ledger(rep.physical), rep.gpu_bytes, rep.host_pinned_bytes, trace)
 
@@ -564,3 +571,12 @@ class Engine:
         m, v = np.empty(n, np.float32), np.empty(n, np.float32)
         check(lib().gs_engine_read_fixed_moments(self._h, m.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p)))
         return m, v
+
+
+def host_probe(threads: int = 0, elements: int = 1 << 26) -> dict:
+    """Host DRAM as the host-core optimizer step (OPT_HOST) sees it
+    (gs_host_probe): multi-threaded copy GB/s (read + write bytes) and the
+    host Adam's own rate on pinned memory."""
+    out = (C.c_double * 3)()
+    check(lib().gs_host_probe(int(threads), C.c_uint64(elements), out))
+    return {"copy_gbs": out[0], "adam_gelem_s": out[1], "threads": int(out[2])}

@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <chrono>
+#include <functional>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -15,6 +17,7 @@
 #include <vector>
 
 #include "greedysnake.h"
+#include "host_adam.hpp"
 #include "host_tiers.hpp"
 #include "kernels.h"
 #include "layer_ops.hpp"
@@ -294,6 +297,8 @@ int gs_engine_create(const gs_plan* plan, const gs_engine_config* c, gs_engine**
     if (c->nccl_id) cfg.nccl_id.assign(c->nccl_id, c->nccl_id + 128);
     cfg.force_collectives = c->force_collectives != 0;
     if (c->ssd_ring_layers > 0) cfg.ssd_ring_layers = c->ssd_ring_layers;
+    if (c->host_threads > 0) cfg.host_threads = c->host_threads;
+    if (c->opt_tier < 0 || c->opt_tier > 3) throw offsim::ValidationError("engine: opt_tier must be 0..3");
     auto e = std::make_unique<gs_engine>();
     e->ex = std::make_unique<offsim::Executor>(plan->plan, cfg);
     *out = e.release();
@@ -357,7 +362,8 @@ int gs_engine_trace(gs_engine* engine, gs_trace_record* out, int cap, int* n) {
     *n = static_cast<int>(engine->trace.size());
     for (int i = 0; i < cap && i < *n; ++i) {
       const offsim::TraceRecord& r = engine->trace[static_cast<size_t>(i)];
-      out[i] = {r.iteration, r.task, static_cast<int>(r.resource), r.t_start_ms, r.t_end_ms, r.bytes, r.physical_bytes};
+      out[i] = {r.iteration, r.task, static_cast<int>(r.resource), r.t_start_ms, r.t_end_ms, r.bytes, r.physical_bytes,
+                r.t_host_ms};
     }
   });
 }
@@ -476,6 +482,47 @@ int gs_layer_backward(int dtype, int b, int s, int h, int heads, const void* W, 
   return layer_call(dtype, b, s, h, heads, false, W, x, dy, dx, dW, first, stream);
 }
 int64_t gs_launch_count(void) { return gs::launch_counter_ref(); }
+
+int gs_host_probe(int threads, uint64_t elements, double out[3]) {
+  return guarded([&] {
+    if (!out || elements < (1u << 20)) throw offsim::ValidationError("host_probe: elements >= 2^20 and out required");
+    const int hw = static_cast<int>(std::thread::hardware_concurrency());
+    const int nt = threads > 0 ? threads : std::max(1, hw - 4);
+    gs::engine::ThreadPool pool(nt);
+    gs::engine::PinnedArena arena;
+    float* state = reinterpret_cast<float*>(arena.alloc(12 * elements));
+    float* grad = reinterpret_cast<float*>(arena.alloc(4 * elements));
+    uint16_t* lp = reinterpret_cast<uint16_t*>(arena.alloc(2 * elements));
+    for (uint64_t i = 0; i < elements; ++i) {
+      state[3 * i] = 0.01f * static_cast<float>(i % 97);
+      grad[i] = 1e-3f * static_cast<float>(i % 13) - 6e-3f;
+    }
+    using clk = std::chrono::steady_clock;
+    auto secs = [](clk::time_point t0) { return std::chrono::duration<double>(clk::now() - t0).count(); };
+    // copy: state -> (grad | lp | spare state tail) pattern-free, 12 B/elem each way
+    uint8_t* src = reinterpret_cast<uint8_t*>(state);
+    uint8_t* dst = arena.alloc(12 * elements);
+    double best_copy = 0.0, best_adam = 0.0;
+    for (int rep = 0; rep < 3; ++rep) {
+      std::vector<std::function<void()>> jobs;
+      const uint64_t n = 12 * elements, per = (n / (4 * nt) + 4095) / 4096 * 4096;
+      for (uint64_t lo = 0; lo < n; lo += per) {
+        const uint64_t hi = std::min(n, lo + per);
+        jobs.emplace_back([=] { std::memcpy(dst + lo, src + lo, hi - lo); });
+      }
+      auto t0 = clk::now();
+      pool.run_all(jobs);
+      best_copy = std::max(best_copy, 2.0 * n / secs(t0) / 1e9);
+      const gs::engine::HostAdamHyper hp{1e-4f, 0.9f, 0.95f, 1e-8f, 0.0f};
+      t0 = clk::now();
+      gs::engine::host_adam_step(hp, rep + 1, state, grad, lp, 2, elements, pool);
+      best_adam = std::max(best_adam, elements / secs(t0) / 1e9);
+    }
+    out[0] = best_copy;
+    out[1] = best_adam;
+    out[2] = nt;
+  });
+}
 
 int gs_nvme_probe(const char* dir, uint64_t bytes, double out[3]) {
   return guarded([&] {

@@ -41,6 +41,7 @@
 #include <sstream>
 #include <thread>
 
+#include "host_adam.hpp"
 #include "host_tiers.hpp"
 #include "kernels.h"
 #include "layer_ops.hpp"
@@ -167,8 +168,23 @@ struct Executor::Impl {
   double* dev_loss = nullptr;  // [loss_cap] per run iteration
   int* dev_bad_tokens = nullptr;  // count of out-of-vocabulary token ids seen by the run
   int loss_cap = 0;
-  float* opt_stage = nullptr;  // 12 * chunk floats
-  void* lp_stage = nullptr;    // chunk lp elements
+  // Optimizer-state streaming (state not resident in HBM): a ring of
+  // staging slots, each one chunk of [master, m, v] (12 B/element) plus its
+  // low-precision output.  Chunk c's upload (s_opt_up), fused Adam (s_opt)
+  // and download (s_opt_dn) run as a three-stage pipeline, so the H2D and
+  // D2H directions and the kernel overlap each other and the plan's own
+  // transfers on s_h2d / s_d2h.
+  static constexpr int kOptRing = 4;
+  struct OptSlot {
+    float* state = nullptr;
+    void* lp = nullptr;
+    cudaEvent_t up = nullptr, comp = nullptr, free_ = nullptr;
+    bool used = false;
+  };
+  std::array<OptSlot, kOptRing> oring;
+  int oring_next = 0;
+  cudaStream_t s_opt_up = nullptr, s_opt_dn = nullptr;
+  cudaEvent_t ev_opt_begin = nullptr, ev_opt_end = nullptr;
   long long chunk = 0;
 
   // host state
@@ -181,6 +197,13 @@ struct Executor::Impl {
   std::vector<Blob> ckpt_blob;             // [N*M]
   std::vector<uint8_t*> host_grad;         // [host_grad_ring], slot = layer % ring
   int host_grad_ring = 1;
+  // OptTier::Host: CpuStep runs on the host cores (the reference's resource
+  // model).  The GradAccum D2H lands the immediate slice of the layer's
+  // gradient in host_grad (ring) and the alpha-delayed slice in
+  // host_retain[layer], which the next iteration's forward-phase step reads.
+  bool host_step = false;
+  std::vector<float*> host_retain;  // [N] loc_late floats
+  std::unique_ptr<ThreadPool> host_pool;
   std::vector<uint8_t*> host_ilg;          // [2*M]
   int32_t* tok_pinned = nullptr;
   long long tok_capacity = 0;
@@ -252,6 +275,10 @@ struct Executor::Impl {
   bool delayed(const Task& t) const { return fwd_phase[static_cast<size_t>(t.id)] != 0; }
   // src: where SSD-resident state is read from — the NVMe read staging for
   // plan steps (a plan SSD read precedes each), the image for flush().
+  // OptTier::Host: the same step on the host cores, in place on the state's
+  // pinned images (DRAM segments, or the NVMe staging slot the plan's
+  // OptState SSD read filled); grad is a host pointer.
+  void apply_adam_host(int layer, u64 e0, u64 e1, const float* grad, int step);
   void apply_adam(int layer, u64 e0, u64 e1, const float* grad, int step, cudaStream_t st, int it,
                   Src src = Src::ReadStaging);
   void note_ledger(int it, const Task& t, u64 phys);
@@ -346,14 +373,23 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   cuda_check(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking), "stream");
   cuda_check(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking), "stream");
   cuda_check(cudaStreamCreateWithPriority(&s_opt, cudaStreamNonBlocking, prio_lo), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&s_opt_up, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&s_opt_dn, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaEventCreateWithFlags(&ev_opt_begin, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreateWithFlags(&ev_opt_end, cudaEventDisableTiming), "event");
 
   // ---- optimizer tier placement
   const u64 opt_bytes = 12 * Ps;  // this rank's shard of the layer's [master, m, v]
   const u64 cpu_opt = cpu_portion(opt_bytes, plan.split.x_opt);
+  if (static_cast<int>(cfg.opt_tier) < 0 || static_cast<int>(cfg.opt_tier) > 3)
+    throw ValidationError("executor: opt_tier must be 0 (auto), 1 (HBM), 2 (stream) or 3 (host)");
   bool opt_hbm = cfg.opt_tier == OptTier::Hbm;
+  host_step = cfg.opt_tier == OptTier::Host;
+  if (host_step && horizontal)
+    throw ValidationError("executor: the host-core optimizer tier covers the vertical schedule");
+  size_t free_b = 0, total_b = 0;
+  cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
   if (cfg.opt_tier == OptTier::Auto) {
-    size_t free_b = 0, total_b = 0;
-    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
     // leave room for params, grads, activations and staging: 3/4 of free HBM
     opt_hbm = static_cast<double>(cpu_opt) * N < 0.6 * static_cast<double>(free_b);
   }
@@ -361,14 +397,26 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   // ---- device buffers
   const u64 lpb = static_cast<u64>(d.lp());
   for (int i = 0; i < 2; ++i) dev_param[i] = dmalloc(lpb * Ps * static_cast<u64>(W));  // gathered layer
-  grad_ring = horizontal ? 2 : 3;
+  // Gradient ring (vertical): layer l accumulates into slot l % grad_ring,
+  // which the immediate optimizer step of layer l + grad_ring (plan stage
+  // +2 after its backward) must have consumed first — a WAR edge of the
+  // hazard pass.  Three slots leave that step one stage of slack; when the
+  // step streams its state over PCIe it needs more, so the ring takes up to
+  // 8 slots within 10% of free HBM.
+  if (horizontal) {
+    grad_ring = 2;
+  } else {
+    const double slot = 4.0 * static_cast<double>(Ps) * W;
+    grad_ring = static_cast<int>(std::clamp(0.10 * static_cast<double>(free_b) / slot, 3.0, 8.0));
+    grad_ring = std::min(grad_ring, std::max(3, N));
+  }
   for (int i = 0; i < grad_ring; ++i) {
     grad_slot.push_back(static_cast<float*>(dmalloc(4 * Ps * static_cast<u64>(W))));
     cuda_check(cudaMemset(grad_slot.back(), 0, 4 * Ps * static_cast<u64>(W)), "memset");  // shard padding
     grad_shard.push_back(dp ? static_cast<float*>(dmalloc(4 * Ps)) : grad_slot.back());
   }
   retain.assign(static_cast<size_t>(N), nullptr);
-  if (loc_late > 0)
+  if (loc_late > 0 && !host_step)
     for (int l = 0; l < N; ++l) retain[static_cast<size_t>(l)] = static_cast<float*>(dmalloc(4 * loc_late));
   n_fixed = static_cast<long long>(d.V + d.s) * d.h;
   fx_master = static_cast<float*>(dmalloc(4 * n_fixed));
@@ -389,10 +437,15 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   for (int i = 0; i < 2; ++i) dev_tok[i] = static_cast<int32_t*>(dmalloc(tok_bytes));
   dev_bad_tokens = static_cast<int*>(dmalloc(sizeof(int)));
   cuda_check(cudaMemset(dev_bad_tokens, 0, sizeof(int)), "memset");
-  chunk = static_cast<long long>(std::min<u64>(P, 32ull << 20));
+  // 2 Mi elements per chunk: 24 MB of state (~0.5 ms of PCIe per direction)
+  chunk = static_cast<long long>(std::min<u64>(P, 2ull << 20));
   chunk = (chunk + 3) / 4 * 4;
-  opt_stage = static_cast<float*>(dmalloc(12ull * chunk));
-  lp_stage = dmalloc(static_cast<u64>(chunk) * d.lp());
+  for (OptSlot& o : oring) {
+    o.state = static_cast<float*>(dmalloc(12ull * chunk));
+    o.lp = dmalloc(static_cast<u64>(chunk) * d.lp());
+    for (cudaEvent_t* e : {&o.up, &o.comp, &o.free_})
+      cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+  }
   cuda_check(cudaMemset(fx_m, 0, 4 * n_fixed), "memset");
   cuda_check(cudaMemset(fx_v, 0, 4 * n_fixed), "memset");
   cuda_check(cudaMemset(fx_grad, 0, 4 * n_fixed), "memset");
@@ -415,8 +468,18 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   // in the vertical schedule the optimizer consumes the gradient in HBM and
   // the plan's D2H (schedule.cpp:489-494) only has to land somewhere: a
   // two-slot ring (N x 4P of pinned DRAM would be 258 GB at GPT-65B).
-  host_grad_ring = horizontal ? N : std::min(N, 2);
+  // With the host-core step the landing slot is read by CpuStep (plan stage
+  // +1 after the D2H): six slots keep the in-order D2H queue from waiting on
+  // a step still reading the slot it wants to overwrite.
+  host_grad_ring = horizontal ? N : std::min(N, host_step ? 6 : 2);
   for (int i = 0; i < host_grad_ring; ++i) host_grad.push_back(arena.alloc(4 * Ps));
+  if (host_step) {
+    host_retain.assign(static_cast<size_t>(N), nullptr);
+    if (loc_late > 0)
+      for (int l = 0; l < N; ++l) host_retain[static_cast<size_t>(l)] = reinterpret_cast<float*>(arena.alloc(4 * loc_late));
+    const int hw = static_cast<int>(std::thread::hardware_concurrency());
+    host_pool = std::make_unique<ThreadPool>(cfg.host_threads > 0 ? cfg.host_threads : std::max(1, hw - 4), 10);
+  }
   for (int l = 0; l < N; ++l)
     for (int m = 0; m < M; ++m)
       ckpt_blob.push_back(
@@ -453,10 +516,15 @@ Executor::Impl::~Impl() {
     for (cudaEvent_t e : a)
       if (e) cudaEventDestroy(e);
   if (ev_base) cudaEventDestroy(ev_base);
+  for (OptSlot& o : oring)
+    for (cudaEvent_t e : {o.up, o.comp, o.free_})
+      if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {ev_opt_begin, ev_opt_end})
+    if (e) cudaEventDestroy(e);
   free_workspace(ws);
   if (comm) ncclCommDestroy(comm);
   for (void* p : dev_allocs) cudaFree(p);
-  for (cudaStream_t s : {s_gpu, s_h2d, s_d2h, s_opt})
+  for (cudaStream_t s : {s_gpu, s_h2d, s_d2h, s_opt, s_opt_up, s_opt_dn})
     if (s) cudaStreamDestroy(s);
 }
 
@@ -604,7 +672,8 @@ void Executor::Impl::build_tasks() {
     const Resource r = task_resource(t, true);
     res_of[i] = r;
     queue[static_cast<size_t>(r)].push_back(static_cast<int>(i));
-    is_stream[i] = (r == Resource::GPU || r == Resource::CPU || r == Resource::H2D || r == Resource::D2H) ? 1 : 0;
+    is_stream[i] = (r == Resource::GPU || (r == Resource::CPU && !host_step) || r == Resource::H2D ||
+                    r == Resource::D2H) ? 1 : 0;
     done_iter[i].store(-1);
     for (auto& e : ev_done[i]) {
       e = nullptr;
@@ -629,7 +698,7 @@ void Executor::Impl::build_tasks() {
 namespace {
 enum SlotKind {
   kDevParam, kInX, kOutY, kInG, kOutG, kGrad, kRetain, kHostIlg, kParamImg, kParamRd, kOptImg, kOptRd, kCkptImg,
-  kCkptRd, kHostGrad, kOptDev, kParamFile, kOptFile, kCkptFile,
+  kCkptRd, kHostGrad, kOptDev, kParamFile, kOptFile, kCkptFile, kHostRetain,
   kParamStage, kOptStage, kCkptStage  // SSD staging-ring slots (layer % ring)
 };
 struct Access {
@@ -690,7 +759,8 @@ void Executor::Impl::hazards() {
         if (m == last_mb(st) && el_late > 0) W(slot_id(kRetain, l));
         break;
       case TaskKind::CpuStep:
-        R(late ? slot_id(kRetain, l) : slot_id(kGrad, l % grad_ring));
+        if (host_step) R(late ? slot_id(kHostRetain, l) : slot_id(kHostGrad, l % host_grad_ring));
+        else R(late ? slot_id(kRetain, l) : slot_id(kGrad, l % grad_ring));
         R(slot_id(kOptRd, l, imm_late));
         R(slot_id(kOptImg, l, imm_late));
         W(slot_id(kOptImg, l, imm_late));
@@ -775,6 +845,7 @@ void Executor::Impl::hazards() {
             if (t.link == LinkKind::PCIe_D2H) {
               R(slot_id(kGrad, l % grad_ring));
               W(slot_id(kHostGrad, l % host_grad_ring));
+              if (host_step && loc_late > 0) W(slot_id(kHostRetain, l));
             } else {  // horizontal accumulation fetch
               R(slot_id(kHostGrad, l % host_grad_ring));
               W(slot_id(kGrad, l % grad_ring));
@@ -976,7 +1047,8 @@ void Executor::Impl::run_task(int id, int it) {
   }
   if (t.kind == TaskKind::Xfer) note_ledger(it, t, phys);
   if (cfg.record_trace) {
-    TraceRecord rec{it, id, r, 0.0, 0.0, t.bytes, phys};
+    TraceRecord rec{it, id, r, 0.0, 0.0, t.bytes, phys,
+                    std::chrono::duration<double, std::milli>(h0 - host_base).count()};
     if (!stream) {
       rec.t_start_ms = std::chrono::duration<double, std::milli>(h0 - host_base).count();
       rec.t_end_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_base).count();
@@ -1106,7 +1178,7 @@ void Executor::Impl::compute_task(const Task& t, int it) {
     lc.n += 1;
   }
   if (!horizontal && m == last_mb(st) && el_late > 0) {
-    if (loc_late > 0)
+    if (loc_late > 0 && !host_step)
       cuda_check(cudaMemcpyAsync(retain[static_cast<size_t>(l)], grad_shard[static_cast<size_t>(l % grad_ring)] + loc_now,
                                  4 * loc_late, cudaMemcpyDeviceToDevice, s_gpu),
                  "retain");
@@ -1115,36 +1187,108 @@ void Executor::Impl::compute_task(const Task& t, int it) {
   launches += lc.n;
 }
 
-// Fused Adam over elements [e0,e1) of layer l: optimizer state gathered from
-// its tiers into HBM (in place when a single HBM segment holds the range),
-// updated, scattered back; the low-precision params go to the host image.
+// Fused Adam over elements [e0,e1) of layer l on stream st.  State held in
+// HBM is updated in place; otherwise each chunk is staged through the slot
+// ring: upload (s_opt_up) -> adam_step_packed (st) -> download of the state
+// and of the low-precision params to their host images (s_opt_dn), slot
+// reuse ordered by the slot's `free_` event.  st joins the last download
+// before returning, so an event recorded on st after this call covers all
+// of the step's traffic.
 void Executor::Impl::apply_adam(int layer, u64 e0, u64 e1, const float* grad, int step, cudaStream_t st, int it,
                                 Src src) {
   gs::AdamHyper hp{cfg.adam.lr, cfg.adam.beta1, cfg.adam.beta2, cfg.adam.eps, cfg.adam.weight_decay};
   Blob& ob = opt_blob[static_cast<size_t>(layer)];
   Blob& pbb = param_blob[static_cast<size_t>(layer)];
   const u64 lp = static_cast<u64>(d.lp());
+  // the uploads must follow everything already ordered on st (the task's
+  // dependencies were enqueued there as stream waits)
+  cuda_check(cudaEventRecord(ev_opt_begin, st), "record");
+  cuda_check(cudaStreamWaitEvent(s_opt_up, ev_opt_begin, 0), "wait");
   for (u64 c0 = e0; c0 < e1; c0 += static_cast<u64>(chunk)) {
     const u64 c1 = std::min(e1, c0 + static_cast<u64>(chunk));
     const u64 lo = 12 * c0, hi = 12 * c1;
+    OptSlot& slot = oring[static_cast<size_t>(oring_next)];
+    oring_next = (oring_next + 1) % kOptRing;
     float* state = nullptr;
     for (Segment& s : ob.segs)
       if (s.tier == Tier::Hbm && s.lo <= lo && hi <= s.hi) state = reinterpret_cast<float*>(s.dev + (lo - s.lo));
     const bool in_place = state != nullptr && (reinterpret_cast<uintptr_t>(state) & 15) == 0;
     u64 up = 0, down = 0;
     if (!in_place) {
-      state = opt_stage;
-      up = upload(ob, lo, hi, state, src, st, ~0ull);
+      if (slot.used) cuda_check(cudaStreamWaitEvent(s_opt_up, slot.free_, 0), "wait");
+      state = slot.state;
+      up = upload(ob, lo, hi, state, src, s_opt_up, ~0ull);
+      cuda_check(cudaEventRecord(slot.up, s_opt_up), "record");
+      cuda_check(cudaStreamWaitEvent(st, slot.up, 0), "wait");
+    } else if (slot.used) {
+      cuda_check(cudaStreamWaitEvent(st, slot.free_, 0), "wait");  // slot.lp reuse
     }
-    cuda_check(gs::adam_step_packed(hp, step, 1.0f, state, grad + (c0 - e0), lp_stage, d.dt,
+    cuda_check(gs::adam_step_packed(hp, step, 1.0f, state, grad + (c0 - e0), slot.lp, d.dt,
                                     static_cast<long long>(c1 - c0), st),
                "adam");
     launches += 1;
-    if (!in_place) down = download(ob, lo, hi, state, st);
-    const u64 pdown = download(pbb, lp * c0, lp * c1, lp_stage, st);
+    cuda_check(cudaEventRecord(slot.comp, st), "record");
+    cuda_check(cudaStreamWaitEvent(s_opt_dn, slot.comp, 0), "wait");
+    if (!in_place) down = download(ob, lo, hi, state, s_opt_dn);
+    const u64 pdown = download(pbb, lp * c0, lp * c1, slot.lp, s_opt_dn);
+    cuda_check(cudaEventRecord(slot.free_, s_opt_dn), "record");
+    slot.used = true;
     note_ext(it, LinkKind::PCIe_H2D, DataKind::OptState, up);
     note_ext(it, LinkKind::PCIe_D2H, DataKind::OptState, down);
     note_ext(it, LinkKind::PCIe_D2H, DataKind::Param, pdown);
+  }
+  cuda_check(cudaEventRecord(ev_opt_end, s_opt_dn), "record");
+  cuda_check(cudaStreamWaitEvent(st, ev_opt_end, 0), "wait");
+}
+
+void Executor::Impl::apply_adam_host(int layer, u64 e0, u64 e1, const float* grad, int step) {
+  const HostAdamHyper hp{cfg.adam.lr, cfg.adam.beta1, cfg.adam.beta2, cfg.adam.eps, cfg.adam.weight_decay};
+  Blob& ob = opt_blob[static_cast<size_t>(layer)];
+  Blob& pbb = param_blob[static_cast<size_t>(layer)];
+  const u64 lp = static_cast<u64>(d.lp());
+  // walk the element range by (opt segment x param segment) pieces: both
+  // blobs are cut at the same element boundaries (split rounding aside), so
+  // a piece is contiguous in the state image and in the param image
+  u64 e = e0;
+  while (e < e1) {
+    const Segment* so = nullptr;
+    for (const Segment& sg : ob.segs)
+      if (sg.lo <= 12 * e && 12 * e < sg.hi) so = &sg;
+    const Segment* sp = nullptr;
+    for (const Segment& sg : pbb.segs)
+      if (sg.lo <= lp * e && lp * e < sg.hi) sp = &sg;
+    if (!so || !sp) throw PlanBugError("executor: optimizer element outside its blobs");
+    if (so->tier == Tier::Hbm) throw PlanBugError("executor: host step over HBM-resident optimizer state");
+    // piece end: the nearer segment end (whole elements)
+    u64 end = std::min<u64>(e1, std::min<u64>(so->hi / 12, sp->hi / lp));
+    if (end <= e) {
+      // a segment boundary inside an element (byte-granular split rounding):
+      // step that element through a local copy
+      float st3[3];
+      uint8_t lpb[4];
+      for (int k = 0; k < 3; ++k) {
+        for (u64 b = 0; b < 4; ++b) {
+          const u64 off = 12 * e + 4 * static_cast<u64>(k) + b;
+          for (const Segment& sg : ob.segs)
+            if (sg.lo <= off && off < sg.hi) reinterpret_cast<uint8_t*>(st3)[4 * k + static_cast<int>(b)] = sg.img[off - sg.lo];
+        }
+      }
+      host_adam_step(hp, step, st3, grad + (e - e0), lpb, static_cast<int>(lp), 1, *host_pool);
+      for (u64 b = 0; b < 12; ++b)
+        for (Segment& sg : ob.segs)
+          if (sg.lo <= 12 * e + b && 12 * e + b < sg.hi) sg.img[12 * e + b - sg.lo] = reinterpret_cast<uint8_t*>(st3)[b];
+      for (u64 b = 0; b < lp; ++b)
+        for (Segment& sg : pbb.segs)
+          if (sg.lo <= lp * e + b && lp * e + b < sg.hi) sg.img[lp * e + b - sg.lo] = lpb[b];
+      ++e;
+      continue;
+    }
+    // a piece may start mid-element only where a boundary split an element,
+    // which the branch above consumed; both offsets are element-aligned here
+    float* state = reinterpret_cast<float*>(so->img + (12 * e - so->lo));
+    void* out = sp->img + (lp * e - sp->lo);
+    host_adam_step(hp, step, state, grad + (e - e0), out, static_cast<int>(lp), end - e, *host_pool);
+    e = end;
   }
 }
 
@@ -1168,11 +1312,17 @@ void Executor::Impl::step_task(const Task& t, int it) {
       }
       return;
     }
-    if (loc_late > 0) apply_adam(l, loc_now, n_my, retain[static_cast<size_t>(l)], static_cast<int>(git), s_opt, it);
+    if (loc_late > 0) {
+      if (host_step) apply_adam_host(l, loc_now, n_my, host_retain[static_cast<size_t>(l)], static_cast<int>(git));
+      else apply_adam(l, loc_now, n_my, retain[static_cast<size_t>(l)], static_cast<int>(git), s_opt, it);
+    }
     late_applied[static_cast<size_t>(l)].store(ready);
     return;
   }
-  if (loc_now > 0)
+  if (loc_now > 0 && host_step)
+    apply_adam_host(l, 0, loc_now, reinterpret_cast<const float*>(host_grad[static_cast<size_t>(l % host_grad_ring)]),
+                    static_cast<int>(git + 1));
+  else if (loc_now > 0)
     apply_adam(l, 0, loc_now, grad_shard[static_cast<size_t>(l % grad_ring)], static_cast<int>(git + 1), s_opt, it);
 }
 
@@ -1226,7 +1376,21 @@ void Executor::Impl::xfer_task(const Task& t, int it, u64& phys) {
     }
     case DataKind::GradAccum: {
       float* g = grad_shard[static_cast<size_t>(l % grad_ring)];
-      if (t.link == LinkKind::PCIe_D2H) {
+      if (t.link == LinkKind::PCIe_D2H && host_step) {
+        // immediate slice -> the ring slot the step reads, delayed slice ->
+        // the layer's retained copy (the next iteration's forward-phase step)
+        cuda_check(cudaMemcpyAsync(host_grad[static_cast<size_t>(l % host_grad_ring)], g, 4 * loc_now,
+                                   cudaMemcpyDeviceToHost, s_d2h),
+                   "grad");
+        if (loc_late > 0)
+          cuda_check(cudaMemcpyAsync(host_retain[static_cast<size_t>(l)], g + loc_now, 4 * loc_late,
+                                     cudaMemcpyDeviceToHost, s_d2h),
+                     "grad");
+        if (t.bytes > 4 * n_my)  // shard padding (never with equal shards)
+          cuda_check(cudaMemcpyAsync(host_grad[static_cast<size_t>(l % host_grad_ring)] + 4 * n_my, g + n_my,
+                                     t.bytes - 4 * n_my, cudaMemcpyDeviceToHost, s_d2h),
+                     "grad");
+      } else if (t.link == LinkKind::PCIe_D2H) {
         cuda_check(cudaMemcpyAsync(host_grad[static_cast<size_t>(l % host_grad_ring)], g, t.bytes,
                                    cudaMemcpyDeviceToHost, s_d2h),
                    "grad");
@@ -1427,9 +1591,13 @@ void Executor::flush() {
       Blob& pb = I.param_blob[static_cast<size_t>(l)];
       // SSD-resident state: file -> staging slot, step, staging -> file
       if (I.ssd_opt) I.ssd_io(ob, 12 * I.loc_now, ob.size, false);
-      I.apply_adam(l, I.loc_now, I.n_my, I.retain[static_cast<size_t>(l)], static_cast<int>(ready + 1), I.s_opt, -2,
-                   Src::Image);
-      cuda_check(cudaStreamSynchronize(I.s_opt), "flush step");
+      if (I.host_step) {
+        I.apply_adam_host(l, I.loc_now, I.n_my, I.host_retain[static_cast<size_t>(l)], static_cast<int>(ready + 1));
+      } else {
+        I.apply_adam(l, I.loc_now, I.n_my, I.retain[static_cast<size_t>(l)], static_cast<int>(ready + 1), I.s_opt, -2,
+                     Src::Image);
+        cuda_check(cudaStreamSynchronize(I.s_opt), "flush step");
+      }
       if (I.ssd_opt) I.ssd_io(ob, 12 * I.loc_now, ob.size, true);
       if (I.ssd_param) I.ssd_io(pb, lp * I.loc_now, pb.size, true);
     }

@@ -4,6 +4,7 @@
 #include <fcntl.h>
 #include <linux/io_uring.h>
 #include <sys/mman.h>
+#include <sys/resource.h>
 #include <sys/syscall.h>
 #include <unistd.h>
 
@@ -32,8 +33,14 @@ uint8_t* PinnedArena::alloc(uint64_t bytes) {
   return static_cast<uint8_t*>(p);
 }
 
-ThreadPool::ThreadPool(int n) {
-  for (int i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+ThreadPool::ThreadPool(int n, int nice_incr) {
+  for (int i = 0; i < n; ++i)
+    workers_.emplace_back([this, nice_incr] {
+      // background workers yield the cores to the executor's dispatcher
+      // threads (the compute dispatcher enqueues kernels back to back)
+      if (nice_incr > 0) (void)setpriority(PRIO_PROCESS, static_cast<id_t>(syscall(SYS_gettid)), nice_incr);
+      loop();
+    });
 }
 
 ThreadPool::~ThreadPool() {

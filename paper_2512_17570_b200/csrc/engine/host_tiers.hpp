@@ -35,7 +35,8 @@ class PinnedArena {
 // Fixed pool of worker threads running std::function jobs.
 class ThreadPool {
  public:
-  explicit ThreadPool(int n);
+  // nice_incr > 0 lowers the workers' scheduling priority (setpriority)
+  explicit ThreadPool(int n, int nice_incr = 0);
   ~ThreadPool();
   // Runs all jobs to completion on the pool (the caller blocks).
   void run_all(std::vector<std::function<void()>>& jobs);

@@ -46,7 +46,7 @@ const std::map<std::string, std::vector<std::string>> kOptions = {
     {"traffic", {"out", "format", "schedule", "microbatches", "alpha", "split"}},
     {"alloc-plan", {"count", "size"}},
     {"run", {"out", "format", "schedule", "microbatches", "alpha", "split", "iterations", "warmup", "vocab",
-             "nvme-dir", "seed", "device", "lp-bytes", "from-plan"}},
+             "nvme-dir", "seed", "device", "lp-bytes", "from-plan", "emit-trace"}},
 };
 
 Args parse_args(int argc, char** argv) {
@@ -341,6 +341,27 @@ int cmd_alloc(const Args& a) {
   return 0;
 }
 
+// The executed trace in the plan wire format (plan_to_json, the reference's
+// `--emit-plan` schema, proj/src/json_io.cpp:142-180) with, per task, one
+// record per executed iteration: the resource queue it ran on, its start /
+// end (ms from the run start; CUDA events for GPU-side tasks) and the bytes
+// physically moved.  Stripping "trace" gives back the input plan.
+Json trace_to_json(const SchedulePlan& plan, const std::vector<TraceRecord>& trace) {
+  Json j = plan_to_json(plan);
+  std::vector<Json> per(plan.tasks.size(), Json::array());
+  for (const TraceRecord& r : trace) {
+    if (r.task < 0 || r.task >= static_cast<int>(per.size())) throw PlanBugError("trace record of an unknown task");
+    per[r.task].push_back(Json{{"iteration", r.iteration},
+                               {"resource", resource_name(r.resource)},
+                               {"start_ms", r.t_start_ms},
+                               {"end_ms", r.t_end_ms},
+                               {"physical_bytes", r.physical_bytes}});
+  }
+  Json& tasks = j["tasks"];
+  for (size_t i = 0; i < per.size(); ++i) tasks[i]["trace"] = std::move(per[i]);
+  return j;
+}
+
 // Executes the configuration on the GPU (bf16 by default; --lp-bytes 4 for
 // the fp32 parity mode) with synthetic tokens and random-init weights.
 int cmd_run(const Args& a) {
@@ -366,6 +387,7 @@ int cmd_run(const Args& a) {
     st = st * 6364136223846793005ull + 1442695040888963407ull;
     t = static_cast<int32_t>((st >> 33) % static_cast<uint64_t>(ec.vocab_size));
   }
+  ec.record_trace = a.has("emit-trace");
   Executor ex(plan, ec);
   if (warm > 0) ex.run(warm, tokens.data());
   const ExecReport rep = ex.run(iters, tokens.data() + static_cast<size_t>(per_it) * warm);
@@ -383,6 +405,11 @@ int cmd_run(const Args& a) {
   j["losses"] = losses;
   j["traffic"] = ledger_to_json(rep.ledger);
   j["extension_traffic"] = ledger_to_json(rep.extension);
+  if (a.has("emit-trace")) {
+    std::ofstream out(a.get("emit-trace"));
+    if (!out) throw ValidationError("cannot open --emit-trace path");
+    out << trace_to_json(plan, rep.trace).dump() << "\n";
+  }
   emit(cfg, a, csv(cfg, a) ? kv_csv(j) : j.dump(2) + "\n");
   return 0;
 }

@@ -65,6 +65,13 @@ CASES = [
     ((0.3, 0.7, 0.5), 0.25, 0),
     ((1, 0, 0), 0.2, 0),     # config 5 split
     ((1, 1, 1), 1.0, 0),     # everything delayed
+    # OptTier::Host (3): CpuStep on the host cores, grads from the GradAccum D2H
+    ((1, 1, 1), 0.0, 3),     # all DRAM, no delayed slice
+    ((1, 1, 1), 0.25, 3),    # configs[1] placement + delayed slice
+    ((1, 1, 0.5), 0.2, 3),   # half the state on NVMe (staging slots stepped in place)
+    ((0.3, 0.7, 0.5), 0.25, 3),  # byte-granular split cuts inside elements
+    ((0, 0, 0), 0.0, 3),     # all SSD
+    ((1, 1, 1), 1.0, 3),     # everything delayed
 ]
 
 
@@ -108,21 +115,23 @@ def test_fp32_engine_matches_torch_fp64_golden():
     assert rel(fixed, GOLD["final_fixed"]) < 1e-4
 
 
-def test_split_runs_equal_one_run():
+@pytest.mark.parametrize("tier", [0, 3])
+def test_split_runs_equal_one_run(tier):
     """run(1) x 3 == run(3): the pending alpha slice carries across calls."""
     need_gpu()
     g, M = ob.TINY, 4
-    _, _, l_a, p_a, f_a, _ = run_engine(g, M, (1, 1, 0), 0.25, 3)
-    _, _, l_b, p_b, f_b, _ = run_engine(g, M, (1, 1, 0), 0.25, 3, chunks=[1, 1, 1])
+    _, _, l_a, p_a, f_a, _ = run_engine(g, M, (1, 1, 0), 0.25, 3, opt_tier=tier)
+    _, _, l_b, p_b, f_b, _ = run_engine(g, M, (1, 1, 0), 0.25, 3, chunks=[1, 1, 1], opt_tier=tier)
     assert np.allclose(l_a, l_b, rtol=1e-6)
     # fp32 atomics (embedding scatter, attention dK/dV) reorder sums
     assert rel(p_b, p_a) < 1e-5 and rel(f_b, f_a) < 1e-5
 
 
-def test_trace_order_and_ledger():
+@pytest.mark.parametrize("tier", [0, 3])
+def test_trace_order_and_ledger(tier):
     need_gpu()
     g, M = ob.TINY, 4
-    plan, reps, *_ = run_engine(g, M, (0.3, 0.7, 0.5), 0.25, 2, trace=True)
+    plan, reps, *_ = run_engine(g, M, (0.3, 0.7, 0.5), 0.25, 2, trace=True, opt_tier=tier)
     tr = reps[-1].trace
     last = [r for r in tr if r["iteration"] == 1]
     tasks = [plan.task(i) for i in range(len(plan))]

@@ -6,22 +6,30 @@ Geometries (BASELINE.json configs):
   GPT-1.3B layer  h=2048, 16 heads, s=2048, b=2, vocab 50304, 2 layers
   GPT-13B layer   h=5120, 40 heads, s=2048, b=2, 1 layer
   GPT-65B layer   h=8192, 64 heads, s=2048, b=1, 1 layer
-each as a vertical plan with the alpha-delayed step (alpha = 0.2), M = 2
-micro-batches, two iterations, the optimizer state in pinned host DRAM and
+each as a vertical plan with the alpha-delayed step, M = 2 micro-batches
+(alpha = 0.2 at GPT-1.3B; 0.1 / 0.04 at the one-layer 13B / 65B slices, the
+largest delay ratios build_vertical's alpha-residency check admits there,
+schedule.cpp:293-305), two iterations, the optimizer state in pinned host DRAM and
 streamed through HBM (opt_tier 2, BASELINE configs[1]'s placement).
 
 bf16 mode runs the production kernels (tcgen05 GEMMs, tcgen05 attention,
-the LN / GELU / cross-entropy / fused Adam kernels).  Gates, stated per
-quantity (measured values are printed; DESIGN.md §3 lists them):
+the LN / GELU / cross-entropy / fused Adam kernels).  Its distance from the
+fp32 reference is judged against torch's own mixed precision on the same
+inputs: tests/torch_ref.py under torch.autocast(bfloat16) (bf16 GEMMs, fp32
+accumulation, fp32 masters / gradients / Adam).  Gates, per quantity
+(measured values are printed; DESIGN.md §3 lists them):
   * per-step loss within 2e-3 relative of fp32;
-  * Adam first moment m after two steps (a linear combination of the two
-    iterations' fp32-accumulated gradients) within 2e-2 norm-relative, for
-    the layer weights and the embedding table;
-  * second moment v within 4e-2 norm-relative;
-  * parameter update (w_final - w_init) within 0.15 norm-relative — Adam's
-    first step is lr * sign(g) element-wise, so every gradient element
-    whose bf16 and fp32 signs differ moves by 2 lr; a wrong gradient gives
-    ~1.4.
+  * Adam moments m, v after two steps (the layer weights and the embedding
+    table; m is a linear combination of the two iterations' fp32-accumulated
+    gradients): norm-relative distance from fp32 at most
+    max(floor, 1.5 x torch-autocast's), floor 2e-2 for m and 4e-2 for v —
+    the bf16 error grows with the contraction length (h = 8192: ~2.4e-2 for
+    both implementations), so a fixed bound would either fail honest bf16
+    or admit a broken gradient;
+  * parameter update (w_final - w_init) within max(0.15, 1.5 x torch's) —
+    Adam's first step is lr * sign(g) element-wise, so every gradient
+    element whose bf16 and fp32 signs differ moves by 2 lr; a wrong
+    gradient gives ~1.4.
 fp32 mode (low_precision_bytes = 4) at the GPT-1.3B geometry holds the
 north-star tolerances: loss 1e-3 relative, parameters after the steps (after
 flush()) 1e-4 relative.
@@ -80,26 +88,45 @@ def run_both(g, lp, M=2, iters=2, alpha=0.2, split=(1, 1, 1), opt_tier=2):
     torch.backends.cudnn.allow_tf32 = False
     ref = tr.train(g, ADAM, l0, f0, toks, device="cuda", dtype="float32")
     torch.cuda.empty_cache()
+    amp = None
+    if lp == 2:
+        amp = tr.train(g, ADAM, l0, f0, toks, device="cuda", dtype="float32", autocast_bf16=True)
+        torch.cuda.empty_cache()
     out = dict(
         loss=float(np.max(np.abs(np.array(rep.losses) - ref["losses"]) / ref["losses"])),
         m=rel(m, ref["m"]), v=rel(v, ref["v"]), fm=rel(fm, ref["fm"]), fv=rel(fv, ref["fv"]),
         dw=rel(l1 - l0, ref["layers"] - l0), dfixed=rel(f1 - f0, ref["fixed"] - f0),
         w=rel(l1, ref["layers"]), fixed=rel(f1, ref["fixed"]))
+    if amp is not None:
+        out["torch_amp"] = dict(
+            loss=float(np.max(np.abs(amp["losses"] - ref["losses"]) / ref["losses"])),
+            m=rel(amp["m"], ref["m"]), v=rel(amp["v"], ref["v"]), fm=rel(amp["fm"], ref["fm"]),
+            fv=rel(amp["fv"], ref["fv"]), dw=rel(amp["layers"] - l0, ref["layers"] - l0),
+            dfixed=rel(amp["fixed"] - f0, ref["fixed"] - f0))
     print(f"\nparity h={g.hidden} lp={lp}: losses {rep.losses} ref {ref['losses'].tolist()} " +
-          " ".join(f"{k}={x:.3e}" for k, x in out.items()))
+          " ".join(f"{k}={x:.3e}" for k, x in out.items() if k != "torch_amp") +
+          (" | torch autocast-bf16: " + " ".join(f"{k}={x:.3e}" for k, x in out["torch_amp"].items())
+           if amp is not None else ""))
     return out
 
 
-@pytest.mark.parametrize("name", ["gpt1.3b", "gpt13b", "gpt65b"])
-def test_bf16_production_path_matches_fp32_reference(name):
-    r = run_both(GEOMS[name], lp=2)
+ALPHA = {"gpt1.3b": 0.2, "gpt13b": 0.1, "gpt65b": 0.04}
+
+
+@pytest.mark.parametrize("name,tier", [("gpt1.3b", gs.OPT_STREAM), ("gpt1.3b", gs.OPT_HOST),
+                                       ("gpt13b", gs.OPT_STREAM), ("gpt65b", gs.OPT_HOST)])
+def test_bf16_production_path_matches_fp32_reference(name, tier):
+    r = run_both(GEOMS[name], lp=2, alpha=ALPHA[name], opt_tier=tier)
+    t = r["torch_amp"]
+    bound = lambda k, floor: max(floor, 1.5 * t[k])  # noqa: E731
     assert r["loss"] < 2e-3
-    assert r["m"] < 2e-2 and r["fm"] < 2e-2
-    assert r["v"] < 4e-2 and r["fv"] < 4e-2
-    assert r["dw"] < 0.15 and r["dfixed"] < 0.15
+    assert r["m"] < bound("m", 2e-2) and r["fm"] < bound("fm", 2e-2)
+    assert r["v"] < bound("v", 4e-2) and r["fv"] < bound("fv", 4e-2)
+    assert r["dw"] < bound("dw", 0.15) and r["dfixed"] < bound("dfixed", 0.15)
 
 
-def test_fp32_mode_at_gpt1_3b_layer_geometry_holds_north_star_tolerances():
-    r = run_both(GEOMS["gpt1.3b"], lp=4)
+@pytest.mark.parametrize("tier", [gs.OPT_STREAM, gs.OPT_HOST])
+def test_fp32_mode_at_gpt1_3b_layer_geometry_holds_north_star_tolerances(tier):
+    r = run_both(GEOMS["gpt1.3b"], lp=4, opt_tier=tier)
     assert r["loss"] < 1e-3
     assert r["w"] < 1e-4 and r["fixed"] < 1e-4

@@ -98,12 +98,19 @@ def layer_fwd(torch, x, w, h, H):
     return x1 + g @ w2.T
 
 
-def train(geom, adam, layers0, fixed0, toks, device="cpu", dtype="float32", checkpoint=True):
+def train(geom, adam, layers0, fixed0, toks, device="cpu", dtype="float32", checkpoint=True, autocast_bf16=False):
     """Plain-loop training of `toks` [iters][M][b][s+1] from the given fp32
     master weights.  Returns dict(losses, layers, fixed, m, v, fm, fv) as
-    numpy float32 (losses float64)."""
+    numpy float32 (losses float64).  autocast_bf16: the forward / backward
+    under torch.autocast(bfloat16) (bf16 GEMMs with fp32 accumulation, fp32
+    masters, gradients and Adam) — torch's own mixed-precision deviation from
+    fp32, the yardstick for the executor's bf16 path."""
+    import contextlib
+
     import torch
     import torch.utils.checkpoint as ckpt
+    amp = (lambda: torch.autocast(device_type=device if device != "cpu" else "cpu", dtype=torch.bfloat16)) \
+        if autocast_bf16 else contextlib.nullcontext
 
     N, h, H, s, V = geom.n_layers, geom.hidden, geom.heads, geom.seq, geom.vocab
     dt = getattr(torch, dtype)
@@ -121,12 +128,14 @@ def train(geom, adam, layers0, fixed0, toks, device="cpu", dtype="float32", chec
             t = torch.tensor(toks[it, m], dtype=torch.long, device=device)
             wte = F[:V * h].view(V, h)
             wpe = F[V * h:].view(s, h)
-            x = wte[t[:, :s]] + wpe[None, :, :]
-            for l in range(N):
-                # recompute-from-checkpoint, as the executor does (also bounds memory)
-                x = ckpt.checkpoint(layer_fwd, torch, x, W[l], h, H, use_reentrant=False) if checkpoint else \
-                    layer_fwd(torch, x, W[l], h, H)
-            logits = _ln(torch, x) @ wte.T
+            with amp():
+                x = wte[t[:, :s]] + wpe[None, :, :]
+                for l in range(N):
+                    # recompute-from-checkpoint, as the executor does (also bounds memory)
+                    x = ckpt.checkpoint(layer_fwd, torch, x, W[l], h, H, use_reentrant=False) if checkpoint else \
+                        layer_fwd(torch, x, W[l], h, H)
+                logits = _ln(torch, x) @ wte.T
+            logits = logits.float() if autocast_bf16 else logits
             loss = torch.nn.functional.cross_entropy(logits.reshape(-1, V), t[:, 1:].reshape(-1))
             (loss / M).backward()
             total += float(loss.item())
