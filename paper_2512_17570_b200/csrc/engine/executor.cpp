@@ -57,10 +57,6 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 
-int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return (e && *e) ? atoi(e) : dflt;
-}
 
 // ------------------------------------------------------------ weight init
 // Bit-identical to oracle/gs_oracle.c (gso_splitmix64 / gso_normal /
@@ -365,10 +361,10 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   (void)cudaGetLastError();  // do not inherit a stale error of an earlier, unrelated call
   // Stream priorities: the compute stream carries the critical path (the
   // dgrad -> LN' -> attention' chain); the optimizer stream's Adam kernels
-  // fill idle SMs (GS_STREAM_PRIO=0 gives every stream the default; measured
-  // +0.5% over it, within run-to-run noise, profiles/round1_stream_prio_ab.txt).
+  // fill idle SMs (measured +0.5% over default priorities, within run-to-run
+  // noise, profiles/round1_stream_prio_ab.txt).
   int prio_lo = 0, prio_hi = 0;
-  if (env_int("GS_STREAM_PRIO", 2)) cuda_check(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "priority range");
+  cuda_check(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "priority range");
   cuda_check(cudaStreamCreateWithPriority(&s_gpu, cudaStreamNonBlocking, prio_hi), "stream");
   cuda_check(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking), "stream");
   cuda_check(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking), "stream");

@@ -137,10 +137,9 @@ bool alloc_workspace(const Dims& d, Workspace& ws) {
   get(reinterpret_cast<void**>(&ws.logits), sizeof(float) * T * d.V);
   get(&ws.dlogits, T * d.V * eb);
   // The weight-gradient stream shares the compute stream's (highest)
-  // priority, above the optimizer stream (GS_STREAM_PRIO=0/1: default / lowest).
+  // priority, above the optimizer stream.
   int prio_lo = 0, prio_hi = 0;
-  const char* pe = getenv("GS_STREAM_PRIO");
-  if (!pe || !*pe || atoi(pe) == 2) cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (ok && (cudaStreamCreateWithPriority(&ws.side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
              cudaEventCreateWithFlags(&ws.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
              cudaEventCreateWithFlags(&ws.ev_join, cudaEventDisableTiming) != cudaSuccess))

@@ -136,50 +136,10 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x on the FMA / ALU pipes (FA4-style MUFU offload): x = j + f with
-// j = round(x) (magic-number add), 2^f on [-0.5, 0.5] by a degree-4 minimax
-// polynomial (max relative error 2.7e-6, far below bf16's 2^-9), then j added
-// into the exponent bits.  Valid for x >= -126 (results below flush to ~0).
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -126.0f);
-  const float t = x + 12582912.0f;  // 1.5 * 2^23: round to nearest integer
-  const float j = t - 12582912.0f;
-  const float f = x - j;
-  float p = 9.5699895e-3f;  // relative-minimax fit on [-0.5, 0.5], |err| < 2.7e-6
-  p = fmaf(p, f, 5.5917580e-2f);
-  p = fmaf(p, f, 2.4024744e-1f);
-  p = fmaf(p, f, 6.9312185e-1f);
-  p = fmaf(p, f, 9.9999930e-1f);
-  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
-}
-
 __device__ __forceinline__ uint32_t pack(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
 }
-
-// ------------------------------------------------------------ forward v2
-// 64-key blocks: 96 KB of shared memory and 256 TMEM columns per CTA, so two
-// CTAs share an SM and one CTA's softmax overlaps the other's MMAs.  P never
-// touches shared memory: the softmax warps tcgen05.st it (bf16 pairs) over
-// the S buffer they have just read, and O += P V is a TS-MMA (A from TMEM).
-// With P double-buffered that way, softmax(kb) no longer waits for PV(kb-1)
-// except to rescale O (rare: lazy rescaling below).
-constexpr int kBK2 = 64;
-constexpr int kKV2 = kBK2 * kD * 2;  // 16 KB
-constexpr int kKS2 = 2;  // K ring depth (V: 2)
-struct FaSmem2 {
-  uint8_t Q[kTile];          // [2 d-chunks][128 rows][128 B]
-  uint8_t K[kKS2][kKV2];     // [2 d-chunks][64 rows][128 B]
-  uint8_t V[2][kKV2];
-  // K and V have their own producers and release points: K(kb) is freed
-  // right after S(kb), V(kb) after PV(kb), so the load of K(kb+2) overlaps
-  // softmax(kb).  (A third K slot, tried, changes nothing: the GS_ATTN_TRACE
-  // timeline shows the S / PV MMAs of the two CTAs on an SM, not the loads,
-  // pacing the blocks.)
-  uint64_t q_full, k_full[kKS2], v_full[2], k_empty[kKS2], v_empty[2], s_full[2], p_full[2], o_done;
-  uint32_t tmem;
-};
 
 // GS_ATTN_TRACE grid schedule: {smid, start, end} of this CTA (see attn_trace_end)
 __device__ __forceinline__ long long gtimer() {
@@ -196,232 +156,6 @@ __device__ __forceinline__ void cta_stamp(long long* tr, int slot) {
     c[0] = sm;
   }
   c[slot] = gtimer();
-}
-
-template <int POLY>  // POLY: every 4th exponential on the FMA pipes instead of the SFU
-__global__ void __launch_bounds__(256, 2)
-    fa_fwd_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
-                      bf16* __restrict__ o, float* __restrict__ lse, int s, int h, int H, float scale_log2,
-                      long long* __restrict__ tr) {
-  extern __shared__ __align__(1024) uint8_t raw2[];
-  FaSmem2& sm = *reinterpret_cast<FaSmem2*>(raw2);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // grid (b*H, s/128): every head's heaviest query tile is launched before
-  // any lighter one (longest-processing-time-first over the whole grid)
-  const int qb = gridDim.y - 1 - blockIdx.y;
-  const int bh = blockIdx.x, bi = bh / H, j = bh % H;
-  const int row0 = bi * s, q0 = qb * kBQ;
-  const int nblk = (q0 + kBQ) / kBK2;  // causal: keys < q0 + 128
-  // GS_ATTN_TRACE: clock64 stamps of CTA (0, 0) (the heaviest tile):
-  // 0 MMA S(kb) issued, 1 MMA P(kb) seen, 2 softmax S(kb) seen, 3 softmax
-  // math done, 4 softmax P(kb) published, 5 producer K(kb), 6 producer V(kb)
-  cta_stamp(tr, 1);
-  long long* trc = (tr && blockIdx.x == 0 && blockIdx.y == 0) ? tr : nullptr;
-#define GS_TRF(ev, i)                                       \
-  do {                                                      \
-    if (trc && (i) < 64) trc[(ev) * 64 + (i)] = clock64();  \
-  } while (0)
-
-  if (threadIdx.x == 0) {
-    bar_init(&sm.q_full, 1);
-    for (int i = 0; i < kKS2; ++i) {
-      bar_init(&sm.k_full[i], 1);
-      bar_init(&sm.k_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      bar_init(&sm.v_full[i], 1);
-      bar_init(&sm.v_empty[i], 1);
-      bar_init(&sm.s_full[i], 1);
-      bar_init(&sm.p_full[i], 128);
-    }
-    bar_init(&sm.o_done, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&sm.tmem)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = sm.tmem;  // S0: 0-63, S1: 64-127, O: 128-255
-
-  if (warp == 0) {
-    if (lane == 0) {  // Q, then the K ring
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_q)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_kv)) : "memory");
-      bar_expect(&sm.q_full, kTile);
-      for (int c = 0; c < 2; ++c) tma2d(sm.Q + c * 16384, &map_q, &sm.q_full, j * kD + 64 * c, row0 + q0);
-      for (int kb = 0; kb < nblk; ++kb) {
-        const int sl = kb % kKS2;
-        bar_wait(&sm.k_empty[sl], ((kb / kKS2) & 1) ^ 1);
-        bar_expect(&sm.k_full[sl], kKV2);
-        for (int c = 0; c < 2; ++c)
-          tma2d(sm.K[sl] + c * 8192, &map_kv, &sm.k_full[sl], h + j * kD + 64 * c, row0 + kb * kBK2);
-        GS_TRF(5, kb);
-      }
-    }
-  } else if (warp == 2) {
-    if (lane == 0) {  // the V ring
-      for (int kb = 0; kb < nblk; ++kb) {
-        const int buf = kb & 1;
-        bar_wait(&sm.v_empty[buf], ((kb >> 1) & 1) ^ 1);
-        bar_expect(&sm.v_full[buf], kKV2);
-        for (int c = 0; c < 2; ++c)
-          tma2d(sm.V[buf] + c * 8192, &map_kv, &sm.v_full[buf], 2 * h + j * kD + 64 * c, row0 + kb * kBK2);
-        GS_TRF(6, kb);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t qa = su32(sm.Q);
-      bar_wait(&sm.q_full, 0);
-      auto issue_s = [&](int kb) {
-        const int buf = kb & 1, sl = kb % kKS2;
-        GS_TRF(7, kb);
-        bar_wait(&sm.k_full[sl], (kb / kKS2) & 1);
-        fence_after();
-        const uint32_t ka = su32(sm.K[sl]);
-#pragma unroll
-        for (int ks = 0; ks < kD / 16; ++ks)
-          mma(tmem + buf * 64, sdesc(qa + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024),
-              sdesc(ka + (ks >> 2) * 8192 + (ks & 3) * 32, 16, 1024),
-              (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24),
-              ks != 0);
-        commit(&sm.s_full[buf]);
-        commit(&sm.k_empty[sl]);
-        GS_TRF(0, kb);
-      };
-      issue_s(0);
-      for (int kb = 0; kb < nblk; ++kb) {
-        const int buf = kb & 1;
-        if (kb + 1 < nblk) issue_s(kb + 1);
-        bar_wait(&sm.p_full[buf], (kb >> 1) & 1);
-        GS_TRF(1, kb);
-        bar_wait(&sm.v_full[buf], (kb >> 1) & 1);
-        fence_after();
-        const uint32_t va = su32(sm.V[buf]);
-#pragma unroll
-        for (int ks = 0; ks < kBK2 / 16; ++ks)  // A = P(kb) in TMEM: 8 columns per 16 keys
-          mma_ts(tmem + 128, tmem + buf * 64 + ks * 8, sdesc(va + ks * 2048, 8192, 1024), idesc(true),
-                 (kb | ks) != 0);
-        commit(&sm.o_done);
-        commit(&sm.v_empty[buf]);
-      }
-    }
-  } else if (warp >= 4) {
-    const int r = (warp - 4) * 32 + lane;
-    const int qrow = q0 + r;
-    const uint32_t lane_base = ((uint32_t)((warp - 4) * 32)) << 16;
-    float m_run = -INFINITY, l_run = 0.0f;
-    for (int kb = 0; kb < nblk; ++kb) {
-      const int buf = kb & 1;
-      bar_wait(&sm.s_full[buf], (kb >> 1) & 1);
-      if (r == 0) GS_TRF(2, kb);
-      fence_after();
-      float sv[kBK2];
-      {  // both TMEM loads in flight before one wait (raw scores)
-        uint32_t rr[2][32];
-        tld32(tmem + lane_base + buf * 64, rr[0]);
-        tld32(tmem + lane_base + buf * 64 + 32, rr[1]);
-        tld_wait();
-#pragma unroll
-        for (int i = 0; i < kBK2; ++i) sv[i] = __uint_as_float(rr[i >> 5][i & 31]);
-      }
-      const bool mask = (kb + 1) * kBK2 > q0;  // blocks crossing the diagonal
-      // max over the raw scores (scale > 0 keeps the order); the log2-domain
-      // scale folds into the exponent's FFMA below.  Eight independent partial
-      // maxima / sums: a single 64-long dependent chain would leave the two
-      // softmax warps of an SMSP stalled on ALU latency.
-      float mp[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) mp[k] = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < kBK2; ++i) {
-        if (mask && kb * kBK2 + i > qrow) sv[i] = -INFINITY;
-        mp[i & 7] = fmaxf(mp[i & 7], sv[i]);
-      }
-      const float mraw = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
-                               fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
-      const float mx = fmaxf(m_run, mraw * scale_log2);
-      // Lazy rescaling: the running max only moves when the block max exceeds
-      // it by more than 2^8 (P <= 256 stays exact in bf16 / fp32); O and l
-      // are then consistent with the stale max and the final O / l, lse are
-      // unchanged.  With a moving max every block would pay a full TMEM
-      // read + write of O.
-      const bool bump = mx > m_run + 8.0f;
-      const float m_new = bump ? mx : m_run;
-      const float corr = bump ? ex2(m_run - mx) : 1.0f;
-      float ps[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
-      const float nm = -m_new;
-#pragma unroll
-      for (int i = 0; i < kBK2; ++i) {
-        const float x = fmaf(sv[i], scale_log2, nm);
-        sv[i] = (POLY && (i & 3) == 3) ? ex2_poly(x) : ex2(x);
-        ps[i & 7] += sv[i];
-      }
-      const float rs = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
-      l_run = l_run * corr + rs;
-      m_run = m_new;
-      if (r == 0) GS_TRF(3, kb);
-      {  // P(kb) -> TMEM over the S buffer just read (lane = query row)
-        uint32_t pk[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) pk[k] = pack(sv[2 * k], sv[2 * k + 1]);
-        tst32(tmem + lane_base + buf * 64, pk);
-      }
-      if (kb > 0 && __any_sync(0xffffffffu, bump)) {
-        bar_wait(&sm.o_done, (kb - 1) & 1);  // PV(kb-1) done: O final for the rescale
-        fence_after();
-#pragma unroll
-        for (int c = 0; c < kD / 32; ++c) {
-          uint32_t rr[32];
-          tld32(tmem + lane_base + 128 + c * 32, rr);
-          tld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * corr);
-          tst32(tmem + lane_base + 128 + c * 32, rr);
-        }
-      }
-      // o_done completes once per PV and a parity wait is only unambiguous
-      // one phase ahead.  Before this warp's p_full(kb) arrive the barrier is
-      // in phase kb-1 or kb (PV(kb) cannot be issued yet), so observe PV(kb-1)
-      // here on the last block; after the arrive it is in phase nblk-1 or
-      // nblk and the epilogue's wait for PV(nblk-1) cannot alias.
-      if (kb == nblk - 1 && kb > 0) bar_wait(&sm.o_done, (kb - 1) & 1);
-      tst_wait();
-      fence_before();
-      bar_arrive(&sm.p_full[buf]);
-      if (r == 0) GS_TRF(4, kb);
-    }
-    bar_wait(&sm.o_done, (nblk - 1) & 1);
-    fence_after();
-    const float inv = 1.0f / l_run;
-    bf16* orow = o + (long long)(row0 + qrow) * h + j * kD;
-#pragma unroll
-    for (int c = 0; c < kD / 32; ++c) {
-      uint32_t rr[32];
-      tld32(tmem + lane_base + 128 + c * 32, rr);
-      tld_wait();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 w;
-        w.x = pack(__uint_as_float(rr[8 * q]) * inv, __uint_as_float(rr[8 * q + 1]) * inv);
-        w.y = pack(__uint_as_float(rr[8 * q + 2]) * inv, __uint_as_float(rr[8 * q + 3]) * inv);
-        w.z = pack(__uint_as_float(rr[8 * q + 4]) * inv, __uint_as_float(rr[8 * q + 5]) * inv);
-        w.w = pack(__uint_as_float(rr[8 * q + 6]) * inv, __uint_as_float(rr[8 * q + 7]) * inv);
-        *reinterpret_cast<uint4*>(orow + c * 32 + 8 * q) = w;
-      }
-    }
-    lse[(long long)bh * s + qrow] = (m_run + log2f(l_run)) * 0.6931471805599453f;
-  }
-  fence_before();
-  __syncthreads();
-  cta_stamp(tr, 2);
-  if (warp == 2) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
-  }
 }
 
 // ------------------------------------------------------------ forward v3
@@ -479,7 +213,6 @@ struct FaSmem3 {
   uint32_t tmem;
 };
 
-template <int POLY>  // exponentials on the FMA pipes: 0 none, 1 one in four, 2 one in two
 __global__ void __launch_bounds__(kThreadsF3, 1)
     fa_fwd_tc3_kernel(const __grid_constant__ CUtensorMap map_t, const __grid_constant__ CUtensorMap map_o,
                       bf16* __restrict__ o, float* __restrict__ lse, int s, int h, int H, float scale_log2,
@@ -649,7 +382,7 @@ __global__ void __launch_bounds__(kThreadsF3, 1)
 #pragma unroll
         for (int i = 64 * half; i < 64 * half + 64; ++i) {
           const float x = fmaf(sv[i], scale_log2, nm);
-          sv[i] = ((POLY == 1 && (i & 3) == 3) || (POLY == 2 && (i & 1))) ? ex2_poly(x) : ex2(x);
+          sv[i] = ex2(x);
           ps[i & 7] += sv[i];
         }
         uint32_t pk[32];  // this half of P_t -> TMEM over S_t (32 columns of bf16 pairs)
@@ -747,269 +480,6 @@ constexpr int kThreadsBwd = 384;  // warps 0 TMA, 1 MMA, 2 TMEM alloc, 4-7 softm
 //   earlier than in v2.  dQ^T leaves through a 32-query fp32 staging half.
 //   TMEM: [0,128)/[128,256) S^T|dP^T of block i&1 (dQ^T(i) overwrites the
 //   S^T half after the softmax read it), [256,384) dV, [384,512) dK.
-constexpr int kQS = 3;  // Q / dO ring depth
-struct FaBwdSmem3 {
-  uint8_t K[kTile], V[kTile];
-  uint8_t Q[kQS][kHalf], dO[kQS][kHalf];
-  uint8_t PT[kPT], dST[kPT];
-  float dq_stage[kBQb / 2][kD];
-  float L[kQS][kBQb], D[kQS][kBQb];
-  uint64_t kv_full, q_full[kQS], q_empty[kQS], s_full[2], ps_full, pds_empty, dq_full[2], dq_empty[2], mma_done;
-  uint32_t tmem;
-};
-
-__global__ void __launch_bounds__(kThreadsBwd, 1)
-    fa_bwd_tc3_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_q,
-                      const __grid_constant__ CUtensorMap map_do, const __grid_constant__ CUtensorMap map_dq,
-                      const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv, int s,
-                      int h, int H, float scale, long long* __restrict__ tr) {
-  extern __shared__ __align__(1024) uint8_t rawb3[];
-  FaBwdSmem3& sm = *reinterpret_cast<FaBwdSmem3*>(rawb3);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = blockIdx.y;  // grid (b*H, s/128): key block 0 (most query blocks) first
-  const int bh = blockIdx.x, bi = bh / H, j = bh % H;
-  const int row0 = bi * s;
-  const int k0 = kb * kBK;
-  const int qb0 = k0 / kBQb, nq = s / kBQb - qb0;
-  const float scale_log2 = scale * 1.4426950408889634f;
-  // GS_ATTN_TRACE diagnostics: clock64 stamps of CTA (0, 0)'s pipeline events
-  // tr[ev * 64 + i]: 0 mma ps_full(i) seen, 1 mma S(i) issued, 2 softmax
-  // s_full(i) seen, 3 softmax math done, 4 softmax P/dS written, 5 drain
-  // dq_full(i) seen, 6 drain dq_empty(i) arrived, 7 producer Q(i) issued
-  long long* trc = (tr && blockIdx.x == 0 && blockIdx.y == 0) ? tr : nullptr;
-#define GS_TR(ev, i)                                             \
-  do {                                                           \
-    if (trc && (i) < 64) trc[(ev) * 64 + (i)] = clock64();       \
-  } while (0)
-
-  if (threadIdx.x == 0) {
-    bar_init(&sm.kv_full, 1);
-    for (int i = 0; i < kQS; ++i) {
-      bar_init(&sm.q_full[i], 1);
-      bar_init(&sm.q_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      bar_init(&sm.s_full[i], 1);
-      bar_init(&sm.dq_full[i], 1);
-      bar_init(&sm.dq_empty[i], 128);
-    }
-    bar_init(&sm.ps_full, 128);
-    bar_init(&sm.pds_empty, 1);
-    bar_init(&sm.mma_done, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = sm.tmem;
-  constexpr uint32_t kDV = 256, kDK = 384;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_do)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_q)) : "memory");
-      bar_expect(&sm.kv_full, 2 * kTile);
-      for (int c = 0; c < 2; ++c) {
-        tma2d(sm.K + c * 16384, &map_qkv, &sm.kv_full, h + j * kD + 64 * c, row0 + k0);
-        tma2d(sm.V + c * 16384, &map_qkv, &sm.kv_full, 2 * h + j * kD + 64 * c, row0 + k0);
-      }
-      for (int i = 0; i < nq; ++i) {
-        const int sl = i % kQS, q0 = (qb0 + i) * kBQb;
-        bar_wait(&sm.q_empty[sl], ((i / kQS) & 1) ^ 1);
-        bar_expect(&sm.q_full[sl], 2 * kHalf + 2 * kBQb * 4);
-        for (int c = 0; c < 2; ++c) {
-          tma2d(sm.Q[sl] + c * 8192, &map_q, &sm.q_full[sl], j * kD + 64 * c, row0 + q0);
-          tma2d(sm.dO[sl] + c * 8192, &map_do, &sm.q_full[sl], j * kD + 64 * c, row0 + q0);
-        }
-        bulk_g2s(sm.L[sl], lse + (long long)bh * s + q0, kBQb * 4, &sm.q_full[sl]);
-        bulk_g2s(sm.D[sl], Dg + (long long)bh * s + q0, kBQb * 4, &sm.q_full[sl]);
-        GS_TR(7, i);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t ka = su32(sm.K), va = su32(sm.V), pa = su32(sm.PT), da = su32(sm.dST);
-      bar_wait(&sm.kv_full, 0);
-      auto issue_s = [&](int i) {  // S^T, dP^T of block i into TMEM buffer i&1
-        const int buf = i & 1, sl = i % kQS;
-        bar_wait(&sm.q_full[sl], (i / kQS) & 1);
-        bar_wait(&sm.dq_empty[buf], ((i >> 1) & 1) ^ 1);  // dQ^T of block i-2 drained
-        GS_TR(1, i);
-        fence_after();
-        const uint32_t qa = su32(sm.Q[sl]), oa = su32(sm.dO[sl]);
-        const uint32_t t0 = tmem + buf * 128;
-#pragma unroll
-        for (int ks = 0; ks < kD / 16; ++ks) {
-          mma(t0, desc_k(ka, ks, 128), desc_k(qa, ks, 64), idesc2(64, false, false), ks != 0);
-          mma(t0 + 64, desc_k(va, ks, 128), desc_k(oa, ks, 64), idesc2(64, false, false), ks != 0);
-        }
-        commit(&sm.s_full[buf]);
-      };
-      issue_s(0);
-      if (nq > 1) issue_s(1);
-      for (int i = 0; i < nq; ++i) {
-        const int buf = i & 1, sl = i % kQS;
-        bar_wait(&sm.ps_full, i & 1);
-        GS_TR(0, i);
-        fence_after();
-        // dQ^T(i) = K^T dS^T into the (already read) S^T half of buffer i&1
-#pragma unroll
-        for (int ks = 0; ks < kBK / 16; ++ks)
-          mma(tmem + buf * 128, desc_mn(ka, ks, 16384), desc_mn(da, ks, 8192), idesc2(64, true, true), ks != 0);
-        commit(&sm.dq_full[buf]);
-        const uint32_t qa = su32(sm.Q[sl]), oa = su32(sm.dO[sl]);
-#pragma unroll
-        for (int ks = 0; ks < kBQb / 16; ++ks) {
-          mma(tmem + kDV, desc_k(pa, ks, 128), desc_mn(oa, ks, 8192), idesc2(128, false, true), (i | ks) != 0);
-          mma(tmem + kDK, desc_k(da, ks, 128), desc_mn(qa, ks, 8192), idesc2(128, false, true), (i | ks) != 0);
-        }
-        commit(&sm.q_empty[sl]);
-        commit(&sm.pds_empty);
-        if (i + 2 < nq) issue_s(i + 2);
-      }
-      commit(&sm.mma_done);
-    }
-  } else if (warp >= 4 && warp < 8) {
-    const int r = (warp - 4) * 32 + lane;  // key row
-    const uint32_t lb = ((uint32_t)((warp & 3) * 32)) << 16;
-    const int key = k0 + r;
-    const uint32_t swz = (uint32_t)(r & 7);
-    const int rowoff = (r >> 3) * 1024 + (r & 7) * 128;
-    for (int i = 0; i < nq; ++i) {
-      const int buf = i & 1, sl = i % kQS, q0 = (qb0 + i) * kBQb;
-      bar_wait(&sm.q_full[sl], (i / kQS) & 1);  // L, D of this block
-      bar_wait(&sm.s_full[buf], (i >> 1) & 1);
-      if (r == 0) GS_TR(2, i);
-      fence_after();
-      float p[kBQb], ds[kBQb];
-      // only the two query blocks on the diagonal (i < 2) hold masked pairs
-      const bool diag = q0 < k0 + kBK;
-#pragma unroll
-      for (int c = 0; c < kBQb / 32; ++c) {
-        uint32_t a[32], b[32];
-        tld32(tmem + lb + buf * 128 + c * 32, a);
-        tld32(tmem + lb + buf * 128 + 64 + c * 32, b);
-        tld_wait();
-        if (diag) {
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const int qi = c * 32 + q;
-            float pv = ex2(fmaf(__uint_as_float(a[q]), scale_log2, -sm.L[sl][qi]));
-            if (q0 + qi < key) pv = 0.0f;  // causal
-            p[qi] = pv;
-            ds[qi] = pv * (__uint_as_float(b[q]) - sm.D[sl][qi]);
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const int qi = c * 32 + q;
-            const float pv = ex2(fmaf(__uint_as_float(a[q]), scale_log2, -sm.L[sl][qi]));
-            p[qi] = pv;
-            ds[qi] = pv * (__uint_as_float(b[q]) - sm.D[sl][qi]);
-          }
-        }
-      }
-      if (r == 0) GS_TR(3, i);
-      bar_wait(&sm.pds_empty, (i & 1) ^ 1);  // MMAs of block i-1 done with P^T / dS^T
-#pragma unroll
-      for (int pc = 0; pc < 8; ++pc) {
-        const float* v = p + pc * 8;
-        const float* w = ds + pc * 8;
-        *reinterpret_cast<uint4*>(sm.PT + rowoff + ((pc ^ swz) << 4)) =
-            make_uint4(pack(v[0], v[1]), pack(v[2], v[3]), pack(v[4], v[5]), pack(v[6], v[7]));
-        *reinterpret_cast<uint4*>(sm.dST + rowoff + ((pc ^ swz) << 4)) =
-            make_uint4(pack(w[0], w[1]), pack(w[2], w[3]), pack(w[4], w[5]), pack(w[6], w[7]));
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      fence_before();
-      bar_arrive(&sm.ps_full);
-      if (r == 0) GS_TR(4, i);
-    }
-    bar_wait(&sm.mma_done, 0);
-    fence_after();
-    bf16* out = dqkv + (long long)(row0 + key) * 3 * h + h + j * kD;
-#pragma unroll
-    for (int c = 0; c < kD / 32; ++c) {
-      uint32_t rr[32];
-      tld32(tmem + lb + kDK + c * 32, rr);
-      tld_wait();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 w;
-        w.x = pack(__uint_as_float(rr[8 * q]) * scale, __uint_as_float(rr[8 * q + 1]) * scale);
-        w.y = pack(__uint_as_float(rr[8 * q + 2]) * scale, __uint_as_float(rr[8 * q + 3]) * scale);
-        w.z = pack(__uint_as_float(rr[8 * q + 4]) * scale, __uint_as_float(rr[8 * q + 5]) * scale);
-        w.w = pack(__uint_as_float(rr[8 * q + 6]) * scale, __uint_as_float(rr[8 * q + 7]) * scale);
-        *reinterpret_cast<uint4*>(out + c * 32 + 8 * q) = w;
-      }
-    }
-  } else if (warp >= 8) {
-    const int r = (warp - 8) * 32 + lane;  // d row of dQ^T; key row for dV
-    const uint32_t lb = ((uint32_t)((warp & 3) * 32)) << 16;
-    for (int i = 0; i < nq; ++i) {
-      const int buf = i & 1;
-      bar_wait(&sm.dq_full[buf], (i >> 1) & 1);
-      if (r == 0) GS_TR(5, i);
-      fence_after();
-      uint32_t rr[kBQb];
-      tld32(tmem + lb + buf * 128, *reinterpret_cast<uint32_t(*)[32]>(rr));
-      tld32(tmem + lb + buf * 128 + 32, *reinterpret_cast<uint32_t(*)[32]>(rr + 32));
-      tld_wait();
-      fence_before();
-      bar_arrive(&sm.dq_empty[buf]);  // TMEM buffer free for S/dP(i+2)
-      if (r == 0) GS_TR(6, i);
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        if (r == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
-        asm volatile("bar.sync 3, 128;" ::: "memory");
-#pragma unroll
-        for (int q = 0; q < kBQb / 2; ++q) sm.dq_stage[q][r] = __uint_as_float(rr[half * (kBQb / 2) + q]) * scale;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("bar.sync 3, 128;" ::: "memory");
-        if (r == 0) {
-          const int q0 = (qb0 + i) * kBQb + half * (kBQb / 2);
-          asm volatile(
-              "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                  reinterpret_cast<uint64_t>(&map_dq)),
-              "r"(su32(&sm.dq_stage[0][0])), "r"(j * kD), "r"(row0 + q0)
-              : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-      }
-    }
-    if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    bar_wait(&sm.mma_done, 0);
-    fence_after();
-    bf16* out = dqkv + (long long)(row0 + k0 + r) * 3 * h + 2 * h + j * kD;
-#pragma unroll
-    for (int c = 0; c < kD / 32; ++c) {
-      uint32_t rr2[32];
-      tld32(tmem + lb + kDV + c * 32, rr2);
-      tld_wait();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 w;
-        w.x = pack(__uint_as_float(rr2[8 * q]), __uint_as_float(rr2[8 * q + 1]));
-        w.y = pack(__uint_as_float(rr2[8 * q + 2]), __uint_as_float(rr2[8 * q + 3]));
-        w.z = pack(__uint_as_float(rr2[8 * q + 4]), __uint_as_float(rr2[8 * q + 5]));
-        w.w = pack(__uint_as_float(rr2[8 * q + 6]), __uint_as_float(rr2[8 * q + 7]));
-        *reinterpret_cast<uint4*>(out + c * 32 + 8 * q) = w;
-      }
-    }
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  }
-}
-
 // ---------------------------------------------------------- backward v4
 // v3 with P^T kept in tensor memory: the softmax warps tcgen05.st P^T (bf16
 // pairs) over the dP^T half they have just read, and dV += P^T dO runs as a
@@ -1310,12 +780,11 @@ EncodeFn encoder() {
 
 }  // namespace
 
+// The tcgen05 path: bf16, head_dim 128, s a multiple of the forward's two
+// 128-query tiles (every BASELINE geometry); anything else runs the generic
+// SIMT kernels (attention.cu), which also serve the fp32 parity mode.
 bool attention_tc_supported(DType dt, int s, int h, int H) {
-  static const bool off = [] {
-    const char* e = getenv("GS_ATTN_TC");
-    return e && atoi(e) == 0;
-  }();
-  return !off && dt == DType::BF16 && h / H == kD && h % H == 0 && s % kBQ == 0 && encoder() != nullptr;
+  return dt == DType::BF16 && h % H == 0 && h / H == kD && s % (2 * kBQ) == 0 && encoder() != nullptr;
 }
 
 
@@ -1370,75 +839,42 @@ static void attn_trace_end(long long* tr, cudaStream_t st, int ncta, int ny,
 }
 
 cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s, int h, int H, cudaStream_t st) {
-  CUtensorMap mq, mkv;
+  if (!attention_tc_supported(DType::BF16, s, h, H)) return cudaErrorInvalidValue;
+  CUtensorMap mq;  // Q / K / V columns of qkv, 64-column x 128-row boxes
   const cuuint64_t dims[2] = {(cuuint64_t)3 * h, (cuuint64_t)b * s};
   const cuuint64_t strides[1] = {(cuuint64_t)3 * h * 2};
   const cuuint32_t elem[2] = {1, 1};
-  for (int rows : {128, 64}) {
-    const cuuint32_t box[2] = {64, (cuuint32_t)rows};
-    if (encoder()(rows == 128 ? &mq : &mkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims,
-                  strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+  {
+    const cuuint32_t box[2] = {64, 128};
+    if (encoder()(&mq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims, strides, box, elem,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  static const int fwd_variant = [] {  // GS_ATTN_FWD=2 keeps the 64-key two-CTA kernel
-    const char* e = getenv("GS_ATTN_FWD");
-    return e ? atoi(e) : 3;
-  }();
-  if (fwd_variant == 3 && s % (2 * kBQ) == 0) {
-    const int smem3 = (int)sizeof(FaSmem3);
-    static const int poly3 = [] {
-      const char* e = getenv("GS_ATTN_POLY");
-      return e ? atoi(e) : 0;
-    }();
-    auto kern3 = poly3 == 2 ? fa_fwd_tc3_kernel<2> : poly3 == 1 ? fa_fwd_tc3_kernel<1> : fa_fwd_tc3_kernel<0>;
-    static bool init3 = false;
-    if (!init3) {
-      for (auto k : {fa_fwd_tc3_kernel<0>, fa_fwd_tc3_kernel<1>, fa_fwd_tc3_kernel<2>}) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
-        if (e != cudaSuccess) return e;
-      }
-      init3 = true;
-    }
-    count_launch();
-    const int ny = s / (2 * kBQ);
-    long long* tr = attn_trace_begin(st, b * H * ny);
-    CUtensorMap mo;  // o, bf16, 64-column x 128-row boxes (TMA stores of O)
-    {
-      const cuuint64_t dims[2] = {(cuuint64_t)h, (cuuint64_t)b * s};
-      const cuuint64_t strides[1] = {(cuuint64_t)h * 2};
-      const cuuint32_t box[2] = {64, 128};
-      if (encoder()(&mo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, o, dims, strides, box, elem,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return cudaErrorInvalidValue;
-    }
-    cudaError_t le = launch_pdl(kern3, dim3(b * H, ny), dim3(kThreadsF3), smem3, st, mq, mo, (bf16*)o, lse, s, h, H,
-                                1.4426950408889634f / sqrtf((float)kD), tr);
-    if (le != cudaSuccess) return le;
-    attn_trace_end(tr, st, b * H * ny, ny, "(v3: grid schedule only)", 0);
-    return cudaGetLastError();
-  }
-  const int smem = (int)sizeof(FaSmem2);
-  static const int poly = [] {  // GS_ATTN_POLY=1: FMA-pipe exp2 for 1 in 4 elements
-    const char* e = getenv("GS_ATTN_POLY");
-    return e ? atoi(e) : 0;
-  }();
-  auto kern = poly ? fa_fwd_tc2_kernel<1> : fa_fwd_tc2_kernel<0>;
-  static bool init2 = false;
-  if (!init2) {
-    for (auto k : {fa_fwd_tc2_kernel<0>, fa_fwd_tc2_kernel<1>}) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-    }
-    init2 = true;
+  const int smem3 = (int)sizeof(FaSmem3);
+  static bool init3 = false;
+  if (!init3) {
+    cudaError_t e = cudaFuncSetAttribute(fa_fwd_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+    if (e != cudaSuccess) return e;
+    init3 = true;
   }
   count_launch();
-  long long* tr = attn_trace_begin(st, b * H * (s / kBQ));
-  kern<<<dim3(b * H, s / kBQ), 256, smem, st>>>(mq, mkv, (bf16*)o, lse, s, h, H,
-                                                             1.4426950408889634f / sqrtf((float)kD), tr);
-  attn_trace_end(tr, st, b * H * (s / kBQ), s / kBQ,
-                 "0 mma_S_issue 1 mma_P_seen 2 sm_S_seen 3 sm_math 4 sm_P_pub 5 prod_K 6 prod_V 7 mma_S_enter", 5);
+  const int ny = s / (2 * kBQ);
+  long long* tr = attn_trace_begin(st, b * H * ny);
+  CUtensorMap mo;  // o, bf16, 64-column x 128-row boxes (TMA stores of O)
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)h, (cuuint64_t)b * s};
+    const cuuint64_t strides[1] = {(cuuint64_t)h * 2};
+    const cuuint32_t box[2] = {64, 128};
+    if (encoder()(&mo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, o, dims, strides, box, elem,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  cudaError_t le = launch_pdl(fa_fwd_tc3_kernel, dim3(b * H, ny), dim3(kThreadsF3), smem3, st, mq, mo, (bf16*)o, lse,
+                              s, h, H, 1.4426950408889634f / sqrtf((float)kD), tr);
+  if (le != cudaSuccess) return le;
+  attn_trace_end(tr, st, b * H * ny, ny, "(v3: grid schedule only)", 0);
   return cudaGetLastError();
 }
 
@@ -1467,21 +903,17 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  static const int variant = [] {  // GS_ATTN_BWD=3: v3 (P^T in smem, 3-slot ring); default 4
-    const char* e = getenv("GS_ATTN_BWD");
-    return e ? atoi(e) : 4;
-  }();
   CUtensorMap mdq;
   {
     const cuuint64_t dims[2] = {(cuuint64_t)h, (cuuint64_t)b * s};
     const cuuint64_t strides[1] = {(cuuint64_t)h * 4};
-    const cuuint32_t box[2] = {128, (cuuint32_t)(variant == 4 ? kDqRows4 : kBQb / 2)};
+    const cuuint32_t box[2] = {128, (cuuint32_t)kDqRows4};
     if (encoder()(&mdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq_acc, dims, strides, box, elem,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  if (variant == 4) {
+  {
     const int smem4 = (int)sizeof(FaBwdSmem4);
     static bool init4 = false;
     if (!init4) {
@@ -1507,23 +939,6 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
     attn_trace_end(tr, st, b * H * (s / kBK), s / kBK);
     return cudaGetLastError();
   }
-  if (variant == 3) {
-    const int smem3 = (int)sizeof(FaBwdSmem3);
-    static bool init3 = false;
-    if (!init3) {
-      cudaError_t e = cudaFuncSetAttribute(fa_bwd_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
-      if (e != cudaSuccess) return e;
-      init3 = true;
-    }
-    count_launch();
-    long long* tr = attn_trace_begin(st, 0);
-    // v3 takes the log2-domain lse (lse2 = lse * log2 e, from fa_prep)
-    fa_bwd_tc3_kernel<<<dim3(b * H, s / kBK), kThreadsBwd, smem3, st>>>(mq, mq64, md, mdq, lse2, D, (bf16*)dqkv, s,
-                                                                          h, H, 1.0f / sqrtf((float)kD), tr);
-    attn_trace_end(tr, st, 0, 1);
-    return cudaGetLastError();
-  }
-  return cudaErrorInvalidValue;  // GS_ATTN_BWD must be 3 or 4
 }
 
 }  // namespace gs

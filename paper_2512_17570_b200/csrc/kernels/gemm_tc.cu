@@ -638,27 +638,17 @@ SkSlot* sk_slot(cudaStream_t s) {
   return k;
 }
 
-// GS_GEMM_SK=1 enables stream-K tail balancing (read per launch so tests can
-// toggle it).  Off by default: measured at GPT-1.3B shapes it loses 7-12%
-// (partial-tile traffic and owner fix-up outweigh the recovered tail wave).
-int sk_mode() {
-  const char* e = getenv("GS_GEMM_SK");
-  return e ? atoi(e) : 0;
-}
-
 // Number of stream-K tiles for `tiles` output tiles on `units` persistent
-// units with kt k-blocks each: the partial last wave (or a grid with fewer
-// tiles than units) is spread over all units when that recovers > 4% and
-// every unit gets >= 4 k-blocks.
+// units with kt k-blocks each.  Only launches that would leave more than
+// half of the units idle (fewer tiles than units / 2: small-M or small-N
+// GEMMs with long K) are split: for a multi-wave launch's partial tail the
+// partial-tile traffic and owner fix-up cost more than the recovered wave
+// (measured 7-12% slower at the GPT-1.3B shapes).  Every unit gets >= 4
+// k-blocks.
 int sk_tiles(int tiles, int units, int kt) {
-  if (!sk_mode() || units <= 1) return 0;
-  const int rem = tiles % units;
-  if (rem == 0) return 0;
-  const double waves = (double)tiles / units;
-  const double eff = waves / std::ceil(waves);
-  if (eff > 0.96) return 0;
-  if ((long long)rem * kt < 4LL * units) return 0;
-  return rem;
+  if (units <= 1 || 2 * tiles >= units) return 0;
+  if ((long long)tiles * kt < 4LL * units) return 0;
+  return tiles;
 }
 
 // Output tensor [M][ldc] (N columns used) for the epilogue's 32 x 32 TMA
@@ -755,14 +745,6 @@ cudaError_t launch_bn(const GemmArgs& g, cudaStream_t s) {
   return launch_epi<BN, true, false, CG>(g, s);
 }
 
-int pair_mode() {  // GS_GEMM_PAIR=0 forces the single-CTA kernel (A/B tests)
-  static int v = [] {
-    const char* e = getenv("GS_GEMM_PAIR");
-    return e ? atoi(e) : 1;
-  }();
-  return v;
-}
-
 }  // namespace
 
 bool gemm_tc_supported(const GemmArgs& g) {
@@ -780,14 +762,13 @@ bool gemm_tc_supported(const GemmArgs& g) {
 
 cudaError_t gemm_tc(const GemmArgs& g, cudaStream_t s) {
   if (!gemm_tc_supported(g)) return cudaErrorInvalidValue;
-  // Pair tiles 256 x 256 whenever N allows (measured: smaller N tiles lose
-  // more per-tile efficiency than they win back in wave quantisation).
-  if (pair_mode()) {  // M % 128 == 0 (supported): a half-empty last pair tile is fine
-    if (g.N % 256 == 0) return launch_bn<256, 2>(g, s);
-    if (g.N % 192 == 0 && g.b_kmajor) return launch_bn<192, 2>(g, s);
-    if (g.N % 128 == 0) return launch_bn<128, 2>(g, s);
-  }
-  return (g.N % 256 == 0) ? launch_bn<256, 1>(g, s) : launch_bn<128, 1>(g, s);
+  // CTA-pair (cta_group::2) tiles, 256 x 256 whenever N allows (measured:
+  // smaller N tiles lose more per-tile efficiency than they win back in wave
+  // quantisation).  M % 128 == 0 (supported): a half-empty last pair tile is
+  // fine.
+  if (g.N % 256 == 0) return launch_bn<256, 2>(g, s);
+  if (g.N % 192 == 0 && g.b_kmajor) return launch_bn<192, 2>(g, s);
+  return launch_bn<128, 2>(g, s);
 }
 
 }  // namespace gs

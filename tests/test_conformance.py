@@ -30,9 +30,16 @@ def test_reference_suite(built, suite, lib):
 
 
 @requires_reference
-def test_reference_acceptance_binary():
-    exe = os.path.join(ROOT, "oracle", "_ref", "acceptance")
+@pytest.mark.parametrize("lib", ["gs", "ref"])
+def test_reference_acceptance_binary(built, lib):
+    """The reference's acceptance criteria c1-c10 (proj/tests/acceptance.cpp:
+    plan == ledger, memory caps, roofline containment, full-SSD plateau, the
+    demo's vertical/horizontal ratio, ...) against this repo's library (gs)
+    and the reference's own (ref)."""
+    exe = os.path.join(built, "gs", "acceptance") if lib == "gs" else os.path.join(ROOT, "oracle", "_ref", "acceptance")
     if not os.path.exists(exe):
-        pytest.skip("oracle/_ref not built")
+        pytest.skip(f"{exe} not built")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0 and "all criteria passed" in r.stdout
+    assert r.returncode == 0 and "all criteria passed" in r.stdout, r.stdout[-3000:]
+    for c in range(1, 11):
+        assert f"PASS criterion {c:2d}:" in r.stdout

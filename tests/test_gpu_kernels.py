@@ -44,21 +44,14 @@ def rel(a, b):
 
 SHAPES = [(128, 128, 64), (256, 384, 128), (512, 256, 320), (512, 768, 256), (256, 640, 128), (1024, 2048, 512),
           (4096, 6144, 2048),
-          # stream-K tails: 128 pair tiles on 74 pairs; fewer tiles than pairs
-          # (every unit a piece); 2 tiles split ~37 ways; single-CTA tiles
+          # multi-wave with a partial tail (data-parallel); 64 tiles on 74 pair
+          # units (data-parallel); stream-K: 2 tiles split ~37 ways, 8 tiles
           (4096, 2048, 8192), (2048, 2048, 4096), (256, 512, 16384), (384, 1024, 4096)]
-
-
-@pytest.fixture(params=["0", "1"], ids=["dp", "stream_k"])
-def stream_k(request, monkeypatch):
-    """Runs a GEMM test with stream-K tail balancing off and on."""
-    monkeypatch.setenv("GS_GEMM_SK", request.param)
-    return request.param
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
 @pytest.mark.parametrize("a_k,b_k", [(True, True), (True, False), (False, False), (False, True)])
-def test_tcgen05_gemm_matches_fp32_reference(M, N, K, a_k, b_k, stream_k):
+def test_tcgen05_gemm_matches_fp32_reference(M, N, K, a_k, b_k):
     d = dev()
     torch.manual_seed(M + N + K)
     Am = torch.randn(M, K, device=d).bfloat16()
@@ -82,8 +75,9 @@ def test_tcgen05_gemm_matches_fp32_reference(M, N, K, a_k, b_k, stream_k):
 
 
 @pytest.mark.parametrize("M,N,K", [(4096, 2048, 8192), (256, 512, 16384)])
-def test_tcgen05_stream_k_is_deterministic(M, N, K, monkeypatch):
-    monkeypatch.setenv("GS_GEMM_SK", "1")
+def test_tcgen05_stream_k_is_deterministic(M, N, K):
+    """(256, 512, 16384) has 2 pair tiles for 74 pair units: stream-K splits
+    their k-blocks over every unit; fixed-order partial sums are bit-stable."""
     d = dev()
     torch.manual_seed(1)
     A = torch.randn(M, K, device=d).bfloat16()
@@ -163,7 +157,7 @@ def attn_reference(qkv, b, s, h, H):
                                                (BF16, 2, 32, 64, 4, 0.5),
                                                # large scores: the running max jumps by >2^8 (lazy O rescale path)
                                                (BF16, 1, 1024, 512, 4, 2.5), (BF16, 2, 512, 256, 2, "ramp"),
-                                               # s % 256 == 128: the 64-key two-CTA forward (v2)
+                                               # s % 256 == 128: the generic SIMT kernels in bf16
                                                (BF16, 2, 384, 512, 4, 0.5), (BF16, 1, 640, 256, 2, 2.5)])
 def test_attention_fwd_bwd(dtype, b, s, h, H, amp):
     d = dev()
@@ -330,15 +324,12 @@ def test_context_stream_runs_kernels():
     assert rel(out.float(), A.float() @ B.float().t()) < 5e-3
 
 
-@pytest.mark.parametrize("fwd_variant", ["3", "2"])
-def test_attention_bit_repeatable_over_many_launches(fwd_variant):
+def test_attention_bit_repeatable_over_many_launches():
     """Pipeline races (an mbarrier parity wait aliasing a phase, a TMEM buffer
     reused early) show up rarely and only at scale: 60 forward + backward
-    launches at the GPT-1.3B shape must all reproduce the first bit for bit.
-    s = 1920 (s % 256 == 128) selects the v2 forward."""
+    launches at the GPT-1.3B shape must all reproduce the first bit for bit."""
     d = dev()
-    b, h, H = 2, 2048, 16
-    s = 2048 if fwd_variant == "3" else 1920
+    b, h, H, s = 2, 2048, 16, 2048
     lib = gs.lib()
     torch.manual_seed(7)
     qkv = (torch.randn(b * s, 3 * h, device=d) * 0.5).bfloat16()
