@@ -367,16 +367,16 @@ def run_ours(args):
     else:
         plan = gs.build_vertical(model, M, gs.StorageSplit(*split), alpha)
     nvme = os.environ.get("GS_NVME_DIR", "/tmp")
-    nccl_id = None
-    if world > 1:  # rank 0's NCCL unique id, shared through the torch process group
+    comm_id = None
+    if world > 1:  # rank 0 draws the peer-memory communicator id; the torch process group broadcasts it
         idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(gs.nccl_unique_id()), dtype=torch.uint8))
+            idt.copy_(torch.frombuffer(bytearray(gs.comm_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().numpy().tobytes())
+        comm_id = bytes(idt.cpu().numpy().tobytes())
     eng = gs.Engine(plan, model, V, gs.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0), seed=1234,
                     device=torch.cuda.current_device(), nvme_dir=nvme, opt_tier=tier, profile=True, rank=rank,
-                    world=world, nccl_id=nccl_id, ssd_ring_layers=ring)
+                    world=world, comm_id=comm_id, ssd_ring_layers=ring)
     K, W = args.steps, args.warmup
     tokens = make_tokens(V, W + 2 * K, M, b, s, seed=7 + rank)
     # warm-up (untimed)

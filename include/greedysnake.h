@@ -137,14 +137,15 @@ typedef struct gs_engine_config {
   int record_trace;
   int profile_kernels;     /* CUDA-event timing per kernel class (gs_engine_kernel_profile) */
   int rank, world;         /* ZeRO-3 data parallelism: model.data_parallel_degree == world */
-  const uint8_t* nccl_id;  /* 128-byte ncclUniqueId from gs_nccl_unique_id() on rank 0 (world > 1) */
+  const uint8_t* comm_id;  /* 128-byte job id from gs_comm_unique_id() on rank 0 (world > 1): peer-memory rendezvous */
   int force_collectives;   /* run the sharded / NCCL path even at world == 1 */
   int ssd_ring_layers;     /* pinned staging slots per SSD-resident data kind (0 -> 8) */
   int host_threads;        /* opt_tier 3: host optimizer threads (0 -> hardware threads - 4) */
 } gs_engine_config;
 
-/* ncclGetUniqueId() for rank 0 of a data-parallel job */
-int gs_nccl_unique_id(uint8_t out[128]);
+/* 128 random bytes naming a data-parallel job's peer-memory communicator
+   (rank 0 draws them; every rank passes the same bytes as comm_id) */
+int gs_comm_unique_id(uint8_t out[128]);
 
 typedef struct gs_run_report {
   double total_ms;          /* CUDA-event time of the whole run */

@@ -59,9 +59,11 @@ struct ExecConfig {
   bool record_trace = false;   // per-task timestamps (adds event records)
   bool profile_kernels = false;  // CUDA-event timing per kernel class on the compute stream
   // ZeRO-3 data parallelism: one executor per rank, model.data_parallel_degree
-  // == world; rank 0's ncclUniqueId (128 bytes) shared out of band.
+  // == world; the job's 128-byte communicator id (rank 0 draws it with
+  // gs_comm_unique_id, the launcher broadcasts it) names the one-node
+  // peer-memory rendezvous (engine/peer_comm.hpp).
   int rank = 0, world = 1;
-  std::vector<uint8_t> nccl_id;
+  std::vector<uint8_t> comm_id;
   bool force_collectives = false;  // run the sharded code path even at world == 1 (tests)
   // SSD-resident bytes have no permanent DRAM copy: each data kind stages
   // them through a ring of this many per-layer pinned slots (slot = layer %

@@ -90,7 +90,7 @@ class _EngineConfig(C.Structure):
                 ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float), ("seed", C.c_uint64),
                 ("device", C.c_int), ("nvme_dir", C.c_char_p), ("odirect", C.c_int), ("opt_tier", C.c_int),
                 ("record_trace", C.c_int), ("profile_kernels", C.c_int), ("rank", C.c_int), ("world", C.c_int),
-                ("nccl_id", C.c_void_p), ("force_collectives", C.c_int), ("ssd_ring_layers", C.c_int),
+                ("comm_id", C.c_void_p), ("force_collectives", C.c_int), ("ssd_ring_layers", C.c_int),
                 ("host_threads", C.c_int)]
 
 
@@ -311,10 +311,11 @@ def overlap_window(plan: SchedulePlan) -> int:
     return int(lib().gs_plan_overlap_window(plan.handle))
 
 
-def nccl_unique_id() -> bytes:
-    """ncclGetUniqueId() (rank 0 of a data-parallel job)."""
+def comm_unique_id() -> bytes:
+    """128 random bytes naming a data-parallel job's peer-memory communicator
+    (rank 0 draws them, every rank passes them as Engine(comm_id=...))."""
     buf = (C.c_uint8 * 128)()
-    check(lib().gs_nccl_unique_id(buf))
+    check(lib().gs_comm_unique_id(buf))
     return bytes(buf)
 
 
@@ -475,14 +476,14 @@ class Engine:
     def __init__(self, plan: SchedulePlan, model: ModelSpec, vocab_size: int, adam: AdamConfig = AdamConfig(),
                  seed: int = 42, device: int = 0, nvme_dir: str = "/tmp", odirect: bool = True, opt_tier: int = 0,
                  record_trace: bool = False, profile: bool = False, rank: int = 0, world: int = 1,
-                 nccl_id: bytes | None = None, force_collectives: bool = False, ssd_ring_layers: int = 0,
+                 comm_id: bytes | None = None, force_collectives: bool = False, ssd_ring_layers: int = 0,
                  host_threads: int = 0):
         self.model = model
         self.vocab_size = vocab_size
         self.plan = plan
         self.microbatches = plan.info()["microbatches"]
         self._nvme = nvme_dir.encode()
-        self._id = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+        self._id = C.create_string_buffer(bytes(comm_id), 128) if comm_id is not None else None
         cfg = _EngineConfig(model._c(), vocab_size, adam.lr, adam.beta1, adam.beta2, adam.eps, adam.weight_decay,
                             seed, device, self._nvme, int(odirect), opt_tier, int(record_trace), int(profile),
                             rank, world, C.cast(self._id, C.c_void_p) if self._id is not None else None,

@@ -3,7 +3,6 @@
 // convention, proj/tools/offsim_main.cpp:400-409) and keeps the last error
 // message per thread.
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -21,6 +20,7 @@
 #include "host_tiers.hpp"
 #include "kernels.h"
 #include "layer_ops.hpp"
+#include "peer_comm.hpp"
 #include "offsim/executor.hpp"
 #include "offsim/json_io.hpp"
 
@@ -294,7 +294,7 @@ int gs_engine_create(const gs_plan* plan, const gs_engine_config* c, gs_engine**
     cfg.profile_kernels = c->profile_kernels != 0;
     cfg.rank = c->rank;
     cfg.world = c->world > 0 ? c->world : 1;
-    if (c->nccl_id) cfg.nccl_id.assign(c->nccl_id, c->nccl_id + 128);
+    if (c->comm_id) cfg.comm_id.assign(c->comm_id, c->comm_id + 128);
     cfg.force_collectives = c->force_collectives != 0;
     if (c->ssd_ring_layers > 0) cfg.ssd_ring_layers = c->ssd_ring_layers;
     if (c->host_threads > 0) cfg.host_threads = c->host_threads;
@@ -627,15 +627,12 @@ int gs_layer_bench(int dtype, int b, int s, int h, int heads, int iters, double 
   });
 }
 
-int gs_nccl_unique_id(uint8_t out[128]) {
-  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
-  ncclUniqueId id;
-  if (ncclGetUniqueId(&id) != ncclSuccess) {
-    g_error = "NCCL: ncclGetUniqueId failed";
-    return GS_ERR_RUNTIME;
-  }
-  std::memcpy(out, &id, sizeof(id));
-  return GS_OK;
+int gs_comm_unique_id(uint8_t out[128]) {
+  return guarded([&] {
+    if (!out) throw offsim::ValidationError("comm_unique_id: out required");
+    const std::vector<uint8_t> id = gs::engine::peer_comm_unique_id();
+    std::memcpy(out, id.data(), id.size());
+  });
 }
 
 }  // extern "C"

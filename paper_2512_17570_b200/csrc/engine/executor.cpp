@@ -25,7 +25,6 @@
 #include "offsim/executor.hpp"
 
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -45,6 +44,7 @@
 #include "host_tiers.hpp"
 #include "kernels.h"
 #include "layer_ops.hpp"
+#include "peer_comm.hpp"
 
 namespace offsim {
 
@@ -142,8 +142,26 @@ struct Executor::Impl {
   int W = 1, R = 0;
   u64 Ps = 0, e_lo = 0, e_hi = 0, n_my = 0, loc_now = 0, loc_late = 0;
   bool dp = false;
-  ncclComm_t comm = nullptr;
   std::vector<float*> grad_shard;  // [ring] reduce-scatter output (aliases grad_slot when !dp)
+  // Collectives over peer memory (engine/peer_comm.hpp).  Parameter
+  // all-gather, pipelined per H2D chunk: each landed chunk of this rank's
+  // shard is announced (kParamReady) on s_h2d, and s_ag copies the peers'
+  // same chunk out of their HBM into the gathered layer buffer.  Gradient
+  // reduce-scatter after a layer's last backward micro-batch on s_rs (off
+  // the compute stream: it overlaps the next stage).  Counters are running
+  // sequence numbers identical on every rank (same plan, same order).
+  std::unique_ptr<PeerComm> peer;
+  int pb_param[2] = {-1, -1}, pb_fx_grad = -1, pb_fx_red = -1;
+  std::vector<int> pb_grad;
+  cudaStream_t s_ag = nullptr, s_rs = nullptr;
+  cudaEvent_t ev_ag[2] = {nullptr, nullptr}, ev_h2d_chunk = nullptr, ev_bwd_done = nullptr;
+  std::vector<cudaEvent_t> ev_rs;   // [grad_ring] shard of slot k reduced
+  uint32_t param_q = 0, grad_q = 0, fixed_q = 0;
+  uint32_t param_last[2] = {0, 0};  // last chunk sequence gathered into dev_param[p]
+  std::vector<uint32_t> grad_last;  // [grad_ring] last reduce-scatter sequence that read slot k
+  float* fx_red = nullptr;          // this rank's shard of the summed embedding gradient
+  long long fx_shard = 0;           // ceil(n_fixed / W)
+  void fixed_allreduce(cudaStream_t st);
 
   // streams
   cudaStream_t s_gpu = nullptr, s_h2d = nullptr, s_d2h = nullptr, s_opt = nullptr;
@@ -349,12 +367,10 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   loc_now = el_now > e_lo ? std::min<u64>(el_now - e_lo, n_my) : 0;
   loc_late = n_my - loc_now;
   if (dp) {
-    if (cfg.nccl_id.size() != sizeof(ncclUniqueId))
-      throw ValidationError("executor: data-parallel run needs the 128-byte NCCL unique id of rank 0");
-    ncclUniqueId id;
-    std::memcpy(&id, cfg.nccl_id.data(), sizeof(id));
-    cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice");
-    if (ncclCommInitRank(&comm, W, id, R) != ncclSuccess) throw std::runtime_error("NCCL: ncclCommInitRank failed");
+    if (cfg.comm_id.size() != 128)
+      throw ValidationError("executor: data-parallel run needs the job's 128-byte communicator id (rank 0 draws it)");
+    if (W > 8) throw ValidationError("executor: peer-memory data parallelism covers one node (world <= 8)");
+    peer = std::make_unique<PeerComm>(R, W, cfg.comm_id, cfg.device);
   }
 
   cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice");
@@ -420,6 +436,22 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   fx_v = static_cast<float*>(dmalloc(4 * n_fixed));
   fx_grad = static_cast<float*>(dmalloc(4 * n_fixed));
   fx_lp = dmalloc(static_cast<u64>(n_fixed) * d.lp());
+  if (dp) {
+    fx_shard = (n_fixed + W - 1) / W;
+    fx_red = static_cast<float*>(dmalloc(4 * static_cast<u64>(fx_shard)));
+    for (int i = 0; i < 2; ++i) pb_param[i] = peer->add(dev_param[i]);
+    for (float* g : grad_slot) pb_grad.push_back(peer->add(g));
+    pb_fx_grad = peer->add(fx_grad);
+    pb_fx_red = peer->add(fx_red);
+    peer->connect();
+    cuda_check(cudaStreamCreateWithPriority(&s_ag, cudaStreamNonBlocking, prio_hi), "stream");
+    cuda_check(cudaStreamCreateWithPriority(&s_rs, cudaStreamNonBlocking, prio_hi), "stream");
+    for (cudaEvent_t* e : {&ev_ag[0], &ev_ag[1], &ev_h2d_chunk, &ev_bwd_done})
+      cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    ev_rs.assign(static_cast<size_t>(grad_ring), nullptr);
+    for (auto& e : ev_rs) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    grad_last.assign(static_cast<size_t>(grad_ring), 0);
+  }
   if (!alloc_workspace(d, ws)) throw InfeasibleError("executor: device workspace allocation failed");
   if (cfg.profile_kernels) ws.prof = &prof;
   dev_bytes += ws.bytes;
@@ -518,7 +550,13 @@ Executor::Impl::~Impl() {
   for (cudaEvent_t e : {ev_opt_begin, ev_opt_end})
     if (e) cudaEventDestroy(e);
   free_workspace(ws);
-  if (comm) ncclCommDestroy(comm);
+  peer.reset();
+  for (cudaEvent_t e : {ev_ag[0], ev_ag[1], ev_h2d_chunk, ev_bwd_done})
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_rs)
+    if (e) cudaEventDestroy(e);
+  for (cudaStream_t s : {s_ag, s_rs})
+    if (s) cudaStreamDestroy(s);
   for (void* p : dev_allocs) cudaFree(p);
   for (cudaStream_t s : {s_gpu, s_h2d, s_d2h, s_opt, s_opt_up, s_opt_dn})
     if (s) cudaStreamDestroy(s);
@@ -1079,9 +1117,10 @@ void Executor::Impl::compute_task(const Task& t, int it) {
     lc.n += 1;
     cuda_check(cudaMemsetAsync(dev_loss + it, 0, sizeof(double), s_gpu), "loss");
     if (fixed_done < git) {  // embedding / head step with the previous iteration's grads
-      if (dp && ncclAllReduce(fx_grad, fx_grad, static_cast<size_t>(n_fixed), ncclFloat, ncclSum, comm, s_gpu) !=
-                    ncclSuccess)
-        throw std::runtime_error("NCCL: all-reduce of the embedding gradient failed");
+      if (dp) {
+        fixed_allreduce(s_gpu);
+        lc.n += 5;  // four counter signals + the sum
+      }
       gs::AdamHyper hp{cfg.adam.lr, cfg.adam.beta1, cfg.adam.beta2, cfg.adam.eps, cfg.adam.weight_decay};
       cuda_check(gs::adam_step(hp, static_cast<int>(git), 1.0f, fx_master, fx_m, fx_v, fx_grad, fx_lp, d.dt, n_fixed,
                                s_gpu),
@@ -1098,13 +1137,10 @@ void Executor::Impl::compute_task(const Task& t, int it) {
   const long long tok_n = 1LL * d.b * (d.s + 1);
   const int32_t* tok = dev_tok[slot] + m * tok_n;
   const void* Wt = dev_param[par];
-  if (dp && (horizontal || m == first_mb(st))) {
-    // first compute of the stage: gather the layer from the per-rank shards
-    // (in place: this rank's H2D chunks already sit at offset R * shard)
-    const u64 sb = static_cast<u64>(d.lp()) * Ps;
-    if (ncclAllGather(static_cast<uint8_t*>(dev_param[par]) + sb * R, dev_param[par], sb, ncclUint8, comm, s_gpu) !=
-        ncclSuccess)
-      throw std::runtime_error("NCCL: all-gather of the layer parameters failed");
+  if (dp && m == first_mb(st)) {
+    // first compute of the stage: the peers' shards of the layer were copied
+    // chunk by chunk on s_ag as they landed (xfer_task, Param H2D)
+    cuda_check(cudaStreamWaitEvent(s_gpu, ev_ag[par], 0), "gather wait");
   }
   const void* wte = fx_lp;
   const void* wpe = static_cast<const uint8_t*>(fx_lp) + 1LL * d.V * d.h * d.lp();
@@ -1162,12 +1198,27 @@ void Executor::Impl::compute_task(const Task& t, int it) {
   bool first;
   if (horizontal) first = (m == 0);  // later MBs accumulate onto the fetched partial sum
   else first = (m == first_mb(st));
+  if (dp && first) {
+    // the slot's previous layer partial must have been read by every peer
+    peer->wait(s_gpu, PeerComm::kGradRead, grad_last[static_cast<size_t>(l % grad_ring)]);
+  }
   cuda_check(layer_backward(d, Wt, x, dy, dx, gslot, first, hp, ws, s_gpu, lc), "layer_backward");
   if (dp && !horizontal && m == last_mb(st)) {
-    // full-layer fp32 gradient of this rank's micro-batches -> summed shard
-    if (ncclReduceScatter(gslot, grad_shard[static_cast<size_t>(l % grad_ring)], Ps, ncclFloat, ncclSum, comm, s_gpu) !=
-        ncclSuccess)
-      throw std::runtime_error("NCCL: reduce-scatter of the layer gradient failed");
+    // full-layer fp32 gradient of this rank's micro-batches -> summed shard,
+    // on s_rs: the next stage's compute does not wait for it
+    const size_t k = static_cast<size_t>(l % grad_ring);
+    cuda_check(cudaEventRecord(ev_bwd_done, s_gpu), "record");
+    cuda_check(cudaStreamWaitEvent(s_rs, ev_bwd_done, 0), "wait");
+    const uint32_t g = ++grad_q;
+    peer->signal(s_rs, PeerComm::kGradReady, g);
+    peer->wait(s_rs, PeerComm::kGradReady, g);
+    gs::PeerSrcs src{};
+    for (int r = 0; r < W; ++r)
+      src.p[r] = static_cast<const float*>(peer->ptr(pb_grad[k], r)) + static_cast<u64>(R) * Ps;
+    cuda_check(gs::peer_sum(src, W, grad_shard[k], static_cast<long long>(Ps), s_rs), "reduce-scatter");
+    lc.n += 3;  // two counter signals + the sum
+    peer->signal(s_rs, PeerComm::kGradRead, g);
+    grad_last[k] = g;
   }
   if (l == 0) {
     cuda_check(gs::embed_bwd(d.dt, tok, dx, fx_grad, fx_grad + 1LL * d.V * d.h, d.b, d.s, d.h, s_gpu), "embed_bwd");
@@ -1176,10 +1227,12 @@ void Executor::Impl::compute_task(const Task& t, int it) {
   if (!horizontal && m == last_mb(st) && el_late > 0) {
     if (loc_late > 0 && !host_step)
       cuda_check(cudaMemcpyAsync(retain[static_cast<size_t>(l)], grad_shard[static_cast<size_t>(l % grad_ring)] + loc_now,
-                                 4 * loc_late, cudaMemcpyDeviceToDevice, s_gpu),
+                                 4 * loc_late, cudaMemcpyDeviceToDevice, dp ? s_rs : s_gpu),
                  "retain");
     late_ready[static_cast<size_t>(l)].store(git);
   }
+  if (dp && !horizontal && m == last_mb(st))
+    cuda_check(cudaEventRecord(ev_rs[static_cast<size_t>(l % grad_ring)], s_rs), "record");
   launches += lc.n;
 }
 
@@ -1288,6 +1341,39 @@ void Executor::Impl::apply_adam_host(int layer, u64 e0, u64 e1, const float* gra
   }
 }
 
+// Embedding / position gradient all-reduce (FixedOps, flush): reduce-scatter
+// over peer memory into this rank's fx_red shard, then all-gather of the
+// peers' shards back into fx_grad.  The counters order every cross-rank
+// read before the write that would clobber it: fx_red is rewritten only
+// after every peer gathered it (kFixedGathered of the previous round), and
+// fx_grad only after every peer summed out of it (kFixedReduced).
+void Executor::Impl::fixed_allreduce(cudaStream_t st) {
+  const uint32_t f = ++fixed_q;
+  const long long lo = std::min<long long>(n_fixed, static_cast<long long>(R) * fx_shard);
+  const long long n = std::min<long long>(fx_shard, n_fixed - lo);
+  peer->wait(st, PeerComm::kFixedGathered, f - 1);
+  peer->signal(st, PeerComm::kFixedReady, f);
+  peer->wait(st, PeerComm::kFixedReady, f);
+  gs::PeerSrcs src{};
+  for (int r = 0; r < W; ++r) src.p[r] = static_cast<const float*>(peer->ptr(pb_fx_grad, r)) + lo;
+  cuda_check(gs::peer_sum(src, W, fx_red, n, st), "embedding reduce-scatter");
+  peer->signal(st, PeerComm::kFixedReduced, f);
+  peer->wait(st, PeerComm::kFixedReduced, f);
+  for (int r = 0; r < W; ++r) {
+    if (r == R) {
+      cuda_check(cudaMemcpyAsync(fx_grad + lo, fx_red, 4 * static_cast<u64>(n), cudaMemcpyDeviceToDevice, st), "gather");
+      continue;
+    }
+    const long long rlo = std::min<long long>(n_fixed, static_cast<long long>(r) * fx_shard);
+    const long long rn = std::min<long long>(fx_shard, n_fixed - rlo);
+    if (rn > 0)
+      cuda_check(cudaMemcpyAsync(fx_grad + rlo, peer->ptr(pb_fx_red, r), 4 * static_cast<u64>(rn),
+                                 cudaMemcpyDeviceToDevice, st),
+                 "embedding gather");
+  }
+  peer->signal(st, PeerComm::kFixedGathered, f);
+}
+
 void Executor::Impl::step_task(const Task& t, int it) {
   const long long git = global_iter + it;
   const int l = t.layer;
@@ -1343,9 +1429,34 @@ void Executor::Impl::xfer_task(const Task& t, int it, u64& phys) {
         const u64 lo = chunk_lo[static_cast<size_t>(t.id)];
         const int use_par = (((st + 1) % 2) + 2) % 2;
         const Src src = fwd ? Src::Auto : Src::ReadStaging;
+        // the peers must have copied this buffer's previous contents (two
+        // stages ago) out of this rank's region before it is overwritten
+        if (dp && lo == 0) peer->wait(s_h2d, PeerComm::kParamRead, param_last[use_par]);
         // this rank's shard lands at its offset of the gathered layer buffer
         phys = upload(b, lo, lo + t.bytes, static_cast<uint8_t*>(dev_param[use_par]) + lp * Ps * R + lo, src, s_h2d,
                       lp * loc_now);
+        if (dp) {
+          // announce the chunk; copy the peers' same chunk once it has landed
+          // there (s_ag follows s_h2d, so it inherits the buffer's local
+          // WAR ordering against the compute that last read it)
+          const uint32_t q = ++param_q;
+          peer->signal(s_h2d, PeerComm::kParamReady, q);
+          cuda_check(cudaEventRecord(ev_h2d_chunk, s_h2d), "record");
+          cuda_check(cudaStreamWaitEvent(s_ag, ev_h2d_chunk, 0), "wait");
+          peer->wait(s_ag, PeerComm::kParamReady, q);
+          for (int r = 0; r < W; ++r) {
+            if (r == R) continue;
+            const u64 off = lp * Ps * static_cast<u64>(r) + lo;
+            cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(dev_param[use_par]) + off,
+                                       static_cast<const uint8_t*>(peer->ptr(pb_param[use_par], r)) + off, t.bytes,
+                                       cudaMemcpyDeviceToDevice, s_ag),
+                       "gather");
+          }
+          peer->signal(s_ag, PeerComm::kParamRead, q);
+          launches += 2;  // the two counter signals
+          cuda_check(cudaEventRecord(ev_ag[use_par], s_ag), "record");
+          param_last[use_par] = q;
+        }
       }
       break;
     }
@@ -1372,6 +1483,8 @@ void Executor::Impl::xfer_task(const Task& t, int it, u64& phys) {
     }
     case DataKind::GradAccum: {
       float* g = grad_shard[static_cast<size_t>(l % grad_ring)];
+      if (dp && t.link == LinkKind::PCIe_D2H)
+        cuda_check(cudaStreamWaitEvent(s_d2h, ev_rs[static_cast<size_t>(l % grad_ring)], 0), "reduce wait");
       if (t.link == LinkKind::PCIe_D2H && host_step) {
         // immediate slice -> the ring slot the step reads, delayed slice ->
         // the layer's retained copy (the next iteration's forward-phase step)
@@ -1600,9 +1713,7 @@ void Executor::flush() {
     I.late_applied[static_cast<size_t>(l)].store(ready);
   }
   if (I.fixed_done < I.global_iter) {
-    if (I.dp && ncclAllReduce(I.fx_grad, I.fx_grad, static_cast<size_t>(I.n_fixed), ncclFloat, ncclSum, I.comm, I.s_opt) !=
-                    ncclSuccess)
-      throw std::runtime_error("NCCL: all-reduce of the embedding gradient failed");
+    if (I.dp) I.fixed_allreduce(I.s_opt);
     gs::AdamHyper hp{I.cfg.adam.lr, I.cfg.adam.beta1, I.cfg.adam.beta2, I.cfg.adam.eps, I.cfg.adam.weight_decay};
     cuda_check(gs::adam_step(hp, static_cast<int>(I.global_iter), 1.0f, I.fx_master, I.fx_m, I.fx_v, I.fx_grad, I.fx_lp,
                              I.d.dt, I.n_fixed, I.s_opt),

@@ -109,4 +109,19 @@ cudaError_t adam_step_packed(const AdamHyper& hp, int step, float grad_scale, fl
 // dst(dt) = src(fp32)
 cudaError_t cast_from_f32(DType dt, const float* src, void* dst, long long n, cudaStream_t s);
 
+// dst[i] = sum over r < world (in rank order) of src.p[r][i]; the sources
+// are peers' buffers mapped through CUDA IPC (kernels/peer.cu)
+constexpr int kMaxPeers = 8;
+struct PeerSrcs {
+  const float* p[kMaxPeers];
+};
+cudaError_t peer_sum(const PeerSrcs& src, int world, float* dst, long long n, cudaStream_t s);
+// cross-rank counters (engine/peer_comm.hpp): release-store `value` into n
+// counters / spin (acquire) until n counters reach `value`
+struct PeerFlags {
+  uint32_t* p[kMaxPeers];
+};
+cudaError_t peer_signal(const PeerFlags& f, int n, uint32_t value, cudaStream_t s);
+cudaError_t peer_wait_spin(const PeerFlags& f, int n, uint32_t value, cudaStream_t s);
+
 }  // namespace gs

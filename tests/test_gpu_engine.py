@@ -202,7 +202,7 @@ def test_fp32_horizontal_engine_matches_oracle(split, tier):
     assert np.array_equal(rep.ledger, gs.plan_traffic(plan))
 
 
-def test_sharded_nccl_path_at_world1_matches_oracle():
+def test_sharded_peer_comm_path_at_world1_matches_oracle():
     """The ZeRO-3 code path (NCCL all-gather of layer shards, reduce-scatter
     of the fp32 gradient, embedding all-reduce, shard-local Adam) forced on at
     world = 1: identical numerics to the oracle."""
@@ -211,7 +211,7 @@ def test_sharded_nccl_path_at_world1_matches_oracle():
     model = gs.ModelSpec(g.n_layers, g.hidden, g.heads, g.seq, g.mb_size, 4, 4, 3, 1)
     plan = gs.build_vertical(model, M, gs.StorageSplit(1, 1, 0), 0.25)
     eng = gs.Engine(plan, model, g.vocab, gs.AdamConfig(**ADAM), seed=42, nvme_dir="/tmp", rank=0, world=1,
-                    nccl_id=gs.nccl_unique_id(), force_collectives=True)
+                    comm_id=gs.comm_unique_id(), force_collectives=True)
     tokens = ob.make_tokens(g, iters, M)
     rep = eng.run(tokens)
     eng.flush()
