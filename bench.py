@@ -152,7 +152,7 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], device="cuda")
+    t = torch.tensor([x], dtype=torch.float64)  # gloo: the timing plumbing, not the data path
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -350,8 +350,17 @@ def run_ours(args):
     rank, world, local = dist_env()
     import torch.distributed as dist
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        # one process per GPU; --share-gpu places every rank on the visible
+        # device(s) round-robin (a functional check of the multi-rank path on
+        # a smaller box: its numbers are not scaling results)
+        ndev = torch.cuda.device_count()
+        if local >= ndev and not args.share_gpu:
+            raise SystemExit(f"bench: rank {rank} needs cuda:{local} but {ndev} GPU(s) are visible (--share-gpu)")
+        torch.cuda.set_device(local % ndev)
+        # gloo carries only the launcher plumbing (id broadcast, barriers,
+        # max-over-ranks timing); the training collectives are the
+        # executor's own peer-memory ones
+        dist.init_process_group("gloo")
     else:
         torch.cuda.set_device(0)
     import paper_2512_17570_b200 as gs
@@ -369,7 +378,7 @@ def run_ours(args):
     nvme = os.environ.get("GS_NVME_DIR", "/tmp")
     comm_id = None
     if world > 1:  # rank 0 draws the peer-memory communicator id; the torch process group broadcasts it
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        idt = torch.zeros(128, dtype=torch.uint8)
         if rank == 0:
             idt.copy_(torch.frombuffer(bytearray(gs.comm_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
@@ -527,6 +536,8 @@ def main():
                     help="horizontal = the micro-batch-major ablation baseline (BASELINE configs[1])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--calibrate", type=int, default=1, help="calibrate offsim::simulate from the trace")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="N > 1 on fewer GPUs: ranks share devices (functional check, not a scaling number)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: re-launch under torch.distributed.run

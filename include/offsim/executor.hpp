@@ -69,7 +69,7 @@ struct ExecConfig {
   // them through a ring of this many per-layer pinned slots (slot = layer %
   // ring); reuse of a slot is ordered by the executor's hazard edges.
   int ssd_ring_layers = 8;
-  int host_threads = 0;  // OptTier::Host worker threads (0: hardware threads - 4, at least 1)
+  int host_threads = 0;  // OptTier::Host worker threads (0: (hardware threads - 4) / world, at least 1)
 };
 
 struct TraceRecord {

@@ -506,7 +506,8 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
     if (loc_late > 0)
       for (int l = 0; l < N; ++l) host_retain[static_cast<size_t>(l)] = reinterpret_cast<float*>(arena.alloc(4 * loc_late));
     const int hw = static_cast<int>(std::thread::hardware_concurrency());
-    host_pool = std::make_unique<ThreadPool>(cfg.host_threads > 0 ? cfg.host_threads : std::max(1, hw - 4), 10);
+    // the node's cores are shared by its W ranks (one process per GPU)
+    host_pool = std::make_unique<ThreadPool>(cfg.host_threads > 0 ? cfg.host_threads : std::max(1, (hw - 4) / W), 10);
   }
   for (int l = 0; l < N; ++l)
     for (int m = 0; m < M; ++m)
