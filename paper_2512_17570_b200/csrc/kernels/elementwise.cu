@@ -110,9 +110,12 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(const T* __restrict
 }
 
 // Vectorised row kernels (h % (16 / sizeof(T)) == 0, the engine's case): a
-// row is owned by a group of nw warps (nw = 1 for h <= 2048 bf16, so the
-// reductions are warp shuffles only), each lane holds C 16-byte vectors of the
-// row as packed storage-type registers, and blocks carry 8 / nw rows.
+// row is owned by a group of nw warps sized so each lane holds at most C = 2
+// 16-byte vectors of every row operand (nw = 4 at h = 2048 bf16, 10 at 5120,
+// 16 at 8192), blocks carry max(1, 8 / nw) rows.  Keeping C small keeps the
+// register footprint at ~40 (full 64-warp occupancy; the earlier one-warp-per-
+// row shape held 8 vectors per operand, 137-174 registers, one CTA per SM and
+// ran latency-bound at 0.33-0.50 of HBM).
 template <typename T> struct Vec;
 template <> struct Vec<float> {
   static constexpr int N = 4;
@@ -141,44 +144,57 @@ template <> struct Vec<__nv_bfloat16> {
   }
 };
 
-// Sum over the nw warps of this thread's row group (uniform nw per launch).
-__device__ __forceinline__ float group_sum(float v, float* red, int nw) {
-  v = warp_sum(v);
+// Sum over the nw warps of this thread's row group (uniform nw per launch);
+// float2 so the backward's two row sums share one pass of barriers.
+__device__ __forceinline__ float2 group_sum2(float2 v, float2* red, int nw) {
+  v.x = warp_sum(v.x);
+  v.y = warp_sum(v.y);
   if (nw == 1) return v;
   const int w = threadIdx.x >> 5, base = (w / nw) * nw;
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[w] = v;
   __syncthreads();
-  float r = 0.0f;
-  for (int i = 0; i < nw; ++i) r += red[base + i];
+  float2 r = make_float2(0.0f, 0.0f);
+  for (int i = 0; i < nw; ++i) {
+    const float2 q = red[base + i];
+    r.x += q.x;
+    r.y += q.y;
+  }
   return r;
 }
 
+constexpr int kVecRowMaxThreads = 512;
+
 template <typename T, int C>
-__global__ void __launch_bounds__(256) ln_fwd_vec_kernel(const T* __restrict__ x, T* __restrict__ y,
-                                                         float* __restrict__ mean, float* __restrict__ rstd,
-                                                         int rows, int h, int nw) {
+__global__ void __launch_bounds__(kVecRowMaxThreads) ln_fwd_vec_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                                       float* __restrict__ mean,
+                                                                       float* __restrict__ rstd, int rows, int h,
+                                                                       int nw) {
   pdl_trigger_and_wait();
   using VT = Vec<T>;
   constexpr int N = VT::N;
-  __shared__ float red[8];
+  __shared__ float2 red[kVecRowMaxThreads / 32];
   const int gt = 32 * nw, t = threadIdx.x % gt;
   const long long row = (long long)blockIdx.x * (blockDim.x / gt) + threadIdx.x / gt;
   const bool live = row < rows;
   const int nv = h / N;
   const uint4* xr = reinterpret_cast<const uint4*>(x + row * h);
   uint4 raw[C];
-  float s = 0.0f;
 #pragma unroll
   for (int k = 0; k < C; ++k) {
     const int v = t + k * gt;
     raw[k] = (live && v < nv) ? __ldg(xr + v) : make_uint4(0, 0, 0, 0);
+  }
+  float s = 0.0f;
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
     float f[N];
     VT::unpack(raw[k], f);
 #pragma unroll
     for (int e = 0; e < N; ++e) s += f[e];
   }
-  const float mu = group_sum(s, red, nw) / h;
+  const float mu = group_sum2(make_float2(s, 0.0f), red, nw).x / h;
+  // two-pass variance from the registers (matches the oracle's arithmetic)
   float ss = 0.0f;
 #pragma unroll
   for (int k = 0; k < C; ++k) {
@@ -189,7 +205,7 @@ __global__ void __launch_bounds__(256) ln_fwd_vec_kernel(const T* __restrict__ x
       for (int e = 0; e < N; ++e) ss += (f[e] - mu) * (f[e] - mu);
     }
   }
-  const float rs = rsqrtf(group_sum(ss, red, nw) / h + kLnEps);
+  const float rs = rsqrtf(group_sum2(make_float2(ss, 0.0f), red, nw).x / h + kLnEps);
   if (!live) return;
   uint4* yr = reinterpret_cast<uint4*>(y + row * h);
 #pragma unroll
@@ -210,14 +226,17 @@ __global__ void __launch_bounds__(256) ln_fwd_vec_kernel(const T* __restrict__ x
 }
 
 // dx = res + rs * (g - mean(g) - xh * mean(g * xh)); res may alias dx or be null.
+// The residual's loads are issued with x and dy, ahead of the row reduction.
 template <typename T, int C>
-__global__ void __launch_bounds__(256) ln_bwd_vec_kernel(const T* __restrict__ x, const float* __restrict__ mean,
-                                                         const float* __restrict__ rstd, const T* __restrict__ dy,
-                                                         const T* res, T* dx, int rows, int h, int nw) {
+__global__ void __launch_bounds__(kVecRowMaxThreads) ln_bwd_vec_kernel(const T* __restrict__ x,
+                                                                       const float* __restrict__ mean,
+                                                                       const float* __restrict__ rstd,
+                                                                       const T* __restrict__ dy, const T* res, T* dx,
+                                                                       int rows, int h, int nw) {
   pdl_trigger_and_wait();
   using VT = Vec<T>;
   constexpr int N = VT::N;
-  __shared__ float red[8];
+  __shared__ float2 red[kVecRowMaxThreads / 32];
   const int gt = 32 * nw, t = threadIdx.x % gt;
   const long long row = (long long)blockIdx.x * (blockDim.x / gt) + threadIdx.x / gt;
   const bool live = row < rows;
@@ -225,14 +244,19 @@ __global__ void __launch_bounds__(256) ln_bwd_vec_kernel(const T* __restrict__ x
   const float mu = live ? mean[row] : 0.0f, rs = live ? rstd[row] : 0.0f;
   const uint4* xr = reinterpret_cast<const uint4*>(x + row * h);
   const uint4* gr = reinterpret_cast<const uint4*>(dy + row * h);
-  uint4 rx[C], rg[C];
-  float sg = 0.0f, sgx = 0.0f;
+  const uint4* rr = reinterpret_cast<const uint4*>(res + row * h);
+  uint4 rx[C], rg[C], rres[C];
 #pragma unroll
   for (int k = 0; k < C; ++k) {
     const int v = t + k * gt;
     const bool ok = live && v < nv;
     rx[k] = ok ? __ldg(xr + v) : make_uint4(0, 0, 0, 0);
     rg[k] = ok ? __ldg(gr + v) : make_uint4(0, 0, 0, 0);
+    rres[k] = (ok && res) ? rr[v] : make_uint4(0, 0, 0, 0);
+  }
+  float sg = 0.0f, sgx = 0.0f;
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
     float fx[N], fg[N];
     VT::unpack(rx[k], fx);
     VT::unpack(rg[k], fg);
@@ -242,11 +266,10 @@ __global__ void __launch_bounds__(256) ln_bwd_vec_kernel(const T* __restrict__ x
       sgx += fg[e] * ((fx[e] - mu) * rs);
     }
   }
-  const float mg = group_sum(sg, red, nw) / h;
-  const float mgx = group_sum(sgx, red, nw) / h;
+  const float2 m = group_sum2(make_float2(sg, sgx), red, nw);
+  const float mg = m.x / h, mgx = m.y / h;
   if (!live) return;
   uint4* dr = reinterpret_cast<uint4*>(dx + row * h);
-  const uint4* rr = reinterpret_cast<const uint4*>(res + row * h);
 #pragma unroll
   for (int k = 0; k < C; ++k) {
     const int v = t + k * gt;
@@ -254,25 +277,22 @@ __global__ void __launch_bounds__(256) ln_bwd_vec_kernel(const T* __restrict__ x
       float fx[N], fg[N], fr[N];
       VT::unpack(rx[k], fx);
       VT::unpack(rg[k], fg);
-      if (res) VT::unpack(rr[v], fr);
+      VT::unpack(rres[k], fr);
 #pragma unroll
-      for (int e = 0; e < N; ++e) {
-        const float d = rs * (fg[e] - mg - ((fx[e] - mu) * rs) * mgx);
-        fx[e] = res ? fr[e] + d : d;
-      }
+      for (int e = 0; e < N; ++e) fx[e] = fr[e] + rs * (fg[e] - mg - ((fx[e] - mu) * rs) * mgx);
       dr[v] = VT::pack(fx);
     }
   }
 }
 
 struct RowShape {
-  int nw, rpb, c;  // warps per row (<= 8), rows per block, 16-byte vectors per lane (<= 16)
+  int nw, rpb, c;  // warps per row (<= 16), rows per block, 16-byte vectors per lane (<= 8 for h <= 12288)
 };
 inline RowShape row_shape(int h, int n) {
   const int nv = h / n;
   RowShape r;
-  r.nw = std::min(8, (nv + 255) / 256);
-  r.rpb = 8 / r.nw;
+  r.nw = std::min(kVecRowMaxThreads / 32, std::max(1, (nv + 63) / 64));
+  r.rpb = std::max(1, 8 / r.nw);
   r.c = (nv + 32 * r.nw - 1) / (32 * r.nw);
   return r;
 }
@@ -287,8 +307,7 @@ inline RowShape row_shape(int h, int n) {
     if ((c) <= 1) { constexpr int C = 1; __VA_ARGS__; }        \
     else if ((c) <= 2) { constexpr int C = 2; __VA_ARGS__; }   \
     else if ((c) <= 4) { constexpr int C = 4; __VA_ARGS__; }   \
-    else if ((c) <= 8) { constexpr int C = 8; __VA_ARGS__; }   \
-    else { constexpr int C = 16; __VA_ARGS__; }                \
+    else { constexpr int C = 32 / Vec<T>::N; __VA_ARGS__; }    \
   } while (0)
 
 // E in {1,2,4,8,16,24,32,48}: smallest covering h

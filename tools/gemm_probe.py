@@ -47,17 +47,37 @@ dqkv = torch.empty_like(qkv)
 work = torch.empty(lib.gs_attention_bwd_workspace(b, s, h, H), dtype=torch.uint8, device=d)
 ms = timed(lambda: gs.check(lib.gs_attention_bwd(1, p(qkv), p(o), p(lse), p(dout), p(dqkv), p(work), b, s, h, H, None)))
 rows.append(dict(kernel="attn_bwd", ms=ms, tflops=2.5 * fl / ms / 1e9))
-# LayerNorm fwd / bwd(+residual): the step's shape (L2-resident) and 16x rows (HBM)
-for rows_ln in (T, 16 * T):
-    x = torch.randn(rows_ln, h, device=d).bfloat16()
+# LayerNorm fwd / bwd(+residual) at the 1.3B / 13B / 65B widths: the step's
+# shape (T rows, L2-resident) and 16x rows at h = 2048 (HBM)
+for h_ln, rows_ln in ((2048, T), (2048, 16 * T), (5120, T), (8192, T)):
+    x = torch.randn(rows_ln, h_ln, device=d).bfloat16()
     y = torch.empty_like(x)
     mean = torch.empty(rows_ln, device=d)
     rstd = torch.empty(rows_ln, device=d)
-    ms = timed(lambda: gs.check(lib.gs_layernorm_fwd(1, p(x), p(y), p(mean), p(rstd), rows_ln, h, None)))
-    rows.append(dict(kernel="ln_fwd", rows=rows_ln, ms=ms, gbs=2 * x.numel() * 2 / ms / 1e6))
-    ms = timed(lambda: gs.check(lib.gs_layernorm_bwd(1, p(x), p(mean), p(rstd), p(y), p(y), rows_ln, h, 1, None)))
-    rows.append(dict(kernel="ln_bwd_acc", rows=rows_ln, ms=ms, gbs=4 * x.numel() * 2 / ms / 1e6))
+    ms = timed(lambda: gs.check(lib.gs_layernorm_fwd(1, p(x), p(y), p(mean), p(rstd), rows_ln, h_ln, None)))
+    rows.append(dict(kernel="ln_fwd", h=h_ln, rows=rows_ln, ms=ms, gbs=2 * x.numel() * 2 / ms / 1e6))
+    ms = timed(lambda: gs.check(lib.gs_layernorm_bwd(1, p(x), p(mean), p(rstd), p(y), p(y), rows_ln, h_ln, 1, None)))
+    rows.append(dict(kernel="ln_bwd_acc", h=h_ln, rows=rows_ln, ms=ms, gbs=4 * x.numel() * 2 / ms / 1e6))
     del x, y
+# the same attention shapes through torch SDPA (cuDNN / flash backends) on
+# this box, as the anchor for the tcgen05 kernels above
+for backend in ("CUDNN_ATTENTION", "FLASH_ATTENTION"):
+    try:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+        q = torch.randn(b, H, s, h // H, device=d, dtype=torch.bfloat16, requires_grad=True)
+        k = torch.randn_like(q, requires_grad=True)
+        v = torch.randn_like(q, requires_grad=True)
+        with sdpa_kernel(getattr(SDPBackend, backend)):
+            ms = timed(lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True))
+            rows.append(dict(kernel=f"sdpa_{backend.lower()}_fwd", ms=ms, tflops=fl / ms / 1e9))
+            out_t = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
+            go = torch.randn_like(out_t)
+            ms_fb = timed(lambda: torch.autograd.grad(
+                torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True), (q, k, v), go))
+            rows.append(dict(kernel=f"sdpa_{backend.lower()}_bwd", ms=ms_fb - ms, tflops=2.5 * fl / (ms_fb - ms) / 1e9,
+                             note="fwd+bwd minus fwd"))
+    except Exception as e:  # noqa: BLE001
+        rows.append(dict(kernel=f"sdpa_{backend.lower()}", error=str(e)[:200]))
 # one layer's FwdCompute / RecomputeAndBwd back to back (no executor): GPU ms
 # per call and the host's enqueue ms per call
 out = (C.c_double * 4)()

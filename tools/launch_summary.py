@@ -3,6 +3,7 @@ launches, share of device time, average duration and — when the list holds
 dram__bytes_read/write.sum — average DRAM bytes per launch.
 Usage: python tools/launch_summary.py launches.csv [--json out.json]"""
 import collections
+import gzip
 import csv
 import json
 import sys
@@ -12,7 +13,8 @@ BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1
 
 
 def load(path):
-    rows = list(csv.reader(open(path)))
+    op = gzip.open if path.endswith(".gz") else open
+    rows = list(csv.reader(op(path, "rt")))
     h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[h]
     ii, ki = hdr.index("ID"), hdr.index("Kernel Name")

@@ -99,9 +99,10 @@ for r in cpu[:3] + cpu[-3:]:
 
 # window around the worst backward gaps: every transfer / step task that
 # overlaps it, with its times relative to the gap start
-for gap, a, c, key in [g for g in gaps if tasks[g[2]]["kind"] == "bwd"][:2]:
+for gap, a, c, key in ([g for g in gaps if tasks[g[2]]["kind"] != "bwd"][:1] +
+                       [g for g in gaps if tasks[g[2]]["kind"] == "bwd"][:2]):
     ga, gc = recs[a]["t_end_ms"], recs[c]["t_start_ms"]
-    print(f"=== window: gap {gap:.2f} ms before bwd L{tasks[c]['layer']} mb{tasks[c]['microbatch']} st{tasks[c]['stage']}")
+    print(f"=== window: gap {gap:.2f} ms before {tasks[c]['kind']} L{tasks[c]['layer']} mb{tasks[c]['microbatch']} st{tasks[c]['stage']}")
     win = [r for r in recs.values() if r["t_end_ms"] > ga - (25 if r["resource"] != "compute" else 4)
            and r["t_start_ms"] < gc + 1]
     for r in sorted(win, key=lambda r: (r["resource"], r["t_start_ms"])):
