@@ -277,6 +277,7 @@ def metric(args):
 def config_dict(args):
     N, h, H, s, b, V, M, split, alpha, tier, ring = CONFIGS[args.config]
     M = args.microbatches or M
+    ring = args.ssd_ring or ring
     alpha = args.alpha if args.alpha >= 0 else alpha
     alpha = alpha if args.schedule == "vertical" else 0.0
     place = (f"CPU-resident fractions (split) in pinned host DRAM, the rest on the NVMe file; "
@@ -285,7 +286,7 @@ def config_dict(args):
                         f"M={M} micro-batches/iteration, split(x_ckpt,x_param,x_opt)={split}, alpha={alpha}; {place}",
             "schedule": args.schedule, "opt_tier": OPT_TIERS[tier],
             "global_batch": M * b * max(args.gpus, 1), "seq_len": s, "microbatches": M, "alpha": alpha,
-            "split": list(split), "parallelism": f"zero3-dp{args.gpus}" if args.gpus > 1 else "single",
+            "split": list(split), "ssd_ring_layers": ring, "parallelism": f"zero3-dp{args.gpus}" if args.gpus > 1 else "single",
             "l2": "working set (params / optimizer state streamed, GBs per iteration) >> 126 MB L2; no flush needed"}
 
 
@@ -368,6 +369,7 @@ def run_ours(args):
         raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world} ranks")
     N, h, H, s, b, V, M, split, alpha, tier, ring = CONFIGS[args.config]
     M = args.microbatches or M
+    ring = args.ssd_ring or ring
     alpha = args.alpha if args.alpha >= 0 else alpha
     model = gs.ModelSpec(N, h, H, s, b, 2, 4, 3, world)  # ZeRO-3 over the ranks
     if args.schedule == "horizontal":
@@ -534,6 +536,7 @@ def main():
     ap.add_argument("--alpha", type=float, default=-1.0, help="override the config's delay ratio")
     ap.add_argument("--schedule", default="vertical", choices=["vertical", "horizontal"],
                     help="horizontal = the micro-batch-major ablation baseline (BASELINE configs[1])")
+    ap.add_argument("--ssd-ring", type=int, default=0, help="override the config's ssd_ring_layers (pinned staging slots)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--calibrate", type=int, default=1, help="calibrate offsim::simulate from the trace")
     ap.add_argument("--share-gpu", action="store_true",

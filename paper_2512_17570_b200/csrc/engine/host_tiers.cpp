@@ -3,7 +3,6 @@
 #include <cuda_runtime.h>
 #include <fcntl.h>
 #include <linux/io_uring.h>
-#include <sched.h>
 #include <sys/mman.h>
 #include <sys/resource.h>
 #include <sys/syscall.h>
@@ -39,18 +38,7 @@ ThreadPool::ThreadPool(int n, int nice_incr) {
     workers_.emplace_back([this, nice_incr] {
       // background workers yield the cores to the executor's dispatcher
       // threads (the compute dispatcher enqueues kernels back to back)
-      if (nice_incr > 0) {
-        // GS_HOST_SCHED=idle: SCHED_IDLE (a waking dispatcher preempts a
-        // worker at once) instead of a positive nice increment
-        const char* pol = std::getenv("GS_HOST_SCHED");
-        if (pol && std::strcmp(pol, "idle") == 0) {
-          sched_param sp{};
-          sp.sched_priority = 0;
-          (void)sched_setscheduler(0, SCHED_IDLE, &sp);
-        } else {
-          (void)setpriority(PRIO_PROCESS, static_cast<id_t>(syscall(SYS_gettid)), nice_incr);
-        }
-      }
+      if (nice_incr > 0) (void)setpriority(PRIO_PROCESS, static_cast<id_t>(syscall(SYS_gettid)), nice_incr);
       loop();
     });
 }

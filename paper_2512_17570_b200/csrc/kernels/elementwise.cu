@@ -110,12 +110,13 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(const T* __restrict
 }
 
 // Vectorised row kernels (h % (16 / sizeof(T)) == 0, the engine's case): a
-// row is owned by a group of nw warps sized so each lane holds at most C = 2
-// 16-byte vectors of every row operand (nw = 4 at h = 2048 bf16, 10 at 5120,
-// 16 at 8192), blocks carry max(1, 8 / nw) rows.  Keeping C small keeps the
-// register footprint at ~40 (full 64-warp occupancy; the earlier one-warp-per-
-// row shape held 8 vectors per operand, 137-174 registers, one CTA per SM and
-// ran latency-bound at 0.33-0.50 of HBM).
+// row is owned by a group of nw warps sized so each lane holds at most C
+// 16-byte vectors of every row operand — 4 in the forward (nw = 2 at h = 2048
+// bf16, 8 at 8192), 2 in the backward (nw = 4 at 2048, 16 at 8192) — and
+// blocks carry max(1, 8 / nw) rows.  Small C keeps the register footprint at
+// ~40-60 (the earlier one-warp-per-row shape held 8 vectors per operand,
+// 137-174 registers, one CTA per SM, and ran latency-bound at 0.33-0.50 of
+// HBM; its h > 4096 instance spilled).
 template <typename T> struct Vec;
 template <> struct Vec<float> {
   static constexpr int N = 4;
@@ -165,6 +166,11 @@ __device__ __forceinline__ float2 group_sum2(float2 v, float2* red, int nw) {
 
 constexpr int kVecRowMaxThreads = 512;
 
+// One reduction per row: sums of (x - K) and (x - K)^2 with the shift K =
+// x[row][0] (broadcast from lane 0's first vector), so the variance is
+// E[(x-K)^2] - E[x-K]^2 without the cancellation of the unshifted one-pass
+// form, and the row needs a single float2 group sum (one barrier pair when
+// nw > 1) instead of the two-pass form's two.
 template <typename T, int C>
 __global__ void __launch_bounds__(kVecRowMaxThreads) ln_fwd_vec_kernel(const T* __restrict__ x, T* __restrict__ y,
                                                                        float* __restrict__ mean,
@@ -185,27 +191,25 @@ __global__ void __launch_bounds__(kVecRowMaxThreads) ln_fwd_vec_kernel(const T* 
     const int v = t + k * gt;
     raw[k] = (live && v < nv) ? __ldg(xr + v) : make_uint4(0, 0, 0, 0);
   }
-  float s = 0.0f;
-#pragma unroll
-  for (int k = 0; k < C; ++k) {
-    float f[N];
-    VT::unpack(raw[k], f);
-#pragma unroll
-    for (int e = 0; e < N; ++e) s += f[e];
-  }
-  const float mu = group_sum2(make_float2(s, 0.0f), red, nw).x / h;
-  // two-pass variance from the registers (matches the oracle's arithmetic)
-  float ss = 0.0f;
+  const float K = live ? ld(x + row * h) : 0.0f;  // the row's first element (an L1 hit)
+  float s = 0.0f, ss = 0.0f;
 #pragma unroll
   for (int k = 0; k < C; ++k) {
     if (t + k * gt < nv) {
       float f[N];
       VT::unpack(raw[k], f);
 #pragma unroll
-      for (int e = 0; e < N; ++e) ss += (f[e] - mu) * (f[e] - mu);
+      for (int e = 0; e < N; ++e) {
+        const float d = f[e] - K;
+        s += d;
+        ss += d * d;
+      }
     }
   }
-  const float rs = rsqrtf(group_sum2(make_float2(ss, 0.0f), red, nw).x / h + kLnEps);
+  const float2 m = group_sum2(make_float2(s, ss), red, nw);
+  const float md = m.x / h;
+  const float mu = K + md;
+  const float rs = rsqrtf(fmaxf(m.y / h - md * md, 0.0f) + kLnEps);
   if (!live) return;
   uint4* yr = reinterpret_cast<uint4*>(y + row * h);
 #pragma unroll
@@ -288,10 +292,13 @@ __global__ void __launch_bounds__(kVecRowMaxThreads) ln_bwd_vec_kernel(const T* 
 struct RowShape {
   int nw, rpb, c;  // warps per row (<= 16), rows per block, 16-byte vectors per lane (<= 8 for h <= 12288)
 };
-inline RowShape row_shape(int h, int n) {
+// per_lane: target 16-byte vectors per lane and row operand (forward 4: one
+// row operand, a single reduction; backward 2: x, dy and the residual live
+// across the reduction)
+inline RowShape row_shape(int h, int n, int per_lane) {
   const int nv = h / n;
   RowShape r;
-  r.nw = std::min(kVecRowMaxThreads / 32, std::max(1, (nv + 63) / 64));
+  r.nw = std::min(kVecRowMaxThreads / 32, std::max(1, (nv + 32 * per_lane - 1) / (32 * per_lane)));
   r.rpb = std::max(1, 8 / r.nw);
   r.c = (nv + 32 * r.nw - 1) / (32 * r.nw);
   return r;
@@ -540,7 +547,7 @@ cudaError_t layernorm_fwd(DType dt, const void* x, void* y, float* mean, float* 
   if (rows == 0) return cudaSuccess;
   GS_DISPATCH(dt, {
     if (h % Vec<T>::N == 0) {
-      const RowShape r = row_shape(h, Vec<T>::N);
+      const RowShape r = row_shape(h, Vec<T>::N, 4);
       GS_ROW_C(r.c, GS_TRY_E(launch_pdl(ln_fwd_vec_kernel<T, C>, dim3((rows + r.rpb - 1) / r.rpb),
                                         dim3(32 * r.nw * r.rpb), 0, s, (const T*)x, (T*)y, mean, rstd, rows, h, r.nw)));
     } else {
@@ -557,7 +564,7 @@ cudaError_t layernorm_bwd(DType dt, const void* x, const float* mean, const floa
   if (rows == 0) return cudaSuccess;
   GS_DISPATCH(dt, {
     if (h % Vec<T>::N == 0) {
-      const RowShape r = row_shape(h, Vec<T>::N);
+      const RowShape r = row_shape(h, Vec<T>::N, 2);
       GS_ROW_C(r.c, GS_TRY_E(launch_pdl(ln_bwd_vec_kernel<T, C>, dim3((rows + r.rpb - 1) / r.rpb),
                                         dim3(32 * r.nw * r.rpb), 0, s, (const T*)x, mean, rstd, (const T*)dy,
                                         (const T*)res, (T*)dx, rows, h, r.nw)));

@@ -1,29 +1,41 @@
-"""Executor trace of the bench workload (GPT-1.3B, vertical, alpha 0.2,
-split (1,1,1)), middle of three iterations: per-phase resource busy time,
+"""Executor trace of a bench workload (default GPT-1.3B, vertical, alpha 0.2,
+split (1,1,1)), middle of the iterations: per-phase resource busy time,
 compute-stream gaps attributed to the plan dependency that finished last
 before each compute task started, and per-stage timing.
 
-usage: python tools/trace_phase.py [M] [opt_tier]"""
+usage: python tools/trace_phase.py [M] [opt_tier] [host_threads] [--config NAME] [--ring R]"""
+import argparse
+import os
 import sys
 
 import numpy as np
 
 sys.path.insert(0, ".")
 import paper_2512_17570_b200 as gs  # noqa: E402
+from bench import CONFIGS  # noqa: E402
 
-N, h, H, s, b, V = 24, 2048, 16, 2048, 2, 50304
-M = int(sys.argv[1]) if len(sys.argv) > 1 else 16
-tier = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-threads = int(sys.argv[3]) if len(sys.argv) > 3 else 0
-alpha = 0.2
+ap = argparse.ArgumentParser()
+ap.add_argument("M", nargs="?", type=int, default=0)
+ap.add_argument("tier", nargs="?", type=int, default=-1)
+ap.add_argument("threads", nargs="?", type=int, default=0)
+ap.add_argument("--config", default="gpt1.3b")
+ap.add_argument("--ring", type=int, default=0, help="ssd_ring_layers override")
+ap.add_argument("--iters", type=int, default=3)
+a = ap.parse_args()
+N, h, H, s, b, V, M, split, alpha, tier, ring = CONFIGS[a.config]
+M = a.M or M
+tier = tier if a.tier < 0 else a.tier
+ring = a.ring or ring
+threads = a.threads
 model = gs.ModelSpec(N, h, H, s, b, 2, 4, 3, 1)
-plan = gs.build_vertical(model, M, gs.StorageSplit(1, 1, 1), alpha)
+plan = gs.build_vertical(model, M, gs.StorageSplit(*split), alpha)
 eng = gs.Engine(plan, model, V, gs.AdamConfig(1e-4), opt_tier=tier, record_trace=True,
-                host_threads=threads)
-tok = np.random.default_rng(7).integers(0, V, size=(3, M, b, s + 1), dtype=np.int32)
+                host_threads=threads, ssd_ring_layers=ring, nvme_dir=os.environ.get("GS_NVME_DIR", "/tmp"))
+tok = np.random.default_rng(7).integers(0, V, size=(a.iters, M, b, s + 1), dtype=np.int32)
 eng.run(tok[:1])
 rep = eng.run(tok)
-print(f"M={M} opt_tier={tier} host_threads={threads}: total ms {rep.total_ms:.1f}, per iteration {rep.total_ms / 3:.1f}")
+print(f"{a.config} M={M} opt_tier={tier} ring={ring} host_threads={threads}: total ms {rep.total_ms:.1f}, "
+      f"per iteration {rep.total_ms / a.iters:.1f}")
 tasks = [plan.task(i) for i in range(len(plan))]
 recs = {r["task"]: r for r in rep.trace if r["iteration"] == 1}
 prev = {r["task"]: r for r in rep.trace if r["iteration"] == 0}
