@@ -278,6 +278,7 @@ def config_dict(args):
     N, h, H, s, b, V, M, split, alpha, tier, ring = CONFIGS[args.config]
     M = args.microbatches or M
     ring = args.ssd_ring or ring
+    tier = tier if args.opt_tier < 0 else args.opt_tier
     alpha = args.alpha if args.alpha >= 0 else alpha
     alpha = alpha if args.schedule == "vertical" else 0.0
     place = (f"CPU-resident fractions (split) in pinned host DRAM, the rest on the NVMe file; "
@@ -370,6 +371,7 @@ def run_ours(args):
     N, h, H, s, b, V, M, split, alpha, tier, ring = CONFIGS[args.config]
     M = args.microbatches or M
     ring = args.ssd_ring or ring
+    tier = tier if args.opt_tier < 0 else args.opt_tier
     alpha = args.alpha if args.alpha >= 0 else alpha
     model = gs.ModelSpec(N, h, H, s, b, 2, 4, 3, world)  # ZeRO-3 over the ranks
     if args.schedule == "horizontal":
@@ -443,6 +445,18 @@ def run_ours(args):
                       "FC1+GELU, FC2+residual, LM head), which run alone on the compute stream; the backward GEMMs "
                       "overlap each other on two streams and are not timed; timed region",
             "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)"}
+    span_flops, span_ms, span_n, _ = prof.get("gemm_span", (0.0, 0.0, 0, 0))
+    if span_ms > 0:
+        # the same launch population sampled without events (offset half a
+        # stride): the kernel's own first-CTA-start .. last-CTA-exit span
+        a_span = span_flops / (span_ms / 1e3) / 1e12
+        roof.update({"achieved_kernel_span": a_span, "frac_kernel_span": a_span / tf_sust,
+                     "avg_launch_ms_kernel_span": span_ms / span_n, "launches_kernel_span": span_n,
+                     "kernel_span_method": "in-kernel %globaltimer (min over CTAs at work start after the PDL wait, "
+                                           "max at CTA exit) on 1 in 16 of the same GEMM launches, none of them "
+                                           "event-bracketed: an event pair between two PDL-chained kernels stops "
+                                           "the next grid from launching under the previous one's drain, so the "
+                                           "event-timed duration also carries that launch ramp"})
     # iteration roofline (north star): max of compute at peak and ledger bytes over measured links
     bw = pcie_bandwidth(torch)
     led, ext = rep.ledger, rep.extension
@@ -480,7 +494,6 @@ def run_ours(args):
                              gpu_working_set_bytes=1 << 30, ssd_duplex=True)
         io_roof = gs.io_roofline(model, mio, M * b, split[2]) * s
     ms_step = dev_ms / K
-    other = {k: v for k, v in prof.items() if k != "gemm"}
     line = {"metric": metric(args),
             "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
@@ -511,7 +524,7 @@ def run_ours(args):
                                          "extension_h2d": float(rep.extension[0].sum()) / 1e9,
                                          "extension_d2h": float(rep.extension[1].sum()) / 1e9},
             "ledger_equals_plan": bool(np.array_equal(led, gs.plan_traffic(plan))),
-            "kernel_ms_per_step": {k: v[1] * v[3] / max(v[2], 1) / K for k, v in prof.items()},
+            "kernel_ms_per_step": {k: v[1] * v[3] / max(v[2], 1) / K for k, v in prof.items() if k != "gemm_span"},
             "kernel_ms_note": "1 launch in 16 per class bracketed by CUDA events, extrapolated; event overhead "
                               "inflates short kernels (LayerNorm ~10 us); device-time shares: profiles/ launch list",
             "losses": rep.losses,
@@ -536,6 +549,8 @@ def main():
     ap.add_argument("--alpha", type=float, default=-1.0, help="override the config's delay ratio")
     ap.add_argument("--schedule", default="vertical", choices=["vertical", "horizontal"],
                     help="horizontal = the micro-batch-major ablation baseline (BASELINE configs[1])")
+    ap.add_argument("--opt-tier", type=int, default=-1, choices=[-1, 0, 1, 2, 3],
+                    help="override the config's optimizer tier (" + ", ".join(f"{k} {v}" for k, v in OPT_TIERS.items()) + ")")
     ap.add_argument("--ssd-ring", type=int, default=0, help="override the config's ssd_ring_layers (pinned staging slots)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--calibrate", type=int, default=1, help="calibrate offsim::simulate from the trace")

@@ -187,6 +187,10 @@ int gs_engine_read_fixed_moments(gs_engine* engine, float* m, float* v);
    sampled launches, and all launches of the class */
 int gs_engine_kernel_profile(gs_engine* engine, double flops[5], double ms[5], int launches[5],
                              int64_t total_launches[5]);
+/* tcgen05 GEMM launches of the last run sampled by in-kernel %globaltimer
+   span (first CTA start .. last CTA exit; one in `stride`, none of them
+   event-timed): algorithmic flops, summed span ms, sampled launches */
+int gs_engine_gemm_span_profile(gs_engine* engine, double* flops, double* ms, int* launches);
 /* time one launch in `stride` per kernel class during later runs (0 = off) */
 int gs_engine_set_profiling(gs_engine* engine, int stride);
 /* record the per-task trace during later runs */

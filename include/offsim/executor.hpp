@@ -124,6 +124,10 @@ class Executor {
     double ms[5];          // sampled launches
     int launches[5];       // sampled launches
     long long total[5];    // all launches of the class
+    // tcgen05 GEMM launches sampled by in-kernel %globaltimer span (first
+    // CTA start .. last CTA exit), not bracketed by events
+    double span_flops = 0, span_ms = 0;
+    int span_launches = 0;
   };
   KernelTotals kernel_profile() const;
   // 0 disables per-kernel timing; n times one launch in n per class.

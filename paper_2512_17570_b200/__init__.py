@@ -541,7 +541,12 @@ class Engine:
         f, m, n, t = (C.c_double * 5)(), (C.c_double * 5)(), (C.c_int * 5)(), (C.c_int64 * 5)()
         check(lib().gs_engine_kernel_profile(self._h, f, m, n, t))
         names = ("gemm", "attention_fwd", "attention_bwd", "layernorm", "other")
-        return {k: (f[i], m[i], n[i], t[i]) for i, k in enumerate(names) if n[i]}
+        out = {k: (f[i], m[i], n[i], t[i]) for i, k in enumerate(names) if n[i]}
+        sf, sm, sn = C.c_double(), C.c_double(), C.c_int()
+        check(lib().gs_engine_gemm_span_profile(self._h, C.byref(sf), C.byref(sm), C.byref(sn)))
+        if sn.value:
+            out["gemm_span"] = (sf.value, sm.value, sn.value, t[0])
+        return out
 
     def set_profiling(self, stride: int) -> None:
         check(lib().gs_engine_set_profiling(self._h, int(stride)))

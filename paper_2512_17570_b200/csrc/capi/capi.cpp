@@ -351,6 +351,14 @@ int gs_engine_kernel_profile(gs_engine* engine, double flops[5], double ms[5], i
     }
   });
 }
+int gs_engine_gemm_span_profile(gs_engine* engine, double* flops, double* ms, int* launches) {
+  return guarded([&] {
+    const offsim::Executor::KernelTotals t = engine->ex->kernel_profile();
+    *flops = t.span_flops;
+    *ms = t.span_ms;
+    *launches = t.span_launches;
+  });
+}
 int gs_engine_set_profiling(gs_engine* engine, int stride) {
   return guarded([&] { engine->ex->set_profiling(stride); });
 }

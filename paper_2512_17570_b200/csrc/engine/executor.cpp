@@ -1776,6 +1776,7 @@ void read_field(Executor::Impl& I, int layer, int f, float* out) {
 Executor::KernelTotals Executor::kernel_profile() const {
   KernelTotals t{};
   impl_->prof.totals(t.flops, t.ms, t.launches, t.total);
+  impl_->prof.span_totals(&t.span_flops, &t.span_ms, &t.span_launches);
   return t;
 }
 

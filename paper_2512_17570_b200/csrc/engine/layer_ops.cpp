@@ -37,6 +37,7 @@ cudaError_t mm(const Dims& d, int M, int N, int K, const void* A, bool a_k, cons
                KernelProfiler* prof = nullptr) {
   Scope sc(prof, KernelProfiler::Gemm, 2.0 * M * N * K, st);
   GemmArgs g;
+  if (prof && sc.a < 0) g.span = prof->span_slot(2.0 * M * N * K);
   g.M = M;
   g.N = N;
   g.K = K;
@@ -97,8 +98,57 @@ void KernelProfiler::totals(double* flops, double* ms, int* launches, long long*
     launches[r.cls] += 1;
   }
 }
+unsigned long long* KernelProfiler::span_slot(double flops) {
+  const int st = stride > 0 ? stride : 1;
+  if (span_seen++ % st != st / 2) return nullptr;
+  if (!span_dev) {
+    if (cudaMalloc(&span_dev, 2 * sizeof(unsigned long long) * kSpanCap) != cudaSuccess) {
+      span_dev = nullptr;
+      (void)cudaGetLastError();
+      return nullptr;
+    }
+    reset();
+  }
+  const size_t i = span_flops.size();
+  if (i >= static_cast<size_t>(kSpanCap)) return nullptr;
+  span_flops.push_back(flops);
+  return span_dev + 2 * i;
+}
+void KernelProfiler::reset() {
+  next = 0;
+  recs.clear();
+  for (int c = 0; c < kCount; ++c) seen[c] = all_launches[c] = 0;
+  span_flops.clear();
+  span_seen = 0;
+  if (span_dev) {  // [min, max] pairs: min = ~0 (0xff bytes), max = 0
+    cudaDeviceSynchronize();
+    std::vector<unsigned long long> init(2 * static_cast<size_t>(kSpanCap));
+    for (size_t i = 0; i < init.size(); i += 2) {
+      init[i] = ~0ULL;
+      init[i + 1] = 0;
+    }
+    cudaMemcpy(span_dev, init.data(), init.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice);
+  }
+}
+void KernelProfiler::span_totals(double* flops, double* ms, int* launches) const {
+  *flops = 0;
+  *ms = 0;
+  *launches = 0;
+  if (!span_dev || span_flops.empty()) return;
+  std::vector<unsigned long long> h(2 * span_flops.size());
+  if (cudaMemcpy(h.data(), span_dev, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return;
+  for (size_t i = 0; i < span_flops.size(); ++i) {
+    const unsigned long long a = h[2 * i], b = h[2 * i + 1];
+    if (a == ~0ULL || b <= a) continue;  // launch not (yet) executed
+    *flops += span_flops[i];
+    *ms += static_cast<double>(b - a) * 1e-6;
+    ++*launches;
+  }
+}
 KernelProfiler::~KernelProfiler() {
   for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  if (span_dev) cudaFree(span_dev);
 }
 
 bool alloc_workspace(const Dims& d, Workspace& ws) {

@@ -40,14 +40,23 @@ struct KernelProfiler {
   long long all_launches[kCount] = {};
   int begin(cudaStream_t st, int cls);           // event index, or -1 when not sampled
   void end(int cls, double flops, int a, cudaStream_t st);
-  void reset() {
-    next = 0;
-    recs.clear();
-    for (int c = 0; c < kCount; ++c) seen[c] = all_launches[c] = 0;
-  }
+  // In-kernel span samples of the tcgen05 GEMM (GemmArgs::span): one launch
+  // in `stride`, offset stride / 2 from the event-timed ones, records its
+  // first-CTA-start .. last-CTA-exit %globaltimer span.  No stream operation
+  // sits between the kernels, so programmatic dependent launch and the
+  // step's timing are undisturbed (an event pair costs each timed launch its
+  // launch ramp).  Device buffer: [kSpanCap] minima, then [kSpanCap] maxima.
+  static constexpr int kSpanCap = 1 << 15;
+  unsigned long long* span_dev = nullptr;
+  std::vector<double> span_flops;
+  long long span_seen = 0;
+  unsigned long long* span_slot(double flops);  // nullptr when not sampled
+  void reset();
   // per class after the stream has completed: sampled flops, sampled ms,
   // sampled launches, all launches
   void totals(double* flops, double* ms, int* launches, long long* total) const;
+  // GEMM span samples after the stream has completed
+  void span_totals(double* flops, double* ms, int* launches) const;
   ~KernelProfiler();
 };
 inline const char* const kProfClasses[] = {"gemm", "attention_fwd", "attention_bwd", "layernorm", "other"};

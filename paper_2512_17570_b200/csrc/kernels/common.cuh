@@ -24,6 +24,12 @@ template <> struct io<__nv_bfloat16> {
 template <typename T> __device__ __forceinline__ float ld(const T* p) { return io<T>::load(p); }
 template <typename T> __device__ __forceinline__ void st(T* p, float v) { io<T>::store(p, v); }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

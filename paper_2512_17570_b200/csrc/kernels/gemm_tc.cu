@@ -351,8 +351,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_g, int M,
                    int N, int K, void* C, const bf16* R, bf16* G, int ldc, int sk_rem, float4* __restrict__ sk_ws,
-                   int* __restrict__ sk_flags, int sk_epoch) {
+                   int* __restrict__ sk_flags, int sk_epoch, unsigned long long* span) {
   pdl_trigger_and_wait();
+  if (span && threadIdx.x == 0) atomicMin(span, globaltimer_ns());
   using Cfg = TileCfg<BN, CG>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -580,6 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     else
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::kTmemCols));
   }
+  if (span && threadIdx.x == 0) atomicMax(span + 1, globaltimer_ns());
 }
 
 // ------------------------------------------------------------- host side
@@ -719,7 +721,7 @@ cudaError_t launch(const GemmArgs& g, cudaStream_t s) {
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   count_launch();
   return cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mg, g.M, g.N, g.K, g.C, (const bf16*)g.R, (bf16*)g.G,
-                            g.ldc ? g.ldc : g.N, rem, sk ? sk->ws : nullptr, sk ? sk->flags : nullptr, epoch);
+                            g.ldc ? g.ldc : g.N, rem, sk ? sk->ws : nullptr, sk ? sk->flags : nullptr, epoch, g.span);
 }
 
 template <int BN, bool A_MN, bool B_MN, int CG>

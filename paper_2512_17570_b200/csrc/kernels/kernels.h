@@ -35,6 +35,10 @@ struct GemmArgs {
   int ldc = 0;              // leading dim of C / R / G (0 -> N)
   Epi epi = Epi::Store;
   DType dt = DType::BF16;   // operand / output storage type
+  // optional in-kernel span sample (tcgen05 path): [0] min over CTAs of the
+  // %globaltimer at work start (after the PDL wait), [1] max at CTA exit;
+  // the caller pre-sets [0] = ~0, [1] = 0
+  unsigned long long* span = nullptr;
 };
 // Chooses the tcgen05 path (bf16, tile-aligned shapes) or the SIMT path.
 cudaError_t gemm(const GemmArgs& g, cudaStream_t s);
