@@ -76,7 +76,7 @@ CONFIGS = {
     # state half in pinned DRAM, half on the NVMe file (38.7 GB), never in HBM.
     # The full 80-layer model needs 773 GB of optimizer state (> this box)
     "gpt65b-8layer": (8, 8192, 64, 2048, 2, 50304, 32, (1.0, 1.0, 0.5), 0.2, 2, 2),
-    "tiny": (4, 64, 4, 32, 2, 128, 4, (0.0, 0.0, 0.0), 0.25, 2, 8),
+    "tiny": (4, 64, 4, 32, 2, 128, 4, (1.0, 1.0, 0.5), 0.25, 2, 8),
 }
 
 
@@ -348,8 +348,10 @@ def calibrate_and_simulate(gs, eng, plan, model, tokens, K, dev_ms):
 
 
 def run_ours(args):
-    import torch
     rank, world, local = dist_env()
+    if world != args.gpus:  # before touching a device: a --gpus N line must come from N ranks
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world} ranks")
+    import torch
     import torch.distributed as dist
     if world > 1:
         # one process per GPU; --share-gpu places every rank on the visible
@@ -366,8 +368,6 @@ def run_ours(args):
     else:
         torch.cuda.set_device(0)
     import paper_2512_17570_b200 as gs
-    if world != args.gpus:
-        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world} ranks")
     N, h, H, s, b, V, M, split, alpha, tier, ring = CONFIGS[args.config]
     M = args.microbatches or M
     ring = args.ssd_ring or ring

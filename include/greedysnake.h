@@ -138,7 +138,7 @@ typedef struct gs_engine_config {
   int profile_kernels;     /* CUDA-event timing per kernel class (gs_engine_kernel_profile) */
   int rank, world;         /* ZeRO-3 data parallelism: model.data_parallel_degree == world */
   const uint8_t* comm_id;  /* 128-byte job id from gs_comm_unique_id() on rank 0 (world > 1): peer-memory rendezvous */
-  int force_collectives;   /* run the sharded / NCCL path even at world == 1 */
+  int force_collectives;   /* run the sharded / peer-memory path even at world == 1 (tests) */
   int ssd_ring_layers;     /* pinned staging slots per SSD-resident data kind (0 -> 8) */
   int host_threads;        /* opt_tier 3: host optimizer threads (0 -> hardware threads - 4) */
 } gs_engine_config;
