@@ -76,6 +76,12 @@ CONFIGS = {
     # state half in pinned DRAM, half on the NVMe file (38.7 GB), never in HBM.
     # The full 80-layer model needs 773 GB of optimizer state (> this box)
     "gpt65b-8layer": (8, 8192, 64, 2048, 2, 50304, 32, (1.0, 1.0, 0.5), 0.2, 2, 2),
+    # BASELINE configs[4] (GPT-175B, 1 GPU, split (1, 0, 0): params and the
+    # whole optimizer state on the NVMe file, checkpoints in DRAM, b=1, M=32)
+    # on a 2-layer slice of its layer geometry (h = 12288, 96 heads): 50.7 GB
+    # on the NVMe file, the most this box's 80 GB disk holds with the probe's
+    # scratch.  CpuStep on the host cores over the staged state
+    "gpt175b-2layer": (2, 12288, 96, 2048, 1, 50304, 32, (1.0, 0.0, 0.0), 0.2, 3, 2),
     "tiny": (4, 64, 4, 32, 2, 128, 4, (1.0, 1.0, 0.5), 0.25, 2, 8),
 }
 

@@ -71,6 +71,7 @@ CASES = [
     ((1, 1, 0.5), 0.2, 3),   # half the state on NVMe (staging slots stepped in place)
     ((0.3, 0.7, 0.5), 0.25, 3),  # byte-granular split cuts inside elements
     ((0, 0, 0), 0.0, 3),     # all SSD
+    ((1, 0, 0), 0.2, 3),     # config 5 split (params + state on NVMe), host-core step
     ((1, 1, 1), 1.0, 3),     # everything delayed
 ]
 

@@ -84,6 +84,10 @@ out = (C.c_double * 4)()
 gs.check(lib.gs_layer_bench(1, 2, 2048, 2048, 16, 20, out))
 rows.append(dict(kernel="layer_fwd", gpu_ms=out[0], host_enqueue_ms=out[1]))
 rows.append(dict(kernel="layer_recompute_bwd", gpu_ms=out[2], host_enqueue_ms=out[3]))
+if len(sys.argv) > 1 and sys.argv[1] == "attn":  # attention / LayerNorm / layer rows only
+    for r in rows:
+        print(json.dumps(r))
+    sys.exit(0)
 # GEMMs last: the GPT-65B shapes heat the GPU and would lower the clocks
 # the attention / layer measurements see
 for name, M, N, K, ak, bk, epi in [
