@@ -21,7 +21,6 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 
 def main():
@@ -29,12 +28,15 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--tier", type=int, default=3, choices=[0, 1, 2, 3],
+                    help="optimizer tier (bench.OPT_TIERS); the horizontal rows use 2 (the host-core tier covers "
+                         "the vertical schedule)")
     ap.add_argument("--model", default="gpt1.3b", choices=["gpt1.3b", "gpt13b"],
                     help="gpt13b: BASELINE configs[2] shape, half the Adam state on NVMe, M and alpha sweep")
     args = ap.parse_args()
     import torch
-    import oracle_bindings as ob
     import paper_2512_17570_b200 as gs
+    from bench import OPT_TIERS, make_tokens
     torch.cuda.set_device(0)
     N, h, H, s, b, V = 24, 2048, 16, 2048, 2, 50304
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops_sustained", 1400.0) \
@@ -47,7 +49,6 @@ def main():
         N, h, H = 40, 5120, 40
         rows = [("vertical", a, (1, 1, 0.5), m) for m in (8, 16, 32) for a in (0.2, 0.0)]
     model = gs.ModelSpec(N, h, H, s, b, 2, 4, 3, 1)
-    g = ob.Geometry(n_layers=N, hidden=h, heads=H, seq=s, mb_size=b, vocab=V)
     for sched, alpha, split, M in rows:
         if sched == "horizontal":
             plan = gs.build_horizontal(model, M, gs.StorageSplit(*split))
@@ -61,11 +62,13 @@ def main():
                     break
                 except gs.InfeasibleError:
                     continue
+        tier = 2 if (sched == "horizontal" and args.tier == 3) else args.tier
         t0 = time.perf_counter()
         eng = gs.Engine(plan, model, V, gs.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0), seed=1234,
-                        nvme_dir=os.environ.get("GS_NVME_DIR", "/tmp"), opt_tier=0)
+                        nvme_dir=os.environ.get("GS_NVME_DIR", "/tmp"), opt_tier=tier,
+                        ssd_ring_layers=4 if args.model == "gpt13b" else 8)
         setup_s = time.perf_counter() - t0
-        tokens = ob.make_tokens(g, args.warmup + args.steps, M, seed=7)
+        tokens = make_tokens(V, args.warmup + args.steps, M, b, s, seed=7)
         eng.run(tokens[:args.warmup])
         dtok = torch.tensor(tokens[args.warmup:], device="cuda")
         torch.cuda.synchronize()
@@ -77,7 +80,8 @@ def main():
         flops = N * 4 * (24 * h * h + 2 * s * h) * tok
         led = rep.ledger
         print(json.dumps({
-            "schedule": sched, "alpha": alpha, "split": list(split), "microbatches": M, "global_batch": M * b,
+            "model": args.model, "schedule": sched, "alpha": alpha, "split": list(split), "microbatches": M,
+            "global_batch": M * b, "opt_tier": OPT_TIERS[tier],
             "tokens_per_s": tok / (ms / 1e3), "ms_per_iteration": ms,
             "compute_roofline_frac": flops / (peak * 1e12) / (ms / 1e3),
             "offload_gb": {"h2d": float(led[0].sum()) / 1e9, "d2h": float(led[1].sum()) / 1e9,
