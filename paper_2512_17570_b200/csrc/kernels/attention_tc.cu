@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
                       const __grid_constant__ CUtensorMap map_do, const __grid_constant__ CUtensorMap map_dq,
                       const __grid_constant__ CUtensorMap map_out,
                       const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv, int s,
-                      int h, int H, float scale, long long* __restrict__ tr, float* __restrict__ dq_red) {
+                      int h, int H, float scale, long long* __restrict__ tr) {
   pdl_trigger_and_wait();
   extern __shared__ __align__(1024) uint8_t rawb4[];
   FaBwdSmem4& sm = *reinterpret_cast<FaBwdSmem4*>(rawb4);
@@ -724,16 +724,6 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       fence_before();
       bar_arrive(&sm.dq_empty[buf]);  // TMEM buffer free for S/dP(i+2)
       if (r == 0) GS_TR4(6, i);
-      if (dq_red) {
-        // A/B: straight from registers into the fp32 accumulator with L2
-        // reductions (lane = d, one coalesced 128-B red per query and warp)
-        float* dst = dq_red + (long long)(row0 + (qb0 + i) * kBQb) * h + j * kD + r;
-#pragma unroll
-        for (int q = 0; q < kBQb; ++q)
-          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst + (long long)q * h), "f"(__uint_as_float(rr[q]) * scale)
-                       : "memory");
-        continue;
-      }
 #pragma unroll
       for (int half = 0; half < kBQb / kDqRows4; ++half) {
         const int sb = half & 1;  // pieces per block is even: piece parity == half parity
@@ -943,10 +933,8 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
     }
-    static const bool dq_red = getenv("GS_ATTN_DQ_RED") != nullptr && atoi(getenv("GS_ATTN_DQ_RED")) != 0;
     cudaError_t le = launch_pdl(fa_bwd_tc4_kernel, dim3(b * H, s / kBK), dim3(kThreadsBwd), smem4, st, mq, mq64, md,
-                                mdq, mout, lse2, D, (bf16*)dqkv, s, h, H, 1.0f / sqrtf((float)kD), tr,
-                                dq_red ? dq_acc : nullptr);
+                                mdq, mout, lse2, D, (bf16*)dqkv, s, h, H, 1.0f / sqrtf((float)kD), tr);
     if (le != cudaSuccess) return le;
     attn_trace_end(tr, st, b * H * (s / kBK), s / kBK);
     return cudaGetLastError();
