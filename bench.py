@@ -438,7 +438,7 @@ def run_ours(args):
     # traffic: DRAM bytes per GEMM launch from the committed ncu launch list of
     # this command (profiles/, dram__bytes_read + write per launch), if present
     traffic, traffic_src = None, None
-    tpath = os.path.join(ROOT, "profiles", "round1_gemm_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "round2", "gemm_traffic_r2q.json")
     if args.config == "gpt1.3b" and os.path.exists(tpath):
         t = json.load(open(tpath))
         traffic, traffic_src = t.get("gemm_dram_bytes_per_launch"), t.get("source")
