@@ -1,6 +1,6 @@
 """Launch one kernel of interest a few times at GPT-1.3B shapes, for ncu
 --set full captures (tools/final_round.sh): qkv | fc1 | wgrad | attn_fwd |
-attn_bwd.  Three launches; profile with `-s 2 -c 1` to skip warm-up."""
+attn_bwd | ln_fwd [h] | ln_bwd [h].  Three launches; profile with `-s 2 -c 1` to skip warm-up."""
 import ctypes as C
 import sys
 
@@ -24,6 +24,16 @@ if what in ("qkv", "fc1", "wgrad"):
     G = torch.empty(M * N, device=d, dtype=torch.bfloat16) if epi == 3 else None
     for _ in range(3):
         gs.check(lib.gs_gemm(1, M, N, K, p(A), ak, p(B), bk, p(Cc), None, p(G), epi, None))
+elif what.startswith("ln"):  # ln_fwd | ln_bwd [h]: LayerNorm at T rows (bwd with the residual accumulate)
+    hh = int(sys.argv[2]) if len(sys.argv) > 2 else h
+    x = torch.randn(T, hh, device=d).bfloat16()
+    y = torch.empty_like(x)
+    mean = torch.empty(T, device=d)
+    rstd = torch.empty(T, device=d)
+    for _ in range(3):
+        gs.check(lib.gs_layernorm_fwd(1, p(x), p(y), p(mean), p(rstd), T, hh, None))
+        if what == "ln_bwd":
+            gs.check(lib.gs_layernorm_bwd(1, p(x), p(mean), p(rstd), p(y), p(y), T, hh, 1, None))
 else:
     qkv = (torch.randn(b * s, 3 * h, device=d) * 0.5).bfloat16()
     o = torch.empty(b * s, h, device=d).bfloat16()
