@@ -20,3 +20,6 @@ run wgrad tc_gemm_kernel 2 wgrad
 run attn_fwd fa_fwd 2 attn_fwd
 run attn_bwd fa_bwd 2 attn_bwd
 rm -f gpurun_out/r2t_*.ncu-rep
+# the data-parallel path under the bench harness: two ranks (torchrun re-launch) sharing cuda:0 — a functional check
+timeout 1200 python bench.py --gpus 2 --share-gpu --steps 3 --warmup 3 --no-cpu-baseline --calibrate 0 > gpurun_out/r2t_bench_dp2.log 2>&1; echo "rc=$?" >> gpurun_out/r2t_bench_dp2.log
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/r2t_bench.log 2>&1; echo "rc=$?" >> gpurun_out/r2t_bench.log
