@@ -229,196 +229,6 @@ __global__ void __launch_bounds__(kVecRowMaxThreads) ln_fwd_vec_kernel(const T* 
   }
 }
 
-// Bulk-staged forward (B200: one bulk async copy per chunk of contiguous
-// rows into shared memory): each CTA owns a contiguous range of rows and
-// issues the loads of its first two chunks (<= 48 KB each) before touching
-// any of them, so a whole wave's reads are in flight at once — at the
-// engine's sizes (4096 rows x 4-16 KB) that is every byte of x; the
-// register-staged form above reached only ~2 bytes in flight per thread
-// between its reductions and ran latency-bound (0.51 of HBM at h = 2048).
-// A warp per row, two passes over the staged row (shifted sums; normalise +
-// coalesced 16-byte stores straight to global).
-constexpr int kLnSlotBytes = 48 * 1024;
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256) ln_fwd_bulk_kernel(const T* __restrict__ x, T* __restrict__ y,
-                                                          float* __restrict__ mean, float* __restrict__ rstd,
-                                                          int rows, int h, int rc) {
-  pdl_trigger_and_wait();
-  using VT = Vec<T>;
-  constexpr int N = VT::N;
-  extern __shared__ __align__(128) uint8_t ln_stage[];
-  __shared__ __align__(8) uint64_t full[2];
-  const int rb = h * (int)sizeof(T);
-  const int lo = (int)((long long)blockIdx.x * rows / gridDim.x);
-  const int hi = (int)((long long)(blockIdx.x + 1) * rows / gridDim.x);
-  const int nchunks = (hi - lo + rc - 1) / rc;
-  auto issue = [&](int c) {  // thread 0: rows [lo + c*rc, ...) are contiguous in x
-    const int r0 = lo + c * rc, nr = min(rc, hi - r0);
-    const uint32_t bytes = (uint32_t)nr * rb, bar = smem_u32(&full[c & 1]);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(ln_stage + (size_t)(c & 1) * rc * rb)),
-                 "l"(x + (long long)r0 * h), "r"(bytes), "r"(bar)
-                 : "memory");
-  };
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[i])));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (nchunks > 0) issue(0);
-    if (nchunks > 1) issue(1);
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  const int nv = h / N;
-  for (int c = 0; c < nchunks; ++c) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "LNW_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra LNW_%=;\n}" ::"r"(smem_u32(&full[c & 1])),
-        "r"((c >> 1) & 1)
-        : "memory");
-    const int r0 = lo + c * rc, nr = min(rc, hi - r0);
-    const uint4* slot = reinterpret_cast<const uint4*>(ln_stage + (size_t)(c & 1) * rc * rb);
-    for (int rr = warp; rr < nr; rr += nwarps) {
-      const uint4* row = slot + (size_t)rr * nv;
-      float f0[N];
-      VT::unpack(row[0], f0);
-      const float K = f0[0];
-      float s = 0.0f, ss = 0.0f;
-#pragma unroll 4
-      for (int v = lane; v < nv; v += 32) {
-        float f[N];
-        VT::unpack(row[v], f);
-#pragma unroll
-        for (int e = 0; e < N; ++e) {
-          const float d = f[e] - K;
-          s += d;
-          ss += d * d;
-        }
-      }
-      s = warp_sum(s);
-      ss = warp_sum(ss);
-      const float md = s / h, mu = K + md;
-      const float rs = rsqrtf(fmaxf(ss / h - md * md, 0.0f) + kLnEps);
-      uint4* yr = reinterpret_cast<uint4*>(y + (long long)(r0 + rr) * h);
-#pragma unroll 4
-      for (int v = lane; v < nv; v += 32) {
-        float f[N];
-        VT::unpack(row[v], f);
-#pragma unroll
-        for (int e = 0; e < N; ++e) f[e] = (f[e] - mu) * rs;
-        yr[v] = VT::pack(f);
-      }
-      if (lane == 0) {
-        if (mean) mean[r0 + rr] = mu;
-        if (rstd) rstd[r0 + rr] = rs;
-      }
-    }
-    __syncthreads();  // every warp is done with slot c & 1
-    if (threadIdx.x == 0 && c + 2 < nchunks) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async refill
-      issue(c + 2);
-    }
-  }
-}
-
-// Bulk-staged backward, same scheme: a chunk stages x, dy and the residual
-// rows (three bulk copies on one barrier) in a <= 96 KB slot, one CTA per SM;
-// dx is written straight to global (it may alias res: a CTA stages its rows
-// before it writes them).
-constexpr int kLnBwdSlotBytes = 96 * 1024;
-template <typename T>
-__global__ void __launch_bounds__(256) ln_bwd_bulk_kernel(const T* __restrict__ x, const float* __restrict__ mean,
-                                                          const float* __restrict__ rstd, const T* __restrict__ dy,
-                                                          const T* res, T* dx, int rows, int h, int rc) {
-  pdl_trigger_and_wait();
-  using VT = Vec<T>;
-  constexpr int N = VT::N;
-  extern __shared__ __align__(128) uint8_t ln_stage_b[];
-  __shared__ __align__(8) uint64_t full[2];
-  const int rb = h * (int)sizeof(T);
-  const int nops = res ? 3 : 2;
-  const int lo = (int)((long long)blockIdx.x * rows / gridDim.x);
-  const int hi = (int)((long long)(blockIdx.x + 1) * rows / gridDim.x);
-  const int nchunks = (hi - lo + rc - 1) / rc;
-  const size_t slot_bytes = (size_t)nops * rc * rb;
-  auto issue = [&](int c) {
-    const int r0 = lo + c * rc, nr = min(rc, hi - r0);
-    const uint32_t bytes = (uint32_t)nr * rb, bar = smem_u32(&full[c & 1]);
-    uint8_t* slot = ln_stage_b + (size_t)(c & 1) * slot_bytes;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes * nops) : "memory");
-    const T* src[3] = {x, dy, res};
-    for (int o = 0; o < nops; ++o)
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       smem_u32(slot + (size_t)o * rc * rb)),
-                   "l"(src[o] + (long long)r0 * h), "r"(bytes), "r"(bar)
-                   : "memory");
-  };
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[i])));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (nchunks > 0) issue(0);
-    if (nchunks > 1) issue(1);
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  const int nv = h / N;
-  for (int c = 0; c < nchunks; ++c) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "LNB_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra LNB_%=;\n}" ::"r"(smem_u32(&full[c & 1])),
-        "r"((c >> 1) & 1)
-        : "memory");
-    const int r0 = lo + c * rc, nr = min(rc, hi - r0);
-    const uint8_t* slot = ln_stage_b + (size_t)(c & 1) * slot_bytes;
-    for (int rr = warp; rr < nr; rr += nwarps) {
-      const uint4* xr = reinterpret_cast<const uint4*>(slot + (size_t)rr * rb);
-      const uint4* gr = reinterpret_cast<const uint4*>(slot + (size_t)rc * rb + (size_t)rr * rb);
-      const uint4* qr = reinterpret_cast<const uint4*>(slot + (size_t)2 * rc * rb + (size_t)rr * rb);
-      const float mu = mean[r0 + rr], rs = rstd[r0 + rr];
-      float sg = 0.0f, sgx = 0.0f;
-#pragma unroll 4
-      for (int v = lane; v < nv; v += 32) {
-        float fx[N], fg[N];
-        VT::unpack(xr[v], fx);
-        VT::unpack(gr[v], fg);
-#pragma unroll
-        for (int e = 0; e < N; ++e) {
-          sg += fg[e];
-          sgx += fg[e] * ((fx[e] - mu) * rs);
-        }
-      }
-      const float mg = warp_sum(sg) / h, mgx = warp_sum(sgx) / h;
-      uint4* dr = reinterpret_cast<uint4*>(dx + (long long)(r0 + rr) * h);
-#pragma unroll 4
-      for (int v = lane; v < nv; v += 32) {
-        float fx[N], fg[N], fr[N];
-        VT::unpack(xr[v], fx);
-        VT::unpack(gr[v], fg);
-        if (res) VT::unpack(qr[v], fr);
-#pragma unroll
-        for (int e = 0; e < N; ++e) {
-          const float d = rs * (fg[e] - mg - ((fx[e] - mu) * rs) * mgx);
-          fx[e] = res ? fr[e] + d : d;
-        }
-        dr[v] = VT::pack(fx);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && c + 2 < nchunks) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(c + 2);
-    }
-  }
-}
-
 // dx = res + rs * (g - mean(g) - xh * mean(g * xh)); res may alias dx or be null.
 // The residual's loads are issued with x and dy, ahead of the row reduction.
 template <typename T, int C>
@@ -736,24 +546,7 @@ cudaError_t layernorm_fwd(DType dt, const void* x, void* y, float* mean, float* 
   if (h > kRowThreads * kMaxPerThread) return cudaErrorInvalidValue;
   if (rows == 0) return cudaSuccess;
   GS_DISPATCH(dt, {
-    static const bool bulk = [] {
-      const char* e = getenv("GS_LN_BULK");
-      return !e || atoi(e) != 0;
-    }();
-    if (bulk && h % Vec<T>::N == 0 && (long long)h * sizeof(T) <= kLnSlotBytes) {
-      const int rb = h * (int)sizeof(T);
-      const int grid = std::min(rows, 2 * num_sms());
-      const int per = (rows + grid - 1) / grid;
-      const int rc = std::max(1, std::min(per, kLnSlotBytes / rb));
-      static bool attr = false;
-      if (!attr) {
-        GS_TRY_E(cudaFuncSetAttribute(ln_fwd_bulk_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      2 * kLnSlotBytes));
-        attr = true;
-      }
-      GS_TRY_E(launch_pdl(ln_fwd_bulk_kernel<T>, dim3(grid), dim3(256), (size_t)2 * rc * rb, s, (const T*)x, (T*)y,
-                          mean, rstd, rows, h, rc));
-    } else if (h % Vec<T>::N == 0) {
+    if (h % Vec<T>::N == 0) {
       const RowShape r = row_shape(h, Vec<T>::N, 4);
       GS_ROW_C(r.c, GS_TRY_E(launch_pdl(ln_fwd_vec_kernel<T, C>, dim3((rows + r.rpb - 1) / r.rpb),
                                         dim3(32 * r.nw * r.rpb), 0, s, (const T*)x, (T*)y, mean, rstd, rows, h, r.nw)));
@@ -770,25 +563,7 @@ cudaError_t layernorm_bwd(DType dt, const void* x, const float* mean, const floa
   if (h > kRowThreads * kMaxPerThread) return cudaErrorInvalidValue;
   if (rows == 0) return cudaSuccess;
   GS_DISPATCH(dt, {
-    static const bool bulk = [] {
-      const char* e = getenv("GS_LN_BULK");
-      return !e || atoi(e) != 0;
-    }();
-    const int nops = res ? 3 : 2;
-    if (bulk && h % Vec<T>::N == 0 && (long long)nops * h * sizeof(T) <= kLnBwdSlotBytes) {
-      const int rb = h * (int)sizeof(T);
-      const int grid = std::min(rows, num_sms());
-      const int per = (rows + grid - 1) / grid;
-      const int rc = std::max(1, std::min(per, kLnBwdSlotBytes / (nops * rb)));
-      static bool attr = false;
-      if (!attr) {
-        GS_TRY_E(cudaFuncSetAttribute(ln_bwd_bulk_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      2 * kLnBwdSlotBytes));
-        attr = true;
-      }
-      GS_TRY_E(launch_pdl(ln_bwd_bulk_kernel<T>, dim3(grid), dim3(256), (size_t)2 * nops * rc * rb, s, (const T*)x,
-                          mean, rstd, (const T*)dy, (const T*)res, (T*)dx, rows, h, rc));
-    } else if (h % Vec<T>::N == 0) {
+    if (h % Vec<T>::N == 0) {
       const RowShape r = row_shape(h, Vec<T>::N, 2);
       GS_ROW_C(r.c, GS_TRY_E(launch_pdl(ln_bwd_vec_kernel<T, C>, dim3((rows + r.rpb - 1) / r.rpb),
                                         dim3(32 * r.nw * r.rpb), 0, s, (const T*)x, mean, rstd, (const T*)dy,
