@@ -397,8 +397,6 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
     throw ValidationError("executor: opt_tier must be 0 (auto), 1 (HBM), 2 (stream) or 3 (host)");
   bool opt_hbm = cfg.opt_tier == OptTier::Hbm;
   host_step = cfg.opt_tier == OptTier::Host;
-  if (host_step && horizontal)
-    throw ValidationError("executor: the host-core optimizer tier covers the vertical schedule");
   size_t free_b = 0, total_b = 0;
   cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
   if (cfg.opt_tier == OptTier::Auto) {

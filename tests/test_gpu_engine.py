@@ -181,7 +181,8 @@ def test_bf16_engine_tcgen05_attention_tracks_oracle():
     assert np.array_equal(reps[-1].ledger, gs.plan_traffic(plan))
 
 
-@pytest.mark.parametrize("split,tier", [((1, 1, 1), 0), ((0, 0, 0), 0), ((0.3, 0.7, 0.5), 2)])
+@pytest.mark.parametrize("split,tier", [((1, 1, 1), 0), ((0, 0, 0), 0), ((0.3, 0.7, 0.5), 2),
+                                        ((1, 1, 1), 3), ((0.3, 0.7, 0.5), 3), ((0, 0, 0), 3)])
 def test_fp32_horizontal_engine_matches_oracle(split, tier):
     """The ablation baseline (build_horizontal, schedule.cpp:127-258) executes
     with the same numerics: gradients accumulate through DRAM across

@@ -29,8 +29,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--tier", type=int, default=3, choices=[0, 1, 2, 3],
-                    help="optimizer tier (bench.OPT_TIERS); the horizontal rows use 2 (the host-core tier covers "
-                         "the vertical schedule)")
+                    help="optimizer tier (bench.OPT_TIERS), every row")
     ap.add_argument("--model", default="gpt1.3b", choices=["gpt1.3b", "gpt13b"],
                     help="gpt13b: BASELINE configs[2] shape, half the Adam state on NVMe, M and alpha sweep")
     args = ap.parse_args()
@@ -62,7 +61,7 @@ def main():
                     break
                 except gs.InfeasibleError:
                     continue
-        tier = 2 if (sched == "horizontal" and args.tier == 3) else args.tier
+        tier = args.tier
         t0 = time.perf_counter()
         eng = gs.Engine(plan, model, V, gs.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0), seed=1234,
                         nvme_dir=os.environ.get("GS_NVME_DIR", "/tmp"), opt_tier=tier,
