@@ -275,6 +275,8 @@ def run_reference(args):
 
 
 def metric(args):
+    if args.schedule == "horizontal":
+        return f"tokens/sec ({args.config} training, horizontal schedule (the ablation baseline))"
     if args.config == "gpt1.3b":
         return METRIC
     return f"tokens/sec ({args.config} training, vertical schedule + alpha-delayed optimizer step)"

@@ -97,3 +97,38 @@ def test_world2_executor_matches_single_process_oracle(tmp_path, cfg):
     # the tied embedding is replicated: identical on both ranks, equal to the oracle's
     assert np.array_equal(res[0]["fixed"], res[1]["fixed"])
     assert rel(res[0]["fixed"], ref_fixed) < 1e-4
+
+
+def _bench_line(args, timeout=900):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "bench.py", *args], cwd=root, capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-4000:])
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_bench_contract_line_single_gpu():
+    """bench.py's driver line on the GPU (tiny config): every contract key,
+    the executed ledger equal to the plan's, kernels launched."""
+    d = _bench_line(["--config", "tiny", "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--calibrate", "0"])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] > 0 and d["ledger_equals_plan"]
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in d["roofline"], k
+
+
+def test_bench_two_ranks_through_torchrun():
+    """`bench.py --gpus 2` re-launches itself under torch.distributed.run; the
+    two ranks (sharing the box's GPU when it has one) run the ZeRO-3
+    peer-memory path and rank 0 reports n_gpus 2."""
+    d = _bench_line(["--gpus", "2", "--share-gpu", "--config", "tiny", "--steps", "2", "--warmup", "3",
+                     "--no-cpu-baseline", "--calibrate", "0"])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["ledger_equals_plan"]
+    assert d["config"]["parallelism"] == "zero3-dp2" and d["config"]["global_batch"] == 2 * 4 * 2
