@@ -205,9 +205,10 @@ def test_fp32_horizontal_engine_matches_oracle(split, tier):
 
 
 def test_sharded_peer_comm_path_at_world1_matches_oracle():
-    """The ZeRO-3 code path (NCCL all-gather of layer shards, reduce-scatter
-    of the fp32 gradient, embedding all-reduce, shard-local Adam) forced on at
-    world = 1: identical numerics to the oracle."""
+    """The ZeRO-3 code path (peer-memory all-gather of layer shards,
+    rank-ordered reduce-scatter of the fp32 gradient, the embedding
+    reduce-scatter + all-gather, shard-local Adam) forced on at world = 1:
+    identical numerics to the oracle."""
     need_gpu()
     g, M, iters = ob.TINY, 4, 3
     model = gs.ModelSpec(g.n_layers, g.hidden, g.heads, g.seq, g.mb_size, 4, 4, 3, 1)
