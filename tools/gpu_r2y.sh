@@ -1,0 +1,6 @@
+# HEAD validation: full GPU suite, smoke, bench (driver default), reference arm
+mkdir -p gpurun_out
+timeout 2400 python -m pytest tests -m gpu -q -rs > gpurun_out/r2y_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/r2y_pytest.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2y_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/r2y_smoke.log
+timeout 900 python bench.py > gpurun_out/r2y_bench.log 2>&1; echo "rc=$?" >> gpurun_out/r2y_bench.log
+timeout 900 python bench.py --impl reference > gpurun_out/r2y_ref.log 2>&1; echo "rc=$?" >> gpurun_out/r2y_ref.log
