@@ -3,8 +3,11 @@
 // peers' HBM (CUDA IPC mappings; NVLink 5 / NVSwitch loads on a multi-GPU
 // node, plain HBM loads for ranks sharing a device) and writes the sum.
 // Sums run in rank order, so every rank's shard is bit-identical to a
-// single-process sum in that order, run after run.  HBM / NVLink bound:
-// float4 loads, grid = a multiple of the SM count.
+// single-process sum in that order, run after run.  NVLink / HBM bound:
+// float4 loads from every rank per thread, a capped grid (32 CTAs) so the
+// reduce leaves the SMs to the compute stream it overlaps.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -77,7 +80,10 @@ cudaError_t peer_wait_spin(const PeerFlags& f, int n, uint32_t value, cudaStream
 cudaError_t peer_sum(const PeerSrcs& src, int world, float* dst, long long n, cudaStream_t s) {
   if (world < 1 || world > kMaxPeers || n < 0) return cudaErrorInvalidValue;
   if (n == 0) return cudaSuccess;
-  const unsigned grid = grid_for(n / 4 + 1, 256);
+  // a few CTAs saturate the peer links (each thread keeps W 16-byte loads in
+  // flight); the reduce runs beside the next stage's GEMMs, so it must not
+  // take their SMs (a 32-per-SM grid would)
+  const unsigned grid = std::min(grid_for(n / 4 + 1, 256), 32u);
   count_launch();
   switch (world) {
     case 1: peer_sum_kernel<1><<<grid, 256, 0, s>>>(src, dst, n); break;
