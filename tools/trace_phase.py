@@ -122,3 +122,20 @@ for gap, a, c, key in ([g for g in gaps if tasks[g[2]]["kind"] != "bwd"][:1] +
         print(f"  {r['resource']:9s} id {r['task']:5d} {t['kind']:8s} {t.get('data', ''):15s} L{t['layer']:<3d} "
               f"mb{t['microbatch']:<3d} st{t['stage']:<3d} {r['t_start_ms'] - ga:8.2f} .. {r['t_end_ms'] - ga:8.2f} ms "
               f"{t.get('bytes', 0) / 1e6:8.1f} MB host {r['t_host_ms'] - ga:8.2f} deps {t['deps']}")
+
+# NVMe queues: per-task bandwidth and the idle gaps between consecutive tasks
+for res in ("ssd_read", "ssd_write"):
+    rs = sorted([r for r in recs.values() if r["resource"] == res], key=lambda r: r["t_start_ms"])
+    if not rs:
+        continue
+    busy = sum(r["t_end_ms"] - r["t_start_ms"] for r in rs)
+    byts = sum(r["bytes"] for r in rs)
+    gaps = [b["t_start_ms"] - a["t_end_ms"] for a, b in zip(rs, rs[1:])]
+    print(f"{res}: {len(rs)} tasks, {byts / 1e9:.2f} GB, busy {busy:.0f} ms -> {byts / 1e6 / max(busy, 1e-9):.2f} GB/s "
+          f"while busy; gaps between tasks: total {sum(g for g in gaps if g > 0):.0f} ms, "
+          f"max {max(gaps) if gaps else 0:.0f} ms")
+    sizes = sorted({round(r['bytes'] / 1e6) for r in rs})
+    for mb in sizes:
+        sel = [r for r in rs if round(r["bytes"] / 1e6) == mb]
+        d = [r["t_end_ms"] - r["t_start_ms"] for r in sel]
+        print(f"   {mb:8d} MB x {len(sel):3d}: mean {np.mean(d):8.1f} ms -> {mb / np.mean(d):.2f} GB/s")
