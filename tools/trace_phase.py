@@ -139,3 +139,9 @@ for res in ("ssd_read", "ssd_write"):
         sel = [r for r in rs if round(r["bytes"] / 1e6) == mb]
         d = [r["t_end_ms"] - r["t_start_ms"] for r in sel]
         print(f"   {mb:8d} MB x {len(sel):3d}: mean {np.mean(d):8.1f} ms -> {mb / np.mean(d):.2f} GB/s")
+    if os.environ.get("GS_TRACE_SSD_LIST"):
+        for r in rs:
+            t = tasks[r["task"]]
+            print(f"     {res} id {r['task']:6d} {t.get('data', ''):10s} L{t['layer']:<3d} st{t['stage']:<4d} "
+                  f"{r['t_start_ms'] - t0:9.1f} .. {r['t_end_ms'] - t0:9.1f} ms  {r['bytes'] / 1e6:8.1f} MB "
+                  f"host {r['t_host_ms'] - t0:9.1f}")
