@@ -263,8 +263,10 @@ struct Executor::Impl {
   Impl(const SchedulePlan& p, const ExecConfig& c);
   ~Impl();
   void* dmalloc(u64 bytes);
-  Blob make_blob(u64 size, std::vector<u64> cuts, u64 cpu_bytes, bool hbm_for_cpu, std::vector<uint8_t*>& ring,
-                 int slot);
+  // ssd: byte ranges [lo, hi) of the blob that live on the NVMe file; the
+  // rest is CPU-resident (pinned DRAM, or HBM when hbm_for_cpu)
+  Blob make_blob(u64 size, const std::vector<std::pair<u64, u64>>& ssd, bool hbm_for_cpu,
+                 std::vector<uint8_t*>& ring, int slot);
   void init_weights();
   void build_tasks();
   void hazards();
@@ -484,10 +486,28 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   ring_param.assign(static_cast<size_t>(ring_k), nullptr);
   ring_opt.assign(static_cast<size_t>(ring_k), nullptr);
   ring_ckpt.assign(static_cast<size_t>(ring_k) * M, nullptr);
+  // Placement of a layer's params / optimizer state, the reference's byte
+  // model (schedule.cpp:309-314): the SSD-resident bytes are ssd_portion of
+  // the whole, and the delayed alpha slice owns scaled_portion(ssd, alpha) of
+  // them, the immediate slice the rest.  Each slice keeps its CPU part first
+  // and its SSD bytes at its end, so every plan SSD transfer of a slice moves
+  // exactly that slice's bytes (a single CPU/SSD cut over the whole blob put
+  // the delayed slice entirely on the SSD: 2x the plan's bytes in the
+  // forward-phase reads and writes, 0.75x in the backward's).
+  auto slice_ssd = [&](u64 size, u64 elem_bytes, double x) {
+    const u64 e = elem_bytes * loc_now;  // immediate | delayed element boundary
+    const u64 ssd = ssd_portion(size, x);
+    u64 late = std::min(scaled_portion(ssd, plan.kind.delay_ratio), size - e);
+    u64 now = ssd - late;
+    if (now > e) {  // byte rounding at x ~ 0: at most a few bytes move across
+      now = e;
+      late = ssd - now;
+    }
+    return std::vector<std::pair<u64, u64>>{{e - now, e}, {size - late, size}};
+  };
   for (int l = 0; l < N; ++l) {
-    param_blob.push_back(
-        make_blob(lp * Ps, {lp * loc_now}, cpu_portion(lp * Ps, plan.split.x_param), false, ring_param, l % ring_k));
-    opt_blob.push_back(make_blob(opt_bytes, {12 * loc_now}, cpu_opt, opt_hbm, ring_opt, l % ring_k));
+    param_blob.push_back(make_blob(lp * Ps, slice_ssd(lp * Ps, lp, plan.split.x_param), false, ring_param, l % ring_k));
+    opt_blob.push_back(make_blob(opt_bytes, slice_ssd(opt_bytes, 12, plan.split.x_opt), opt_hbm, ring_opt, l % ring_k));
   }
   // GradAccum D2H landing buffers.  The horizontal schedule reads a layer's
   // partial sum back for the next micro-batch, so it keeps one per layer;
@@ -510,7 +530,7 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   for (int l = 0; l < N; ++l)
     for (int m = 0; m < M; ++m)
       ckpt_blob.push_back(
-          make_blob(cb, {}, cpu_portion(cb, plan.split.x_ckpt), false, ring_ckpt, (l % ring_k) * M + m));
+          make_blob(cb, {{cpu_portion(cb, plan.split.x_ckpt), cb}}, false, ring_ckpt, (l % ring_k) * M + m));
   auto has_ssd = [](const Blob& b) {
     for (const Segment& sg : b.segs)
       if (sg.tier == Tier::Ssd) return true;
@@ -574,11 +594,13 @@ void* Executor::Impl::dmalloc(u64 bytes) {
 // segments live in pinned DRAM (or HBM), SSD segments get an NVMe region and
 // a 4 KiB-aligned place in staging slot ring[slot] (allocated by the first
 // blob that uses the slot; blobs of one kind have identical segments).
-Blob Executor::Impl::make_blob(u64 size, std::vector<u64> cuts, u64 cpu_bytes, bool hbm_for_cpu,
+Blob Executor::Impl::make_blob(u64 size, const std::vector<std::pair<u64, u64>>& ssd, bool hbm_for_cpu,
                                std::vector<uint8_t*>& ring, int slot) {
-  cuts.push_back(0);
-  cuts.push_back(size);
-  cuts.push_back(cpu_bytes);
+  std::vector<u64> cuts = {0, size};
+  for (const auto& r : ssd) {
+    cuts.push_back(r.first);
+    cuts.push_back(r.second);
+  }
   std::sort(cuts.begin(), cuts.end());
   cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
   Blob b;
@@ -588,7 +610,9 @@ Blob Executor::Impl::make_blob(u64 size, std::vector<u64> cuts, u64 cpu_bytes, b
     s.lo = cuts[i];
     s.hi = cuts[i + 1];
     if (s.hi <= s.lo || s.hi > size) continue;
-    if (s.lo < cpu_bytes) {
+    bool on_ssd = false;
+    for (const auto& r : ssd) on_ssd = on_ssd || (s.lo >= r.first && s.hi <= r.second);
+    if (!on_ssd) {
       s.tier = hbm_for_cpu ? Tier::Hbm : Tier::Dram;
       if (hbm_for_cpu) {
         s.dev = static_cast<uint8_t*>(dmalloc(s.size()));

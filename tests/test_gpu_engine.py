@@ -154,6 +154,28 @@ def test_trace_order_and_ledger(tier):
     assert np.array_equal(led, gs.plan_traffic(plan))
 
 
+@pytest.mark.parametrize("split,alpha,tier", [((0.3, 0.7, 0.5), 0.25, 0), ((1, 0.4, 0.3), 0.2, 3),
+                                              ((0, 0, 0), 0.25, 2), ((1, 1, 0), 0.5, 3)])
+def test_every_ssd_task_moves_its_plan_bytes(split, alpha, tier):
+    """Per task, the NVMe bytes physically moved are the plan's bytes (up to
+    the 4 KiB O_DIRECT rounding of each staged segment): the delayed alpha
+    slice owns scaled_portion(ssd, alpha) of a layer's SSD-resident params /
+    optimizer state (schedule.cpp:309-314), the immediate slice the rest."""
+    need_gpu()
+    g, M = ob.TINY, 4
+    plan, reps, *_ = run_engine(g, M, split, alpha, 2, trace=True, opt_tier=tier)
+    tasks = [plan.task(i) for i in range(len(plan))]
+    n = 0
+    for r in reps[-1].trace:
+        t = tasks[r["task"]]
+        if r["iteration"] != 1 or t["kind"] != "xfer" or not t["link"].startswith("SSD"):
+            continue
+        segs = M if t["data"] == "ckpt" else 2
+        assert t["bytes"] <= r["physical_bytes"] < t["bytes"] + 4096 * segs, (t, r["physical_bytes"])
+        n += 1
+    assert n > 0
+
+
 def test_bf16_engine_tracks_oracle():
     """bf16 training mode (reported separately): loss within 2e-2 of the
     fp32 oracle over 3 steps at a tensor-core-tiled geometry."""
