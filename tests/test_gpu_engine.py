@@ -155,7 +155,7 @@ def test_trace_order_and_ledger(tier):
 
 
 @pytest.mark.parametrize("split,alpha,tier", [((0.3, 0.7, 0.5), 0.25, 0), ((1, 0.4, 0.3), 0.2, 3),
-                                              ((0, 0, 0), 0.25, 2), ((1, 1, 0), 0.5, 3)])
+                                              ((1, 0, 0), 0.25, 2), ((0.8, 0.2, 0.1), 0.2, 3), ((1, 1, 0), 0.5, 3)])
 def test_every_ssd_task_moves_its_plan_bytes(split, alpha, tier):
     """Per task, the NVMe bytes physically moved are the plan's bytes (up to
     the 4 KiB O_DIRECT rounding of each staged segment): the delayed alpha
