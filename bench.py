@@ -67,15 +67,16 @@ CONFIGS = {
     "gpt1.3b-hbm-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2, 1, 8),
     "gpt1.3b-stream-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2, 2, 8),
     "gpt1.3b-host-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 1.0), 0.2, 3, 8),
-    "gpt1.3b-ssd-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 0.0), 0.2, 2, 8),
+    "gpt1.3b-ssd-opt": (24, 2048, 16, 2048, 2, 50304, 16, (1.0, 1.0, 0.0), 0.2, 3, 8),
     # BASELINE configs[2] shape on this box (196 GB DRAM, 80 GB disk): half of
     # the optimizer state (75.5 GB) on the NVMe tier, the other half in DRAM
-    "gpt13b-nvme": (40, 5120, 40, 2048, 2, 50304, 16, (1.0, 1.0, 0.5), 0.2, 2, 2),
+    "gpt13b-nvme": (40, 5120, 40, 2048, 2, 50304, 16, (1.0, 1.0, 0.5), 0.2, 3, 4),
     # GPT-65B layer geometry (h = 8192, 64 heads, b = 2, M = 32: BASELINE
     # configs[3] per rank, split (1,1,0.5)) on an 8-layer slice: the optimizer
-    # state half in pinned DRAM, half on the NVMe file (38.7 GB), never in HBM.
-    # The full 80-layer model needs 773 GB of optimizer state (> this box)
-    "gpt65b-8layer": (8, 8192, 64, 2048, 2, 50304, 32, (1.0, 1.0, 0.5), 0.2, 2, 2),
+    # state half in pinned DRAM, half on the NVMe file (38.7 GB), never in HBM,
+    # stepped by the host cores; 4 layers of NVMe staging.  The full 80-layer
+    # model needs 773 GB of optimizer state (> this box)
+    "gpt65b-8layer": (8, 8192, 64, 2048, 2, 50304, 32, (1.0, 1.0, 0.5), 0.2, 3, 4),
     # BASELINE configs[4] (GPT-175B, 1 GPU, split (1, 0, 0): params and the
     # whole optimizer state on the NVMe file, checkpoints in DRAM, b=1, M=32)
     # on a 2-layer slice of its layer geometry (h = 12288, 96 heads): 50.7 GB
