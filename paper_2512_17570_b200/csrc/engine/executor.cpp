@@ -497,7 +497,13 @@ Executor::Impl::Impl(const SchedulePlan& p, const ExecConfig& c) : plan(p), cfg(
   auto slice_ssd = [&](u64 size, u64 elem_bytes, double x) {
     const u64 e = elem_bytes * loc_now;  // immediate | delayed element boundary
     const u64 ssd = ssd_portion(size, x);
-    u64 late = std::min(scaled_portion(ssd, plan.kind.delay_ratio), size - e);
+    // one rank: exactly the plan's bytes; ZeRO-3 shards: each rank's delayed
+    // elements carry the layer's CPU/SSD proportion (a shard's share of the
+    // delayed slice is not alpha)
+    u64 late = W == 1 ? scaled_portion(ssd, plan.kind.delay_ratio)
+                      : static_cast<u64>(std::llround(static_cast<double>(ssd) * static_cast<double>(size - e) /
+                                                      static_cast<double>(std::max<u64>(size, 1))));
+    late = std::min(late, size - e);
     u64 now = ssd - late;
     if (now > e) {  // byte rounding at x ~ 0: at most a few bytes move across
       now = e;
