@@ -19,7 +19,8 @@ struct HostAdamHyper {
 // executor's optimizer-state layout), grad fp32, lp_out bf16 (lp_bytes 2) or
 // fp32 (4).  Same arithmetic as the GPU kernel (kernels/elementwise.cu
 // adam_update) and the oracle (gso_adam_step).  Split over the pool's
-// threads in cache-line-aligned blocks.
+// threads in cache-line-aligned blocks; AVX-512 where the CPU has it
+// (bit-identical to the scalar loop, tests/test_host_adam.py).
 void host_adam_step(const HostAdamHyper& hp, int step, float* state, const float* grad, void* lp_out, int lp_bytes,
                     uint64_t n, ThreadPool& pool);
 
