@@ -37,7 +37,14 @@ cudaError_t mm(const Dims& d, int M, int N, int K, const void* A, bool a_k, cons
                KernelProfiler* prof = nullptr) {
   Scope sc(prof, KernelProfiler::Gemm, 2.0 * M * N * K, st);
   GemmArgs g;
-  if (prof && sc.a < 0) g.span = prof->span_slot(2.0 * M * N * K);
+  if (prof) {
+    if (prof->span_on_events < 0) {
+      const char* e = std::getenv("GS_PROF_SPAN_ON_EVENTS");
+      prof->span_on_events = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (prof->span_on_events ? sc.a >= 0 : sc.a < 0)
+      g.span = prof->span_on_events ? prof->span_slot_at(2.0 * M * N * K) : prof->span_slot(2.0 * M * N * K);
+  }
   g.M = M;
   g.N = N;
   g.K = K;
@@ -108,6 +115,28 @@ unsigned long long* KernelProfiler::span_slot(double flops) {
       return nullptr;
     }
     reset();
+  }
+  const size_t i = span_flops.size();
+  if (i >= static_cast<size_t>(kSpanCap)) return nullptr;
+  span_flops.push_back(flops);
+  return span_dev + 2 * i;
+}
+unsigned long long* KernelProfiler::span_slot_at(double flops) {
+  ++span_seen;
+  if (!span_dev) {
+    if (cudaMalloc(&span_dev, 2 * sizeof(unsigned long long) * kSpanCap) != cudaSuccess) {
+      span_dev = nullptr;
+      (void)cudaGetLastError();
+      return nullptr;
+    }
+    // not reset(): this launch's begin event is outstanding
+    std::vector<unsigned long long> init(2 * static_cast<size_t>(kSpanCap));
+    for (size_t i = 0; i < init.size(); i += 2) {
+      init[i] = ~0ULL;
+      init[i + 1] = 0;
+    }
+    cudaMemcpy(span_dev, init.data(), init.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice);
+    span_flops.clear();
   }
   const size_t i = span_flops.size();
   if (i >= static_cast<size_t>(kSpanCap)) return nullptr;

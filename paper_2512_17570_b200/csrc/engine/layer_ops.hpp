@@ -51,6 +51,11 @@ struct KernelProfiler {
   std::vector<double> span_flops;
   long long span_seen = 0;
   unsigned long long* span_slot(double flops);  // nullptr when not sampled
+  // GS_PROF_SPAN_ON_EVENTS=1 (diagnostic): take the span samples on the
+  // event-bracketed launches instead, to split an event-timed duration into
+  // the kernel's own span and the ramp before it.
+  int span_on_events = -1;
+  unsigned long long* span_slot_at(double flops);
   void reset();
   // per class after the stream has completed: sampled flops, sampled ms,
   // sampled launches, all launches
