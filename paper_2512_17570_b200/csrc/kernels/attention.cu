@@ -1,4 +1,3 @@
-#include <cstdlib>
 // Causal multi-head attention of the layer executor (forward with saved
 // log-sum-exp, recompute-based backward).
 //
@@ -151,15 +150,11 @@ __global__ void kv_store_kernel(const float* __restrict__ kv, T* __restrict__ dq
 // (8 bf16 each, 16-byte loads) and L2 = lse * log2(e); the same pass zeroes
 // the fp32 dQ accumulator the kernel reduce-adds into (no separate memset).
 __global__ void fa_prep_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout, const float* __restrict__ lse,
-                               float* __restrict__ D, float* __restrict__ L2, float* __restrict__ dq,
-                               int* __restrict__ dq_cnt, int b, int s, int h, int H) {
+                               float* __restrict__ D, float* __restrict__ L2, float* __restrict__ dq, int b, int s,
+                               int h, int H) {
   pdl_trigger_and_wait();
   const long long rows = (long long)b * H * s;
   const int sub = threadIdx.x & 15;
-  if (dq_cnt)  // per (bh, 64-query block) arrival counters of the fused dQ cast
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < rows / 64;
-         i += (long long)gridDim.x * blockDim.x)
-      dq_cnt[i] = 0;
   for (long long gr = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 4; gr < rows;
        gr += ((long long)gridDim.x * blockDim.x) >> 4) {
     const int bh = (int)(gr / s), t = (int)(gr % s), bi = bh / H, j = bh % H;
@@ -203,9 +198,8 @@ __global__ void dq_store_vec_kernel(const float* __restrict__ dq, bf16* __restri
 }  // namespace
 
 size_t attention_bwd_workspace(int b, int s, int h, int H) {
-  // tcgen05 path: dq fp32 [b*s][h] + D, L2 [b*H*s] + dQ arrival counters
-  // [b*H*s/64];  simt path: dk|dv fp32 [b*s][2h]
-  const size_t fa = sizeof(float) * ((size_t)b * s * h + 2 * (size_t)b * H * s) + sizeof(int) * ((size_t)b * H * s / 64 + 1);
+  // tcgen05 path: dq fp32 [b*s][h] + D, L2 [b*H*s];  simt path: dk|dv fp32 [b*s][2h]
+  const size_t fa = sizeof(float) * ((size_t)b * s * h + 2 * (size_t)b * H * s);
   const size_t simt = sizeof(float) * (size_t)b * s * 2 * h;
   return fa > simt ? fa : simt;
 }
@@ -234,18 +228,12 @@ cudaError_t attention_bwd(DType dt, const void* qkv, const void* o, const float*
     float* D = dq + (size_t)b * s * h;
     float* L2 = D + (size_t)b * H * s;
     const long long rows = (long long)b * H * s;
-    static const bool fused = [] {
-      const char* v = getenv("GS_DQ_FUSED");
-      return !(v && v[0] == '0');
-    }();
-    int* cnt = fused ? reinterpret_cast<int*>(L2 + (size_t)b * H * s) : nullptr;
     count_launch();
     cudaError_t e = launch_pdl(fa_prep_kernel, dim3(grid_for(rows * 16, 256)), dim3(256), 0, st, (const bf16*)o,
-                               (const bf16*)dout, lse, D, L2, dq, cnt, b, s, h, H);
+                               (const bf16*)dout, lse, D, L2, dq, b, s, h, H);
     if (e != cudaSuccess) return e;
-    e = attention_bwd_tc(qkv, dout, lse, L2, D, dqkv, dq, cnt, b, s, h, H, st);
+    e = attention_bwd_tc(qkv, dout, lse, L2, D, dqkv, dq, b, s, h, H, st);
     if (e != cudaSuccess) return e;
-    if (fused) return cudaSuccess;
     count_launch();
     return launch_pdl(dq_store_vec_kernel, dim3(grid_for((long long)b * s * h / 8, 256)), dim3(256), 0, st,
                       (const float*)dq, (bf16*)dqkv, (long long)b * s, h);

@@ -507,49 +507,14 @@ struct FaBwdSmem4 {
   float L[kQS4][kBQb], D[kQS4][kBQb];
   uint64_t kv_full, q_full[kQS4], q_empty[kQS4], s_full[2], ps_full, pds_empty, dq_full[2], dq_empty[2], mma_done;
   uint32_t tmem;
-  int dq_last;
 };
-
-// dQ drain warps (128 threads, r = 0..127), after the reduce-adds of query
-// block qb were issued with `pending` younger bulk groups behind them: wait
-// for qb's groups to complete, release them at GPU scope and count this key
-// block in.  Query block qb (64 queries) has qb / 2 + 1 contributing key
-// blocks (128 keys each, causal); the one that arrives last reads the summed
-// fp32 rows back from L2 and writes the bf16 Q columns of dqkv.  dq_cnt is
-// zeroed by the prologue kernel of the same call.
-__device__ __forceinline__ void dq_arrive(int qb, int pending, int r, int& last_flag, const float* __restrict__ dq_acc,
-                                          int* __restrict__ dq_cnt, bf16* __restrict__ dqkv, int bh, int s, int h,
-                                          int j, int row0) {
-  if (r == 0) {
-    if (pending) asm volatile("cp.async.bulk.wait_group 4;" ::: "memory");
-    else asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    __threadfence();
-    const int old = atomicAdd(dq_cnt + (long long)bh * (s / kBQb) + qb, 1);
-    last_flag = old == qb / 2;
-    __threadfence();
-  }
-  asm volatile("bar.sync 3, 128;" ::: "memory");
-  const bool last = last_flag != 0;
-  asm volatile("bar.sync 3, 128;" ::: "memory");  // last_flag is rewritten by the next arrival
-  if (!last) return;
-  const int c4 = (r & 31) * 4;
-#pragma unroll 4
-  for (int q = r >> 5; q < kBQb; q += 4) {
-    const long long row = row0 + (long long)qb * kBQb + q;
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(dq_acc + row * h + j * kD + c4));
-    __nv_bfloat162 o2[2] = {__floats2bfloat162_rn(v.x, v.y), __floats2bfloat162_rn(v.z, v.w)};
-    *reinterpret_cast<uint2*>(dqkv + row * 3LL * h + j * kD + c4) = *reinterpret_cast<const uint2*>(o2);
-  }
-}
 
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     fa_bwd_tc4_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_q,
                       const __grid_constant__ CUtensorMap map_do, const __grid_constant__ CUtensorMap map_dq,
                       const __grid_constant__ CUtensorMap map_out,
                       const float* __restrict__ lse, const float* __restrict__ Dg, bf16* __restrict__ dqkv, int s,
-                      int h, int H, float scale, long long* __restrict__ tr, const float* __restrict__ dq_acc,
-                      int* __restrict__ dq_cnt) {
+                      int h, int H, float scale, long long* __restrict__ tr) {
   pdl_trigger_and_wait();
   extern __shared__ __align__(1024) uint8_t rawb4[];
   FaBwdSmem4& sm = *reinterpret_cast<FaBwdSmem4*>(rawb4);
@@ -779,12 +744,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
-      // block i-1's reduce-adds are complete once only block i's groups are
-      // pending: count this CTA in; the last key block to contribute casts
-      // the query block's dQ to bf16 (no separate pass over dq_acc)
-      if (dq_cnt && i > 0) dq_arrive(qb0 + i - 1, kBQb / kDqRows4, r, sm.dq_last, dq_acc, dq_cnt, dqkv, bh, s, h, j, row0);
     }
-    if (dq_cnt) dq_arrive(qb0 + nq - 1, 0, r, sm.dq_last, dq_acc, dq_cnt, dqkv, bh, s, h, j, row0);
     if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     bar_wait(&sm.mma_done, 0);
     fence_after();
@@ -919,12 +879,10 @@ cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s,
 }
 
 // dqkv: writes the dK / dV columns; dq_acc (fp32 [b*s][h], zeroed by the
-// caller) receives dQ; D = rowsum(dO * O) per (bh, q).  With dq_cnt (b*H*s/64
-// ints, zeroed by the caller) the kernel also writes dQ's bf16 Q columns of
-// dqkv itself (the last contributing key block per query block); without it
-// the caller converts dq_acc afterwards.
+// caller) receives dQ; D = rowsum(dO * O) per (bh, q).
 cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* lse2, const float* D,
-                             void* dqkv, float* dq_acc, int* dq_cnt, int b, int s, int h, int H, cudaStream_t st) {
+                             void* dqkv,
+                             float* dq_acc, int b, int s, int h, int H, cudaStream_t st) {
   CUtensorMap mq, mq64, md;
   const cuuint32_t elem[2] = {1, 1};
   for (int rows : {128, 64}) {
@@ -976,8 +934,7 @@ cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse
         return cudaErrorInvalidValue;
     }
     cudaError_t le = launch_pdl(fa_bwd_tc4_kernel, dim3(b * H, s / kBK), dim3(kThreadsBwd), smem4, st, mq, mq64, md,
-                                mdq, mout, lse2, D, (bf16*)dqkv, s, h, H, 1.0f / sqrtf((float)kD), tr,
-                                (const float*)dq_acc, dq_cnt);
+                                mdq, mout, lse2, D, (bf16*)dqkv, s, h, H, 1.0f / sqrtf((float)kD), tr);
     if (le != cudaSuccess) return le;
     attn_trace_end(tr, st, b * H * (s / kBK), s / kBK);
     return cudaGetLastError();

@@ -58,7 +58,8 @@ size_t attention_bwd_workspace(int b, int s, int h, int H);
 bool attention_tc_supported(DType dt, int s, int h, int H);
 cudaError_t attention_fwd_tc(const void* qkv, void* o, float* lse, int b, int s, int h, int H, cudaStream_t st);
 cudaError_t attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* lse2, const float* D,
-                             void* dqkv, float* dq_acc, int* dq_cnt, int b, int s, int h, int H, cudaStream_t st);
+                             void* dqkv,
+                             float* dq_acc, int b, int s, int h, int H, cudaStream_t st);
 cudaError_t attention_bwd(DType dt, const void* qkv, const void* o, const float* lse, const void* dout,
                           void* dqkv, void* work, int b, int s, int h, int H, cudaStream_t st);
 
