@@ -130,3 +130,67 @@ def test_fp32_mode_at_gpt1_3b_layer_geometry_holds_north_star_tolerances(tier):
     r = run_both(GEOMS["gpt1.3b"], lp=4, opt_tier=tier)
     assert r["loss"] < 1e-3
     assert r["w"] < 1e-4 and r["fixed"] < 1e-4
+
+
+def _rel_rows(a, b, base=None):
+    """norm-relative distance of two [N][P] float32 stacks (optionally of
+    their deltas from `base`), accumulated per layer in float64 so no
+    full-size float64 temporaries are made."""
+    num = den = 0.0
+    for l in range(len(b)):
+        x = np.asarray(a[l], np.float64)
+        y = np.asarray(b[l], np.float64)
+        if base is not None:
+            z = np.asarray(base[l], np.float64)
+            x, y = x - z, y - z
+        num += float(np.sum((x - y) ** 2))
+        den += float(np.sum(y * y))
+    return (num / den) ** 0.5
+
+
+def test_bench_configuration_matches_fp32_reference():
+    """bench.py's own workload, whole (BASELINE configs[1]: GPT-1.3B, all 24
+    layers, M=16 micro-batches of b=2, s=2048, vertical plan with alpha=0.2,
+    split (1,1,1), optimizer state in pinned DRAM stepped by the host cores,
+    bench's Adam hyper-parameters and seed), two iterations through the
+    product executor in bf16, against the same two iterations of
+    tests/torch_ref.py in fp32 and under torch autocast-bf16 on the same
+    tokens.  Gates as the geometry test above (loss 2e-3; moments and
+    parameter deltas within 1.5x of autocast's own distance from fp32)."""
+    torch = need_gpu()
+    adam = dict(lr=1e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0)
+    g = ob.Geometry(n_layers=24, hidden=2048, heads=16, seq=2048, mb_size=2, vocab=50304)
+    M, iters = 16, 2
+    model = gs.ModelSpec(g.n_layers, g.hidden, g.heads, g.seq, g.mb_size, 2, 4, 3, 1)
+    plan = gs.build_vertical(model, M, gs.StorageSplit(1.0, 1.0, 1.0), 0.2)
+    eng = gs.Engine(plan, model, g.vocab, gs.AdamConfig(**adam), seed=1234, nvme_dir="/tmp", opt_tier=gs.OPT_HOST,
+                    ssd_ring_layers=8)
+    l0, f0 = eng.read_params()
+    toks = np.stack([tr.tokens(g.vocab, g.mb_size, g.seq, M, it) for it in range(iters)])
+    rep = eng.run(toks)
+    eng.flush()
+    l1, f1 = eng.read_params()
+    m, v = eng.read_moments()
+    eng.close()
+    assert np.array_equal(rep.ledger, gs.plan_traffic(plan)), "executed ledger != plan ledger"
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    ref = tr.train(g, adam, l0, f0, toks, device="cuda", dtype="float32")
+    torch.cuda.empty_cache()
+    ours = dict(loss=float(np.max(np.abs(np.array(rep.losses) - ref["losses"]) / ref["losses"])),
+                m=_rel_rows(m, ref["m"]), v=_rel_rows(v, ref["v"]), dw=_rel_rows(l1, ref["layers"], l0),
+                dfixed=rel(f1 - f0, ref["fixed"] - f0))
+    del m, v, l1
+    amp = tr.train(g, adam, l0, f0, toks, device="cuda", dtype="float32", autocast_bf16=True)
+    torch.cuda.empty_cache()
+    t = dict(loss=float(np.max(np.abs(amp["losses"] - ref["losses"]) / ref["losses"])),
+             m=_rel_rows(amp["m"], ref["m"]), v=_rel_rows(amp["v"], ref["v"]),
+             dw=_rel_rows(amp["layers"], ref["layers"], l0), dfixed=rel(amp["fixed"] - f0, ref["fixed"] - f0))
+    print(f"\nbench config (24 layers, M=16): losses {rep.losses} fp32 {ref['losses'].tolist()} "
+          f"autocast {amp['losses'].tolist()} | ours " + " ".join(f"{k}={x:.3e}" for k, x in ours.items()) +
+          " | torch autocast-bf16 " + " ".join(f"{k}={x:.3e}" for k, x in t.items()))
+    bound = lambda k, floor: max(floor, 1.5 * t[k])  # noqa: E731
+    assert ours["loss"] < 2e-3
+    assert ours["m"] < bound("m", 2e-2)
+    assert ours["v"] < bound("v", 4e-2)
+    assert ours["dw"] < bound("dw", 0.15) and ours["dfixed"] < bound("dfixed", 0.15)
