@@ -82,11 +82,17 @@ int KernelProfiler::begin(cudaStream_t st, int cls) {
     }
   }
   const int a = static_cast<int>(next++);
+  if (fence < 0) {
+    const char* e = std::getenv("GS_PROF_FENCE");
+    fence = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (fence) gs::stream_fence(st);
   cudaEventRecord(pool[static_cast<size_t>(a)], st);
   return a;
 }
 void KernelProfiler::end(int cls, double flops, int a, cudaStream_t st) {
   const int b = static_cast<int>(next++);
+  if (fence) gs::stream_fence(st);
   cudaEventRecord(pool[static_cast<size_t>(b)], st);
   recs.push_back({cls, flops, a, b});
 }

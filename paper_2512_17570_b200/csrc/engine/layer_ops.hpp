@@ -55,6 +55,9 @@ struct KernelProfiler {
   // event-bracketed launches instead, to split an event-timed duration into
   // the kernel's own span and the ramp before it.
   int span_on_events = -1;
+  // GS_PROF_FENCE=1 (diagnostic): a no-op non-PDL grid before each event of
+  // a timed pair, so the events mark completions of the work before them
+  int fence = -1;
   unsigned long long* span_slot_at(double flops);
   void reset();
   // per class after the stream has completed: sampled flops, sampled ms,

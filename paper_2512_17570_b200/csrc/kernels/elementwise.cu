@@ -598,6 +598,16 @@ cudaError_t add(DType dt, const void* a, const void* b, void* y, long long n, cu
 }
 cudaError_t fill_zero(void* p, size_t bytes, cudaStream_t s) { return cudaMemsetAsync(p, 0, bytes, s); }
 
+// One-CTA no-op grid launched without the programmatic-serialisation
+// attribute: it starts only once its predecessor grid has fully completed and
+// never triggers its dependents early, so a CUDA event recorded after it
+// marks that completion (the profiler's fence around a timed launch).
+__global__ void stream_fence_kernel() {}
+cudaError_t stream_fence(cudaStream_t s) {
+  stream_fence_kernel<<<1, 32, 0, s>>>();
+  return cudaGetLastError();
+}
+
 __global__ void copy_words_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     dst[i] = src[i];

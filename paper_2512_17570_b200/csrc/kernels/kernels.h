@@ -78,6 +78,8 @@ cudaError_t gelu_bwd(DType dt, const void* u, const void* dg, void* du, long lon
 // y = a + b
 cudaError_t add(DType dt, const void* a, const void* b, void* y, long long n, cudaStream_t s);
 cudaError_t fill_zero(void* p, size_t bytes, cudaStream_t s);
+// no-op grid without PDL: orders an event after its predecessor's completion
+cudaError_t stream_fence(cudaStream_t s);
 // dst[i] = src[i] by SM threads (src may be mapped pinned host memory): a
 // small copy that does not queue behind bulk DMA on the copy engines.
 cudaError_t copy_words(uint32_t* dst, const uint32_t* src, long long n, cudaStream_t s);
