@@ -398,7 +398,7 @@ def run_ours(args):
         comm_id = bytes(idt.cpu().numpy().tobytes())
     eng = gs.Engine(plan, model, V, gs.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0), seed=1234,
                     device=torch.cuda.current_device(), nvme_dir=nvme, opt_tier=tier, profile=True, rank=rank,
-                    world=world, comm_id=comm_id, ssd_ring_layers=ring)
+                    world=world, comm_id=comm_id, ssd_ring_layers=ring, host_threads=args.host_threads)
     K, W = args.steps, args.warmup
     tokens = make_tokens(V, W + 2 * K, M, b, s, seed=7 + rank)
     # warm-up (untimed)
@@ -561,6 +561,8 @@ def main():
     ap.add_argument("--opt-tier", type=int, default=-1, choices=[-1, 0, 1, 2, 3],
                     help="override the config's optimizer tier (" + ", ".join(f"{k} {v}" for k, v in OPT_TIERS.items()) + ")")
     ap.add_argument("--ssd-ring", type=int, default=0, help="override the config's ssd_ring_layers (pinned staging slots)")
+    ap.add_argument("--host-threads", type=int, default=0,
+                    help="host-core optimizer threads per rank (0: hardware threads - 4, split over the node's ranks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--calibrate", type=int, default=1, help="calibrate offsim::simulate from the trace")
     ap.add_argument("--share-gpu", action="store_true",

@@ -1805,6 +1805,7 @@ Executor::KernelTotals Executor::kernel_profile() const {
   KernelTotals t{};
   impl_->prof.totals(t.flops, t.ms, t.launches, t.total);
   impl_->prof.span_totals(&t.span_flops, &t.span_ms, &t.span_launches);
+  if (const char* p = getenv("GS_PROF_DUMP")) impl_->prof.dump_pairs(p);
   return t;
 }
 

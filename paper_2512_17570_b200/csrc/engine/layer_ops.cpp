@@ -1,3 +1,4 @@
+#include <cstdio>
 #include <cstdlib>
 
 #include "layer_ops.hpp"
@@ -180,6 +181,28 @@ void KernelProfiler::span_totals(double* flops, double* ms, int* launches) const
     *ms += static_cast<double>(b - a) * 1e-6;
     ++*launches;
   }
+}
+void KernelProfiler::dump_pairs(const char* path) const {
+  if (span_on_events != 1 || !span_dev) return;
+  std::vector<unsigned long long> h(2 * span_flops.size());
+  if (h.empty() ||
+      cudaMemcpy(h.data(), span_dev, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return;
+  FILE* f = std::fopen(path, "w");
+  if (!f) return;
+  std::fprintf(f, "sample,flops,event_ms,span_ms\n");
+  size_t i = 0;
+  for (const Rec& r : recs) {
+    if (r.cls != Gemm) continue;
+    if (i >= span_flops.size()) break;
+    float t = 0.0f;
+    cudaEventElapsedTime(&t, pool[static_cast<size_t>(r.a)], pool[static_cast<size_t>(r.b)]);
+    const unsigned long long a = h[2 * i], b = h[2 * i + 1];
+    const double sp = (a == ~0ULL || b <= a) ? -1.0 : static_cast<double>(b - a) * 1e-6;
+    std::fprintf(f, "%zu,%.0f,%.4f,%.4f\n", i, r.flops, t, sp);
+    ++i;
+  }
+  std::fclose(f);
 }
 KernelProfiler::~KernelProfiler() {
   for (cudaEvent_t e : pool) cudaEventDestroy(e);

@@ -65,6 +65,9 @@ struct KernelProfiler {
   void totals(double* flops, double* ms, int* launches, long long* total) const;
   // GEMM span samples after the stream has completed
   void span_totals(double* flops, double* ms, int* launches) const;
+  // GS_PROF_SPAN_ON_EVENTS diagnostics: per sampled GEMM launch, flops,
+  // event ms and in-kernel span ms, one CSV line each
+  void dump_pairs(const char* path) const;
   ~KernelProfiler();
 };
 inline const char* const kProfClasses[] = {"gemm", "attention_fwd", "attention_bwd", "layernorm", "other"};
